@@ -1,0 +1,79 @@
+// Internal host-side declarations shared by the translation units of
+// libshiftsolve_b200.so.  Not part of the public ABI (see include/).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/shiftsolve_b200.h"
+
+namespace ss {
+
+// Greedy annihilation plan in device-friendly form: one packed word per
+// rotation (r | c1 << 8 | c2 << 16, 1-based, as schedule.py stores them) and
+// the exclusive prefix of job sizes (step t owns rotations
+// [job_off[t], job_off[t+1])).
+struct Sched {
+    int nr = 0, nc = 0, steps = 0, rots = 0, max_job = 0;
+    std::vector<uint32_t> rot;      // host copy
+    std::vector<int32_t> job_off;   // host copy, steps+1 entries
+    uint32_t* d_rot = nullptr;      // device copies
+    int32_t* d_job_off = nullptr;
+};
+
+// Host greedy schedule (schedule.py:88-159), triplets 1-based.
+int greedy_schedule(int n_rows, int n_cols, std::vector<int64_t>& job,
+                    std::vector<int64_t>& info);
+
+enum Phase { PH_REDUCTION = 0, PH_RQ = 1, PH_BATCHED_GEMM = 2, PH_OUTER_GEMM = 3, PH_TAIL = 4 };
+
+}  // namespace ss
+
+struct ss_handle {
+    int device = 0;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    std::string err;
+    // grow-only device workspace
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    void* ws2 = nullptr;  // second workspace (reduction)
+    size_t ws2_bytes = 0;
+    double* d_scal = nullptr;  // [fro2, trace, scratch...]
+    std::map<std::pair<int, int>, ss::Sched> sched;
+    // accounting
+    int timing = 0;
+    double sec[5] = {0, 0, 0, 0, 0};
+    double flops[5] = {0, 0, 0, 0, 0};
+    int64_t launches = 0;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+};
+
+namespace ss {
+
+int set_err(ss_handle* h, int code, const std::string& msg);
+int cuda_err(ss_handle* h, cudaError_t e, const char* what);
+// Ensure workspace of at least `bytes`; which=0 main, 1 secondary.
+int ensure_ws(ss_handle* h, size_t bytes, int which = 0);
+// Cached device schedule for (nr, nc).
+const Sched* get_sched(ss_handle* h, int nr, int nc);
+
+}  // namespace ss
+
+#define SS_CUDA_TRY(h, expr)                                   \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return ss::cuda_err(h, _e, #expr); \
+    } while (0)
+
+#define SS_LAUNCH_CHECK(h)                                     \
+    do {                                                       \
+        (h)->launches++;                                       \
+        cudaError_t _e = cudaGetLastError();                   \
+        if (_e != cudaSuccess) return ss::cuda_err(h, _e, "kernel launch"); \
+    } while (0)

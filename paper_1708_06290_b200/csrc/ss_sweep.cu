@@ -1,0 +1,764 @@
+// Batched shifted solves on controller-Hessenberg data, sm_100a.
+//
+// Reference path (solvers.py:130-313): for every shift sigma_l the stacked
+// matrix [top; Ahat - sigma_l I] is RQ-factorised bottom-up by a sliding
+// window; only the m "active" transformed columns Z2 are kept per shift and
+// the nb shift-independent panel columns Z1 of Ahat are shared by all
+// shifts.  Per window step (solvers.py:165-200):
+//     block  = [Z1 | Z2_l] rows r0..r0+nb  (lazy -sigma on Ahat's diagonal)
+//     P_l    = first m columns of the block's scheduled Givens RQ factor
+//     Z2_l[0:r0] <- Z2_l[0:r0] P_l[nb:] + Z1[0:r0] P_l[:nb] - sigma_l e P_l[:mnb]
+// then the m x m head is reduced and back-substituted (solvers.py:204-231)
+// and G_l = -Chat X (or x_l = Q X for the reduced solve).
+//
+// B200 mapping ("streamed" path: per-shift window state in HBM/L2):
+//   k_seed      one pass writing Z2 for all shifts of a batch
+//   k_rq        one CTA per shift per step: block packed in shared memory,
+//               greedy-schedule Givens with one warp per rotation, P_l by
+//               reverse accumulation (O(K m) instead of O(K (nb+m)))
+//   k_update    the dominant FP64 kernel: a CTA owns a 64-row tile of the
+//               real panel (staged once in shared memory, reused by every
+//               shift of its group) and streams each shift's Z2 rows through
+//               registers; 2 rows x CC columns complex register tile per
+//               thread, P_l broadcast from shared memory
+//   k_head      one CTA per shift: m x m head RQ fused with the triangular
+//               solve and the -Chat X (or Q X) epilogue; only G / x leave
+//               the device.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+
+using namespace ssd;
+
+namespace {
+
+constexpr int kRows = 64;        // rows per k_update tile (2 per lane)
+constexpr int kUpdThreads = 256;  // 8 warps
+
+struct Dims {
+    int n, m, ptop;
+    int ident_top;  // 1: identity top of height n (reduced solve)
+    const double* A;
+    int64_t lda;
+    const double* T;  // dense top rows (Chat), ptop x n
+    int64_t ldt;
+    const double2* shifts;  // batch-local
+    int sb;                 // shifts in this batch
+    int64_t LDZ;            // leading dim of one Z2 column
+};
+
+__device__ __forceinline__ double panel_val(const Dims& d, int i, int col) {
+    if (i < d.ptop) {
+        if (d.ident_top) return i == col ? 1.0 : 0.0;
+        return d.T[i + (int64_t)col * d.ldt];
+    }
+    return d.A[(i - d.ptop) + (int64_t)col * d.lda];
+}
+
+// ---------------------------------------------------------------------------
+// ||A||_F^2 and trace(A), deterministic two-pass reduction (solvers.py:104-110)
+// ---------------------------------------------------------------------------
+__global__ void k_fro2_trace_part(int n, const double* __restrict__ A, int64_t lda,
+                                  double* __restrict__ part) {
+    __shared__ double sf[32], st[32];
+    double f = 0.0, t = 0.0;
+    for (int j = blockIdx.x; j < n; j += gridDim.x) {
+        const double* col = A + (int64_t)j * lda;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double v = col[i];
+            f = fma(v, v, f);
+        }
+        if (threadIdx.x == 0) t += col[j];
+    }
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = f;
+    if (threadIdx.x == 0) st[0] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ff = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ff += sf[w];
+        part[2 * blockIdx.x] = ff;
+        part[2 * blockIdx.x + 1] = st[0];
+    }
+}
+
+__global__ void k_fro2_trace_final(int nparts, const double* __restrict__ part,
+                                   double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double f = 0.0, t = 0.0;
+        for (int b = 0; b < nparts; ++b) {
+            f += part[2 * b];
+            t += part[2 * b + 1];
+        }
+        out[0] = f;
+        out[1] = t;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// seed (solvers.py:157-163): Z2_l = last m columns of [top; A], -sigma_l on
+// A's diagonal.  Both ping-pong buffers are seeded so rows a step does not
+// rewrite (the still-zero identity rows of the reduced solve) stay valid.
+// ---------------------------------------------------------------------------
+__global__ void k_seed(Dims d, double2* __restrict__ Za, double2* __restrict__ Zb) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    if (i >= d.LDZ) return;
+    const double2 sig = d.shifts[l];
+    for (int c = 0; c < d.m; ++c) {
+        const int col = d.n - d.m + c;
+        double2 v = cz();
+        if (i < d.ptop + d.n) {
+            v.x = panel_val(d, i, col);
+            if (i == d.ptop + col) {
+                v.x -= sig.x;
+                v.y -= sig.y;
+            }
+        }
+        const int64_t idx = ((int64_t)l * d.m + c) * d.LDZ + i;
+        Za[idx] = v;
+        Zb[idx] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-step block RQ: one CTA per shift (solvers.py:170-184, batched.py:64-122)
+// ---------------------------------------------------------------------------
+struct Step {
+    int k, nb, mnb, r0, c0, nc;
+    int steps, rots;
+    const uint32_t* rot;
+    const int32_t* joff;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline size_t rq_smem_bytes(int nb, int m, int steps, int rots) {
+    const int nc = nb + m;
+    size_t b = 0;
+    b += align16((size_t)rots * 4);           // rot
+    b += align16((size_t)(steps + 1) * 4);    // joff
+    b += align16((size_t)rots * 8);           // rc
+    b += align16((size_t)rots * 16);          // rs
+    const int zw = pk_size(nb, m) > nc * m ? pk_size(nb, m) : nc * m;
+    b += (size_t)zw * 16;                     // Zb / W
+    return b;
+}
+
+__global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* __restrict__ Pbuf) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int l = blockIdx.x;
+    const int nb = st.nb, m = d.m, nc = st.nc;
+    size_t off = 0;
+    uint32_t* rot = (uint32_t*)(smem + off);
+    off += align16((size_t)st.rots * 4);
+    int* joff = (int*)(smem + off);
+    off += align16((size_t)(st.steps + 1) * 4);
+    double* rc = (double*)(smem + off);
+    off += align16((size_t)st.rots * 8);
+    double2* rs = (double2*)(smem + off);
+    off += align16((size_t)st.rots * 16);
+    double2* Zb = (double2*)(smem + off);
+
+    for (int u = threadIdx.x; u < st.rots; u += blockDim.x) rot[u] = st.rot[u];
+    for (int u = threadIdx.x; u <= st.steps; u += blockDim.x) joff[u] = st.joff[u];
+
+    // pack the block (solvers.py:174-181); block row t is A-row k-nb+t
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const double2 sig = d.shifts[l];
+    const int arow0 = st.k - nb;
+    for (int col = warp; col < nc; col += nw) {
+        double2* dst = Zb + pk_off(col, nb);
+        const int hgt = pk_height(col, nb);
+        if (col < nb) {
+            const double* src = d.A + arow0 + (int64_t)(st.c0 + col) * d.lda;
+            for (int t = lane; t < hgt; t += 32) {
+                double2 v = make_double2(src[t], 0.0);
+                if (t + m == col) {  // A's main diagonal inside the panel
+                    v.x -= sig.x;
+                    v.y -= sig.y;
+                }
+                dst[t] = v;
+            }
+        } else {
+            const double2* src = Z2 + ((int64_t)l * m + (col - nb)) * d.LDZ + st.r0;
+            for (int t = lane; t < hgt; t += 32) dst[t] = src[t];
+        }
+    }
+    __syncthreads();
+    block_rq_forward(Zb, nb, rot, joff, st.steps, rc, rs);
+    block_rq_reverse(Zb, nc, m, rot, joff, st.steps, rc, rs);  // W aliases the block
+    double2* dstP = Pbuf + (int64_t)l * nc * m;
+    for (int u = threadIdx.x; u < nc * m; u += blockDim.x) dstP[u] = Zb[u];
+}
+
+// ---------------------------------------------------------------------------
+// per-step window update (solvers.py:186-199):
+//   Z2out_l[i] = Z2in_l[i] P_l[nb:nb+m] + Z1[i] P_l[0:nb] - sigma_l P_l[i-(r0-m)]
+// ---------------------------------------------------------------------------
+struct UpdCfg {
+    int rlo;   // first row updated (0, or c0 for the identity top)
+    int SG;    // shifts per CTA
+    int SC;    // shifts staged concurrently
+};
+
+template <int CC>
+__global__ void __launch_bounds__(kUpdThreads)
+    k_update(Dims d, Step st, UpdCfg u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
+             const double2* __restrict__ Pbuf) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nb = st.nb, m = d.m, nc = st.nc, r0 = st.r0;
+    double* Pan = (double*)smem;                                  // [nb][kRows]
+    double2* Pst = (double2*)(smem + align16((size_t)nb * kRows * 8));  // [SC][nc*m]
+    const int i0 = u.rlo + blockIdx.x * kRows;
+    const int l0 = blockIdx.y * u.SG;
+    const int lend = min(l0 + u.SG, d.sb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    for (int v = threadIdx.x; v < nb * kRows; v += blockDim.x) {
+        const int j = v / kRows, ii = v - j * kRows;
+        const int i = i0 + ii;
+        Pan[v] = (i < r0) ? panel_val(d, i, st.c0 + j) : 0.0;
+    }
+    const int ncg = (m + CC - 1) / CC;
+    const int row_a = i0 + lane, row_b = i0 + lane + 32;
+    const bool ok_a = row_a < r0, ok_b = row_b < r0;
+    const int dlo = r0 - m;  // first row receiving the lazy-shift correction
+
+    for (int lc = l0; lc < lend; lc += u.SC) {
+        const int nsc = min(u.SC, lend - lc);
+        __syncthreads();
+        {
+            const double2* src = Pbuf + (int64_t)lc * nc * m;
+            const int tot = nsc * nc * m;
+            for (int v = threadIdx.x; v < tot; v += blockDim.x) Pst[v] = src[v];
+        }
+        __syncthreads();
+        for (int unit = warp; unit < nsc * ncg; unit += kUpdThreads / 32) {
+            const int ls = unit / ncg, g = unit - ls * ncg;
+            const int l = lc + ls;
+            const double2* Pl = Pst + (int64_t)ls * nc * m;
+            const int cb = g * CC;
+            const int ncol = min(CC, m - cb);
+            double2 acc0[CC], acc1[CC];
+#pragma unroll
+            for (int c = 0; c < CC; ++c) acc0[c] = acc1[c] = cz();
+            // Z1 (real panel) part: the shared "outer GEMM"
+            for (int j = 0; j < nb; ++j) {
+                const double a0 = Pan[j * kRows + lane], a1 = Pan[j * kRows + lane + 32];
+#pragma unroll
+                for (int c = 0; c < CC; ++c) {
+                    if (c < ncol) {
+                        const double2 p = Pl[j + (cb + c) * nc];
+                        acc0[c] = rfma(a0, p, acc0[c]);
+                        acc1[c] = rfma(a1, p, acc1[c]);
+                    }
+                }
+            }
+            // Z2 part: the per-shift "batched GEMM"
+            const double2* zin = Zin + (int64_t)l * m * d.LDZ;
+            for (int j = 0; j < m; ++j) {
+                const double2 z0 = ok_a ? zin[(int64_t)j * d.LDZ + row_a] : cz();
+                const double2 z1 = ok_b ? zin[(int64_t)j * d.LDZ + row_b] : cz();
+#pragma unroll
+                for (int c = 0; c < CC; ++c) {
+                    if (c < ncol) {
+                        const double2 p = Pl[nb + j + (cb + c) * nc];
+                        acc0[c] = cfma(z0, p, acc0[c]);
+                        acc1[c] = cfma(z1, p, acc1[c]);
+                    }
+                }
+            }
+            const double2 sig = d.shifts[l];
+            double2* zo = Zout + ((int64_t)l * m + cb) * d.LDZ;
+#pragma unroll
+            for (int c = 0; c < CC; ++c) {
+                if (c < ncol) {
+                    if (ok_a) {
+                        double2 v = acc0[c];
+                        const int dd = row_a - dlo;
+                        if (dd >= 0 && dd < st.mnb) v = csub(v, cmul(sig, Pl[dd + (cb + c) * nc]));
+                        zo[(int64_t)c * d.LDZ + row_a] = v;
+                    }
+                    if (ok_b) {
+                        double2 v = acc1[c];
+                        const int dd = row_b - dlo;
+                        if (dd >= 0 && dd < st.mnb) v = csub(v, cmul(sig, Pl[dd + (cb + c) * nc]));
+                        zo[(int64_t)c * d.LDZ + row_b] = v;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// head (solvers.py:204-231 + :262-268 / :303-310): one CTA per shift.
+// Warp 0 reduces the m x m head with the reference's rotation order,
+// accumulating the rotations in Qh (m x m) instead of rotating every top
+// row; the fused back-substitution gives X; then the epilogue applies
+// top rows x (Qh X) with all warps.
+// ---------------------------------------------------------------------------
+struct HeadOut {
+    int mode;          // 0 transfer function, 1 reduced solve
+    const double* B;   // Bhat, read [0:m, 0:m]
+    int64_t ldb;
+    const double2* bd; // reduced: b_dirs (batch-local), m x sb
+    int64_t ldbd;
+    double rtol;
+    const double* scal;  // [fro2, trace]
+    double2* out;        // tf: G (batch-local, column l*m); reduced: X (batch-local)
+    int64_t ldo;
+    int32_t* fail;       // batch-local
+};
+
+__global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int m = d.m, l = blockIdx.x;
+    const int q = h.mode == 0 ? m : 1;
+    double2* Hh = (double2*)smem;  // m x m, col-major
+    double2* Qh = Hh + m * m;      // m x m
+    double2* X = Qh + m * m;       // m x q
+    __shared__ int s_fail;
+    const double2* zl = Z2 + (int64_t)l * m * d.LDZ;
+    for (int u = threadIdx.x; u < m * m; u += blockDim.x) {
+        const int c = u / m, r = u - c * m;
+        Hh[u] = zl[(int64_t)c * d.LDZ + d.ptop + r];
+        Qh[u] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    }
+    // right-hand side: Bhat[0:m,0:m] (tf) or Bhat[0:m,0:m] b_l (reduced)
+    for (int u = threadIdx.x; u < m * q; u += blockDim.x) {
+        const int c = u / m, r = u - c * m;
+        double2 v;
+        if (h.mode == 0) {
+            v = make_double2(h.B[r + (int64_t)c * h.ldb], 0.0);
+        } else {
+            v = cz();
+            for (int j = 0; j < m; ++j)
+                v = rfma(h.B[r + (int64_t)j * h.ldb], h.bd[j + (int64_t)l * h.ldbd], v);
+        }
+        X[u] = v;  // holds rhs until row r is solved
+    }
+    if (threadIdx.x == 0) s_fail = -1;
+    __syncthreads();
+
+    const double2 sig = d.shifts[l];
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const double fro2 = h.scal[0], tr = h.scal[1];
+        const double sc2 = fro2 - 2.0 * (sig.x * tr) + (sig.x * sig.x + sig.y * sig.y) * d.n;
+        const double tol = h.rtol * sqrt(sc2 > 0.0 ? sc2 : 0.0);
+        int fail = -1;
+        for (int i = m - 1; i >= 0; --i) {
+            for (int jj = 0; jj < i; ++jj) {
+                const double2 a = Hh[i + i * m], b = Hh[i + jj * m];
+                double c;
+                double2 s, rho;
+                givens(a, b, c, s, rho);
+                for (int r = lane; r < m; r += 32) {
+                    if (r != i) {
+                        double2 hh = Hh[r + i * m], tt = Hh[r + jj * m];
+                        rot_apply(c, s, hh, tt);
+                        Hh[r + i * m] = hh;
+                        Hh[r + jj * m] = tt;
+                    }
+                    double2 qa = Qh[r + i * m], qb = Qh[r + jj * m];
+                    rot_apply(c, s, qa, qb);
+                    Qh[r + i * m] = qa;
+                    Qh[r + jj * m] = qb;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    Hh[i + jj * m] = cz();
+                    Hh[i + i * m] = rho;
+                }
+                __syncwarp();
+            }
+            const double2 piv = Hh[i + i * m];
+            if (cabsd(piv) <= tol) {
+                fail = i;
+                break;
+            }
+            for (int c = lane; c < q; c += 32) {
+                double2 acc = cz();
+                for (int j = i + 1; j < m; ++j) acc = cfma(Hh[i + j * m], X[j + c * m], acc);
+                X[i + c * m] = cdiv(csub(X[i + c * m], acc), piv);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_fail = fail;
+    }
+    __syncthreads();
+    const int fail = s_fail;
+    if (fail >= 0) {
+        const double qn = __longlong_as_double(0x7ff8000000000000ULL);
+        if (h.mode == 0) {
+            for (int u = threadIdx.x; u < d.ptop * m; u += blockDim.x) {
+                const int c = u / d.ptop, i = u - c * d.ptop;
+                h.out[i + ((int64_t)l * m + c) * h.ldo] = make_double2(qn, qn);
+            }
+        } else {
+            for (int i = threadIdx.x; i < d.n; i += blockDim.x)
+                h.out[i + (int64_t)l * h.ldo] = make_double2(qn, qn);
+        }
+        if (threadIdx.x == 0) h.fail[l] = fail;
+        return;
+    }
+    // V = Qh X  (m x q), stored over Hh
+    for (int u = threadIdx.x; u < m * q; u += blockDim.x) {
+        const int c = u / m, r = u - c * m;
+        double2 acc = cz();
+        for (int j = 0; j < m; ++j) acc = cfma(Qh[r + j * m], X[j + c * m], acc);
+        Hh[u] = acc;
+    }
+    __syncthreads();
+    const double2* V = Hh;
+    if (h.mode == 0) {
+        // G_l = -(top rows) V   (p x m)
+        for (int u = threadIdx.x; u < d.ptop * m; u += blockDim.x) {
+            const int c = u / d.ptop, i = u - c * d.ptop;
+            double2 acc = cz();
+            for (int j = 0; j < m; ++j) acc = cfma(zl[(int64_t)j * d.LDZ + i], V[j + c * m], acc);
+            h.out[i + ((int64_t)l * m + c) * h.ldo] = make_double2(-acc.x, -acc.y);
+        }
+    } else {
+        for (int i = threadIdx.x; i < d.n; i += blockDim.x) {
+            double2 acc = cz();
+            for (int j = 0; j < m; ++j) acc = cfma(zl[(int64_t)j * d.LDZ + i], V[j], acc);
+            h.out[i + (int64_t)l * h.ldo] = acc;
+        }
+    }
+    if (threadIdx.x == 0) h.fail[l] = -1;
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+template <int CC>
+int launch_update_cc(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const Dims& d,
+                     const Step& s, const UpdCfg& u, const double2* zin, double2* zout,
+                     const double2* pbuf) {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && configured < smem) {
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_update<CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)h->smem_optin));
+        configured = h->smem_optin;
+    }
+    k_update<CC><<<grid, kUpdThreads, smem, st>>>(d, s, u, zin, zout, pbuf);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+int launch_update(ss_handle* h, int CC, dim3 grid, size_t smem, cudaStream_t st, const Dims& d,
+                  const Step& s, const UpdCfg& u, const double2* zin, double2* zout,
+                  const double2* pbuf) {
+    switch (CC) {
+#define SS_CASE(K) \
+    case K: return launch_update_cc<K>(h, grid, smem, st, d, s, u, zin, zout, pbuf);
+        SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6)
+        SS_CASE(7) SS_CASE(8) SS_CASE(9) SS_CASE(10) SS_CASE(11) SS_CASE(12)
+#undef SS_CASE
+        default: return ss::set_err(h, SS_EARG, "unsupported column tile");
+    }
+}
+
+// columns per thread tile: m itself when small, else a divisor in [8, 12]
+int pick_cc(int m) {
+    if (m <= 12) return m;
+    for (int c = 12; c >= 8; --c)
+        if (m % c == 0) return c;
+    return 10;
+}
+
+struct Timer {
+    ss_handle* h;
+    cudaStream_t st;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+    cudaEvent_t pending = nullptr;
+    int phase = -1;
+    void begin(int ph) {
+        if (!h->timing) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        pending = e;
+        phase = ph;
+    }
+    void end() {
+        if (!h->timing || !pending) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        rec.push_back({phase, {pending, e}});
+        pending = nullptr;
+    }
+    void flush() {
+        if (!h->timing) return;
+        cudaStreamSynchronize(st);
+        for (auto& r : rec) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.second.first, r.second.second);
+            h->sec[r.first] += ms * 1e-3;
+            cudaEventDestroy(r.second.first);
+            cudaEventDestroy(r.second.second);
+        }
+        rec.clear();
+    }
+};
+
+int max_nb_for(ss_handle* h, int m, int nb_req) {
+    int nb = nb_req;
+    while (nb > 1) {
+        const size_t need = rq_smem_bytes(nb, m, nb * m, nb * m);
+        const size_t upd = align16((size_t)nb * kRows * 8) + (size_t)(nb + m) * m * 16;
+        if (need <= h->smem_optin && upd <= h->smem_optin && nb + m <= 255) break;
+        nb = nb > 8 ? nb - 8 : nb - 1;
+    }
+    return nb < 1 ? 1 : nb;
+}
+
+struct SweepArgs {
+    int mode;  // 0 tf, 1 reduced
+    int n, m, p;
+    const double* A;
+    int64_t lda;
+    const double* B;
+    int64_t ldb;
+    const double* C;
+    int64_t ldc;
+    const double2* shifts;
+    int64_t s;
+    const double2* bd;
+    int64_t ldbd;
+    int nb;
+    int64_t batch;
+    double rtol;
+    double2* out;
+    int64_t ldo;
+    int32_t* fail;
+};
+
+int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
+    const int n = a.n, m = a.m;
+    const int ptop = a.mode == 0 ? a.p : n;
+    if (a.s == 0) return SS_OK;
+    SS_CUDA_TRY(h, cudaSetDevice(h->device));
+    const double rtol = a.rtol > 0.0 ? a.rtol : 1e3 * n * 2.220446049250313e-16;
+    const int nb0 = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
+    const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
+
+    Timer tm{h, st};
+    // fro2 / trace for the per-shift singularity thresholds
+    {
+        const int parts = std::min(4 * h->num_sms, std::max(n, 1));
+        int rc = ss::ensure_ws(h, 1 << 20, 1);  // scratch for partial sums
+        if (rc) return rc;
+        double* part = (double*)h->ws2;
+        if (parts * 2 * sizeof(double) > h->ws2_bytes) return ss::set_err(h, SS_EARG, "scratch");
+        k_fro2_trace_part<<<parts, 256, 0, st>>>(n, a.A, a.lda, part);
+        SS_LAUNCH_CHECK(h);
+        k_fro2_trace_final<<<1, 32, 0, st>>>(parts, part, h->d_scal);
+        SS_LAUNCH_CHECK(h);
+    }
+
+    // batch size from memory: 2 window buffers + P per shift
+    const int ncmax = nb0 + m;
+    const size_t per_shift = 2 * (size_t)LDZ * m * 16 + (size_t)ncmax * m * 16 + 64;
+    int64_t sb_max = a.batch > 0 ? a.batch : a.s;
+    {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const size_t cap = std::max<size_t>(fr / 2 + h->ws_bytes / 2, per_shift);
+        sb_max = std::min<int64_t>(sb_max, (int64_t)(cap / per_shift));
+        sb_max = std::max<int64_t>(sb_max, 1);
+    }
+    sb_max = std::min<int64_t>(sb_max, a.s);
+    {
+        int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256, 0);
+        if (rc) return rc;
+    }
+    double2* Zbuf[2];
+    Zbuf[0] = (double2*)h->ws;
+    Zbuf[1] = Zbuf[0] + (size_t)sb_max * m * LDZ;
+    double2* Pbuf = Zbuf[1] + (size_t)sb_max * m * LDZ;
+
+    const int CC = pick_cc(m);
+    const int ncg = (m + CC - 1) / CC;
+    const int rq_threads = m <= 16 ? 256 : 512;
+
+    static bool rq_attr = false;
+    if (!rq_attr) {
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_rq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)h->smem_optin));
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)h->smem_optin));
+        rq_attr = true;
+    }
+
+    for (int64_t lo = 0; lo < a.s; lo += sb_max) {
+        const int sb = (int)std::min<int64_t>(sb_max, a.s - lo);
+        Dims d;
+        d.n = n;
+        d.m = m;
+        d.ptop = ptop;
+        d.ident_top = a.mode == 1;
+        d.A = a.A;
+        d.lda = a.lda;
+        d.T = a.C;
+        d.ldt = a.ldc;
+        d.shifts = a.shifts + lo;
+        d.sb = sb;
+        d.LDZ = LDZ;
+        {
+            dim3 g((unsigned)((LDZ + 255) / 256), (unsigned)sb);
+            k_seed<<<g, 256, 0, st>>>(d, Zbuf[0], Zbuf[1]);
+            SS_LAUNCH_CHECK(h);
+        }
+        int cur = 0;
+        int k = n;
+        while (k >= m + 1) {
+            Step s;
+            s.k = k;
+            s.nb = std::min(nb0, k - m);
+            s.mnb = std::min(m, s.nb);
+            s.r0 = ptop + k - s.nb;
+            s.c0 = k - m - s.nb;
+            s.nc = s.nb + m;
+            const ss::Sched* sc = ss::get_sched(h, s.nb, s.nc);
+            if (!sc) return ss::set_err(h, SS_ENOMEM, "schedule allocation failed");
+            s.steps = sc->steps;
+            s.rots = sc->rots;
+            s.rot = sc->d_rot;
+            s.joff = sc->d_job_off;
+            // block RQ
+            tm.begin(ss::PH_RQ);
+            const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
+            k_rq<<<sb, rq_threads, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            SS_LAUNCH_CHECK(h);
+            tm.end();
+            // window update
+            UpdCfg u;
+            u.rlo = a.mode == 1 ? s.c0 : 0;
+            u.SC = std::max(1, (kUpdThreads / 32) / ncg);
+            const size_t pst = (size_t)s.nc * m * 16;
+            while (u.SC > 1 && align16((size_t)s.nb * kRows * 8) + u.SC * pst > 96 * 1024) u.SC--;
+            u.SG = u.SC * 2;
+            const int rows = s.r0 - u.rlo;
+            dim3 g((unsigned)((rows + kRows - 1) / kRows), (unsigned)((sb + u.SG - 1) / u.SG));
+            const size_t smem_u = align16((size_t)s.nb * kRows * 8) + u.SC * pst;
+            tm.begin(ss::PH_OUTER_GEMM);
+            int rc = launch_update(h, CC, g, smem_u, st, d, s, u, Zbuf[cur], Zbuf[cur ^ 1], Pbuf);
+            if (rc) return rc;
+            tm.end();
+            // reference flop accounting (batched.py:58-61, solvers.py:194-199)
+            double rq_fl = 0.0;
+            for (int qq = 0; qq < sc->rots; ++qq)
+                rq_fl += 20.0 * ((sc->rot[qq] & 0xffu) + s.nc) + 16.0;
+            h->flops[ss::PH_RQ] += rq_fl * sb;
+            h->flops[ss::PH_BATCHED_GEMM] += (double)sb * (8.0 * s.r0 * m * m + 8.0 * s.mnb * m);
+            h->flops[ss::PH_OUTER_GEMM] += 8.0 * s.r0 * ((double)sb * m) * s.nb;
+            cur ^= 1;
+            k -= s.nb;
+        }
+        HeadOut ho;
+        ho.mode = a.mode;
+        ho.B = a.B;
+        ho.ldb = a.ldb;
+        ho.bd = a.bd ? a.bd + lo * a.ldbd : nullptr;
+        ho.ldbd = a.ldbd;
+        ho.rtol = rtol;
+        ho.scal = h->d_scal;
+        ho.out = a.mode == 0 ? a.out + lo * m * a.ldo : a.out + lo * a.ldo;
+        ho.ldo = a.ldo;
+        ho.fail = a.fail + lo;
+        tm.begin(ss::PH_TAIL);
+        const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
+        k_head<<<sb, 128, smem_h, st>>>(d, ho, Zbuf[cur]);
+        SS_LAUNCH_CHECK(h);
+        tm.end();
+        h->flops[ss::PH_TAIL] += a.mode == 0 ? (double)sb * 8.0 * a.p * m * m : (double)sb * 8.0 * n * m;
+    }
+    tm.flush();
+    return SS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ss_tf_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t lda,
+               const double* Bhat, int64_t ldb, const double* Chat, int64_t ldc,
+               const double* shifts, int64_t s, int nb, int64_t batch, double rtol, double* G,
+               int64_t ldg, int32_t* fail_row, void* stream) {
+    if (!h) return SS_EARG;
+    if (n < 1 || m < 1 || m > n || p < 0 || s < 0)
+        return ss::set_err(h, SS_EDIM, "inconsistent controller-Hessenberg form");
+    if (lda < n || ldb < m || (p > 0 && ldc < p) || (p > 0 && ldg < p))
+        return ss::set_err(h, SS_EDIM, "leading dimension too small");
+    if (nb < 1) return ss::set_err(h, SS_EARG, "window block size must be >= 1");
+    if (s > 0 && (!Ahat || !Bhat || !shifts || !fail_row || (p > 0 && (!Chat || !G))))
+        return ss::set_err(h, SS_EARG, "null pointer");
+    SweepArgs a{};
+    a.mode = 0;
+    a.n = n;
+    a.m = m;
+    a.p = p;
+    a.A = Ahat;
+    a.lda = lda;
+    a.B = Bhat;
+    a.ldb = ldb;
+    a.C = Chat;
+    a.ldc = ldc > 0 ? ldc : 1;
+    a.shifts = (const double2*)shifts;
+    a.s = s;
+    a.bd = nullptr;
+    a.ldbd = 0;
+    a.nb = nb;
+    a.batch = batch;
+    a.rtol = rtol;
+    a.out = (double2*)G;
+    a.ldo = ldg > 0 ? ldg : 1;
+    a.fail = fail_row;
+    return run_sweep(h, a, (cudaStream_t)stream);
+}
+
+int ss_solve_reduced(ss_handle* h, int n, int m, const double* Ahat, int64_t lda,
+                     const double* Bhat, int64_t ldb, const double* shifts, int64_t s,
+                     const double* bdirs, int64_t ldbd, int nb, int64_t batch, double rtol,
+                     double* X, int64_t ldx, int32_t* fail_row, void* stream) {
+    if (!h) return SS_EARG;
+    if (n < 1 || m < 1 || m > n || s < 0)
+        return ss::set_err(h, SS_EDIM, "inconsistent controller-Hessenberg form");
+    if (lda < n || ldb < m || ldbd < m || ldx < n)
+        return ss::set_err(h, SS_EDIM, "leading dimension too small");
+    if (nb < 1) return ss::set_err(h, SS_EARG, "window block size must be >= 1");
+    if (s > 0 && (!Ahat || !Bhat || !shifts || !bdirs || !X || !fail_row))
+        return ss::set_err(h, SS_EARG, "null pointer");
+    SweepArgs a{};
+    a.mode = 1;
+    a.n = n;
+    a.m = m;
+    a.p = 0;
+    a.A = Ahat;
+    a.lda = lda;
+    a.B = Bhat;
+    a.ldb = ldb;
+    a.C = nullptr;
+    a.ldc = 1;
+    a.shifts = (const double2*)shifts;
+    a.s = s;
+    a.bd = (const double2*)bdirs;
+    a.ldbd = ldbd;
+    a.nb = nb;
+    a.batch = batch;
+    a.rtol = rtol;
+    a.out = (double2*)X;
+    a.ldo = ldx;
+    a.fail = fail_row;
+    return run_sweep(h, a, (cudaStream_t)stream);
+}
+
+}  // extern "C"

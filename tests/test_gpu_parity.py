@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, the
+reference's golden vectors and the independent LU oracle.
+
+Tolerances (north_star): ||G_gpu - G_ref|| / ||G_ref|| <= 1e-10 per shift
+(FP64), tighter where the reference tests are tighter; parameter invariance
+<= 1e-12; batch composition / failure isolation bitwise.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bounded_shifts, golden, probe_shifts
+
+import paper_1708_06290_b200 as ss
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(float).eps
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def per_shift_rel(G, Gr, m, s):
+    return max(rel(G[:, l * m:(l + 1) * m], Gr[:, l * m:(l + 1) * m]) for l in range(s))
+
+
+def chf_of(S, pre, suffix=""):
+    n, m, p = (int(v) for v in S[pre + "dims"][:3])
+    return ss.ControllerHessForm(Ahat=S[pre + "Ahat" + suffix], Bhat=S[pre + "Bhat" + suffix],
+                                 Chat=S[pre + "Chat" + suffix], m=m, n=n, p=p)
+
+
+# --------------------------------------------------------------------------
+# transfer function
+# --------------------------------------------------------------------------
+
+def test_scalar_resolvent_exact():
+    """test_solvers.py:32-40 known answer, 4 eps."""
+    chf = ss.ControllerHessForm(Ahat=np.array([[1.5]]), Bhat=np.array([[2.0]]),
+                                Chat=np.array([[3.0]]), m=1, n=1, p=1)
+    sigma = 2.0 + 0.5j
+    res = ss.eval_transfer_function(chf, [sigma], nb=4)
+    expect = 3.0 * 2.0 / (sigma - 1.5)
+    assert abs(res.G[0, 0] - expect) <= 4 * EPS * abs(expect)
+
+
+@pytest.mark.parametrize("case", range(17))
+def test_golden_systems_tf_and_reduced(case):
+    S = golden("systems.npz")
+    pre = f"s{case}_"
+    n, m, p, seed, nb = (int(v) for v in S[pre + "dims"])
+    chf = chf_of(S, pre)
+    shifts = S[pre + "shifts"]
+    s = len(shifts)
+    res = ss.eval_transfer_function(chf, shifts, nb=nb)
+    assert res.failures == {}
+    assert per_shift_rel(res.G, S[pre + "G"], m, s) <= 1e-10      # vs reference
+    assert per_shift_rel(res.G, S[pre + "Glu"], m, s) <= 1e-10    # vs LU oracle (orig triple)
+    Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts, nb=nb)
+    assert per_shift_rel(res.G, Go, m, s) <= 1e-11                 # vs C oracle
+    red = ss.solve_shifted_reduced(chf, shifts, S[pre + "bdirs"], nb=nb)
+    assert red.failures == {}
+    for l in range(s):
+        assert rel(red.x[:, l], S[pre + "x"][:, l]) <= 1e-10
+        assert rel(red.x[:, l], S[pre + "xlu"][:, l]) <= 1e-10
+
+
+def test_criterion4_corpus_vs_lu():
+    """test_acceptance.py:130-163 style: random systems, 16 bounded-condition
+    shifts each, nb in {4, 8, 16}: tf and reduced <= 1e-10 vs dense LU."""
+    rng = np.random.default_rng(7)
+    worst_tf = worst_red = 0.0
+    for case in range(40):
+        n = int(rng.integers(4, 65))
+        m = int(rng.integers(1, min(4, n - 1) + 1))
+        p = int(rng.integers(1, 5))
+        sysb = ss.random_stable_system(n, m, p, seed=20_000 + case, circular=False)
+        chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+        shifts = bounded_shifts(rng, chf.Ahat, 16)
+        nb = int(rng.choice([4, 8, 16]))
+        res = ss.eval_transfer_function(chf, shifts, nb=nb)
+        bd = rng.standard_normal((m, 16)) + 1j * rng.standard_normal((m, 16))
+        red = ss.solve_shifted_reduced(chf, shifts, bd, nb=nb)
+        for l, sig in enumerate(shifts):
+            Go = O.oracle_transfer_function(sysb.A, sysb.B, sysb.C, sig)
+            worst_tf = max(worst_tf, rel(res.value(l), Go))
+            xo = O.lu_solve_shifted(chf.Ahat, sig, chf.Bhat @ bd[:, l])
+            worst_red = max(worst_red, rel(red.x[:, l], xo))
+    assert worst_tf <= 1e-10 and worst_red <= 1e-10, (worst_tf, worst_red)
+
+
+def test_parameter_invariance(rng):
+    """test_solvers.py:52-59 / test_acceptance.py:166-199: nb and batch size."""
+    sysb = ss.random_stable_system(48, 3, 2, seed=5, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    shifts = bounded_shifts(rng, chf.Ahat, 10)
+    ref = ss.eval_transfer_function(chf, shifts, nb=6).G
+    for nb in (3, 6, 8, 32, 64):
+        for bs in (1, 4, None):
+            G = ss.eval_transfer_function(chf, shifts, nb=nb, batch_size=bs).G
+            assert np.abs(G - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_batch_composition_bitwise(rng):
+    """Each shift is computed in isolation: any subset / batch size gives
+    bitwise identical slices (reference solvers.py:25-28)."""
+    sysb = ss.random_stable_system(80, 4, 3, seed=9, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=16)
+    shifts = probe_shifts(rng, 20, scale=5.0)
+    full = ss.eval_transfer_function(chf, shifts, nb=16).G
+    part = ss.eval_transfer_function(chf, shifts[5:12], nb=16).G
+    assert np.array_equal(part, full[:, 5 * 4:12 * 4])
+    b3 = ss.eval_transfer_function(chf, shifts, nb=16, batch_size=3).G
+    assert np.array_equal(b3, full)
+
+
+def test_failure_isolation_bitwise():
+    """test_acceptance.py:311-339 with the reference's own failure case."""
+    F = golden("failure.npz")
+    chf = ss.ControllerHessForm(Ahat=F["Ahat"], Bhat=F["Bhat"], Chat=F["Chat"], m=2, n=24, p=2)
+    full = F["shifts"]
+    marked = ss.eval_transfer_function(chf, full, nb=8, on_singular="mark")
+    assert marked.failures == {7: 0}
+    assert np.isnan(marked.value(7)).all()
+    keep = [i for i in range(16) if i != 7]
+    clean = ss.eval_transfer_function(chf, full[keep], nb=8)
+    for lc, li in enumerate(keep):
+        assert np.array_equal(marked.value(li), clean.value(lc))
+    ok = ~np.isnan(F["G"])
+    assert np.abs(marked.G[ok] - F["G"][ok]).max() <= 1e-10 * np.abs(F["G"][ok]).max()
+    with pytest.raises(ss.SingularShiftError) as ei:
+        ss.eval_transfer_function(chf, full, nb=8)
+    assert ei.value.failures == [(7, 0)]
+    redm = ss.solve_shifted_reduced(chf, full, F["bdirs"], nb=8, on_singular="mark")
+    assert redm.failures == {int(a): int(b) for a, b in F["rfailures"]}
+    assert np.isnan(redm.x[:, 7]).all()
+
+
+def test_singular_shift_raises_by_default():
+    sysb = ss.random_stable_system(16, 2, 2, seed=8, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    ev = np.linalg.eigvals(chf.Ahat)[0]
+    with pytest.raises(ss.SingularShiftError):
+        ss.eval_transfer_function(chf, [ev], nb=4)
+
+
+def test_result_slicing():
+    sysb = ss.random_stable_system(12, 2, 2, seed=0, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    res = ss.eval_transfer_function(chf, [1j, 2j], nb=4)
+    assert res.value(1).shape == (2, 2)
+    assert np.array_equal(res.value(0), res.G[:, :2])
+
+
+def test_counters_populated():
+    sysb = ss.random_stable_system(20, 2, 2, seed=17, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    c = ss.PhaseCounters()
+    ss.eval_transfer_function(chf, [1j, 2j], nb=4, counter=c)
+    snap = c.snapshot()
+    for ph in ("small_batched_rq", "outer_gemm", "tail_solves", "batched_gemm"):
+        assert snap[ph][0] > 0 and snap[ph][1] > 0
+
+
+def test_config1_full_vs_reference():
+    """BASELINE configs[0] end to end: GPU reduction + GPU sweep vs the
+    reference's G (CPU reduction + CPU sweep) on the same seeded input."""
+    g = golden("config1.npz")
+    n, m, p = (int(v) for v in g["dims"])
+    sysb = ss.random_stable_system(n, m, p, seed=int(g["seed"]), circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=64)
+    res = ss.eval_transfer_function(chf, g["shifts"], nb=32)
+    assert res.failures == {}
+    assert per_shift_rel(res.G, g["G"], m, 100) <= 1e-10
+    for k, l in enumerate(g["lu_idx"]):
+        assert rel(res.value(int(l)), g["Glu"][:, k * m:(k + 1) * m]) <= 1e-10
+
+
+def test_device_resident_inputs_stay_on_device():
+    sysb = ss.random_stable_system(64, 3, 2, seed=4, circular=False)
+    chf = ss.reduce_controller_hessenberg(torch.tensor(sysb.A, device="cuda"),
+                                          torch.tensor(sysb.B, device="cuda"),
+                                          torch.tensor(sysb.C, device="cuda"), block_size=16)
+    assert isinstance(chf.Ahat, torch.Tensor) and chf.Ahat.is_cuda
+    sh = torch.tensor(1j * np.linspace(1, 5, 9), device="cuda")
+    res = ss.eval_transfer_function(chf, sh, nb=16)
+    assert isinstance(res.G, torch.Tensor) and res.G.is_cuda
+    Gh = ss.eval_transfer_function(chf.numpy(), sh.cpu().numpy(), nb=16).G
+    assert np.array_equal(res.G.cpu().numpy(), Gh)
+
+
+# --------------------------------------------------------------------------
+# reduced solves
+# --------------------------------------------------------------------------
+
+def test_reduced_triangular_back_substitution(rng):
+    """test_solvers.py:89-106."""
+    n, m = 8, 2
+    Ahat = np.asfortranarray(np.triu(rng.standard_normal((n, n))) + 4 * np.eye(n))
+    Bhat = np.zeros((n, m), order="F")
+    Bhat[:m, :m] = np.triu(rng.standard_normal((m, m))) + 2 * np.eye(m)
+    chf = ss.ControllerHessForm(Ahat=Ahat, Bhat=Bhat, Chat=np.zeros((1, n), order="F"), m=m, n=n, p=1)
+    sigma = 0.3 + 0.2j
+    bdir = np.zeros((m, 1), dtype=complex)
+    bdir[0, 0] = 1.0
+    res = ss.solve_shifted_reduced(chf, [sigma], bdir, nb=4)
+    M = Ahat - sigma * np.eye(n)
+    rhs = (Bhat @ bdir[:, 0]).astype(complex)
+    x = np.zeros(n, dtype=complex)
+    for i in range(n - 1, -1, -1):
+        x[i] = (rhs[i] - M[i, i + 1:] @ x[i + 1:]) / M[i, i]
+    assert np.linalg.norm(res.x[:, 0] - x) <= 1e-12 * np.linalg.norm(x)
+
+
+def test_reduced_zero_shift_and_certificate(rng):
+    sysb = ss.random_stable_system(32, 2, 2, seed=7, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    bdir = rng.standard_normal((2, 1)) + 0j
+    res = ss.solve_shifted_reduced(chf, [0.0], bdir, nb=8)
+    xo = O.lu_solve_shifted(chf.Ahat, 0.0, chf.Bhat @ bdir[:, 0])
+    assert rel(res.x[:, 0], xo) <= 1e-10
+    shifts = probe_shifts(rng, 4, scale=2.0)
+    bdirs = rng.standard_normal((2, 4)) + 0j
+    res = ss.solve_shifted_reduced(chf, shifts, bdirs, nb=8)
+    for l, sigma in enumerate(shifts):
+        rhs = (chf.Bhat @ bdirs[:, l]).astype(complex)
+        cert = ss.residual_certificate(chf, sigma, res.x[:, l], rhs)
+        assert cert <= 1e3 * chf.n * EPS
+
+
+# --------------------------------------------------------------------------
+# pseudospectrum grid
+# --------------------------------------------------------------------------
+
+def test_pseudospectrum_siso_and_inf(rng):
+    sysb = ss.random_stable_system(12, 1, 1, seed=21, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    pts = probe_shifts(rng, 4, scale=2.0)
+    vals = ss.structured_pseudospectrum_grid(chf, pts, nb=4)
+    res = ss.eval_transfer_function(chf, pts, nb=4)
+    assert np.allclose(vals, np.abs(res.G[0, :]), atol=1e-13 * np.abs(res.G).max())
+    ev = np.linalg.eigvals(chf.Ahat)
+    bad = ev[np.argmax(np.abs(ev.imag))]
+    v2 = ss.structured_pseudospectrum_grid(chf, [bad, 1.0 + 1.0j], nb=4)
+    assert np.isinf(v2[0]) and np.isfinite(v2[1])
+
+
+def test_pseudospectrum_mimo_svd_and_symmetry(rng):
+    n, m, p = 5, 2, 2
+    Qb, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = Qb @ np.diag([-1.0, -2.0, -3.0, -4.0, -5.0]) @ Qb.T
+    B = rng.standard_normal((n, m))
+    C = rng.standard_normal((p, n))
+    chf = ss.reduce_controller_hessenberg(A, B, C, block_size=2)
+    pts = np.array([0.5 + 0.5j, -1.5 + 2j, 3.0 - 1j])
+    vals = ss.structured_pseudospectrum_grid(chf, pts, nb=2)
+    for z, v in zip(pts, vals):
+        Gz = O.oracle_transfer_function(A, B, C, z)
+        assert abs(v - np.linalg.svd(Gz, compute_uv=False)[0]) <= 1e-10 * max(v, 1.0)
+    sysb = ss.random_stable_system(14, 2, 2, seed=24, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    pts = np.array([0.4 + 1.3j, 0.4 - 1.3j, -0.6 + 2j, -0.6 - 2j])
+    vals = ss.structured_pseudospectrum_grid(chf, pts, nb=4)
+    assert abs(vals[0] - vals[1]) <= 1e-12 * vals[0]
+    assert abs(vals[2] - vals[3]) <= 1e-12 * vals[2]
+
+
+def test_far_point_asymptotics():
+    sysb = ss.random_stable_system(16, 2, 2, seed=22, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    z = 1e8 * np.linalg.norm(sysb.A)
+    val = ss.structured_pseudospectrum_grid(chf, [z + 0j], nb=8)[0]
+    approx = np.linalg.svd(sysb.C @ sysb.B, compute_uv=False)[0] / z
+    assert abs(val / approx - 1.0) <= 1e-6
+
+
+# --------------------------------------------------------------------------
+# GPU reduction
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", [0, 3, 9, 15, 16])
+@pytest.mark.parametrize("bs", [1, 7, 64])
+def test_reduction_matches_reference(case, bs):
+    S = golden("systems.npz")
+    pre = f"s{case}_"
+    n, m = int(S[pre + "dims"][0]), int(S[pre + "dims"][1])
+    A, B, C = S[pre + "A"], S[pre + "B"], S[pre + "C"]
+    chf = ss.reduce_controller_hessenberg(A, B, C, block_size=bs, accumulate=True)
+    nA = np.linalg.norm(A)
+    assert np.abs(chf.Ahat - S[pre + "Ahat"]).max() <= 1e-11 * nA
+    assert np.abs(chf.Bhat - S[pre + "Bhat"]).max() <= 1e-11 * np.linalg.norm(B)
+    assert np.abs(chf.Chat - S[pre + "Chat"]).max() <= 1e-11 * nA * np.linalg.norm(C)
+    for j in range(n):
+        assert np.all(chf.Ahat[j + m + 1:, j] == 0.0)
+    for j in range(m):
+        assert np.all(chf.Bhat[j + 1:, j] == 0.0)
+    sim = np.linalg.norm(chf.Q.T @ A @ chf.Q - chf.Ahat)
+    assert sim <= 64 * n * EPS * nA
+
+
+def test_reduction_criterion3_corpus():
+    """test_acceptance.py:83-127 style: blocked GPU reduction vs the oracle's
+    unblocked reduction through the LU transfer function, b in {1,7,64}."""
+    rng = np.random.default_rng(2024)
+    worst_sim = worst_tf = 0.0
+    for case in range(12):
+        n = int(rng.integers(6, 129)) if case >= 2 else 128
+        m = int(rng.integers(1, min(8, n - 1) + 1))
+        p = int(rng.integers(1, 9))
+        sysb = ss.random_stable_system(n, m, p, seed=10_000 + case, circular=False)
+        Ao, Bo, Co, _ = O.reduce_chf(sysb.A, sysb.B, sysb.C)
+        probes = bounded_shifts(rng, sysb.A, 3)
+        for b in (1, 7, 64):
+            for strat in ("sequential", "overlapped"):
+                chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=b,
+                                                      strategy=strat, accumulate=True)
+                sim = np.linalg.norm(chf.Q.T @ sysb.A @ chf.Q - chf.Ahat)
+                worst_sim = max(worst_sim, sim / (64 * n * EPS * np.linalg.norm(sysb.A)))
+                for sig in probes:
+                    Gb = O.oracle_transfer_function(chf.Ahat, chf.Bhat, chf.Chat, sig)
+                    Go = O.oracle_transfer_function(Ao, Bo, Co, sig)
+                    worst_tf = max(worst_tf, rel(Gb, Go))
+    assert worst_sim <= 1.0 and worst_tf <= 1e-10, (worst_sim, worst_tf)
+
+
+def test_reduction_strategies_bitwise():
+    sysb = ss.random_stable_system(70, 3, 2, seed=31, circular=False)
+    a = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=16)
+    b = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=16, strategy="overlapped")
+    assert np.array_equal(a.Ahat, b.Ahat) and np.array_equal(a.Chat, b.Chat)
+
+
+# --------------------------------------------------------------------------
+# larger sizes: oracle on sampled shifts + size-independent properties
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,m,p,nb", [(1000, 10, 10, 64), (2000, 1, 1, 64), (1500, 20, 20, 48)])
+def test_medium_sizes_vs_oracle(n, m, p, nb):
+    sysb = ss.random_stable_system(n, m, p, seed=n + m, circular=True)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=64)
+    shifts = 1j * np.logspace(-2, 2, 24) * np.sqrt(n) + 0.1
+    res = ss.eval_transfer_function(chf, shifts, nb=nb)
+    assert res.failures == {}
+    idx = [0, 7, 23]
+    Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts[idx], nb=nb)
+    for k, l in enumerate(idx):
+        assert rel(res.value(l), Go[:, k * m:(k + 1) * m]) <= 1e-10
+    # conjugate symmetry of a real system: G(conj s) = conj G(s)
+    res2 = ss.eval_transfer_function(chf, np.conj(shifts), nb=nb)
+    assert per_shift_rel(res2.G, np.conj(res.G), m, len(shifts)) <= 1e-10
+    # residual of the reduced solve on one shift
+    bd = np.ones((m, 1), dtype=complex)
+    red = ss.solve_shifted_reduced(chf, shifts[3:4], bd, nb=nb)
+    cert = ss.residual_certificate(chf, shifts[3], red.x[:, 0], chf.Bhat @ bd[:, 0])
+    assert cert <= 1e3 * n * EPS
