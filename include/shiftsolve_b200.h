@@ -91,11 +91,22 @@ int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64_t lda, dou
 /* Per-phase accounting under the reference phase names (counters.py:17-23):
  * index 0 contr_hess_reduction, 1 small_batched_rq, 2 batched_gemm,
  * 3 outer_gemm, 4 tail_solves.  flops follow the reference's shape-only
- * formulas; seconds are CUDA-event times, collected only while timing is
- * enabled (timing synchronises the stream at the end of each call). */
+ * formulas; seconds are CUDA-event times recorded around every kernel while
+ * timing is enabled.  Recording never synchronises; ss_phase_stats and
+ * ss_update_kernel_stats wait for the recorded events and fold them in. */
 int ss_set_timing(ss_handle* h, int enabled);
-int ss_phase_stats(const ss_handle* h, double* seconds5, double* flops5);
+int ss_phase_stats(ss_handle* h, double* seconds5, double* flops5);
 void ss_reset_stats(ss_handle* h);
+
+/* Live statistics of the dominant kernel (the window update, k_update):
+ * launches, summed CUDA-event seconds and summed algorithmic flops
+ * (4 m x structurally-nonzero panel entries per shift) since
+ * the last ss_reset_stats, for roofline accounting. */
+int ss_update_kernel_stats(ss_handle* h, int64_t* launches, double* seconds, double* alg_flops);
+
+/* Diagnostic: measured FP64 FMA throughput of this device (TFLOP/s) from a
+ * DFMA-chain kernel over all SMs -- the denominator of the FP64 roofline. */
+int ss_probe_dfma_peak(ss_handle* h, double* tflops);
 
 /* Number of device kernels this handle has launched since creation. */
 int64_t ss_launch_count(const ss_handle* h);

@@ -20,7 +20,7 @@ SS_OK, SS_EDIM, SS_EARG, SS_ECUDA, SS_ENOMEM = 0, 1, 2, 3, 4
 EXPORTED = (
     "ss_version", "ss_create", "ss_destroy", "ss_last_error", "ss_greedy_schedule",
     "ss_tf_eval", "ss_solve_reduced", "ss_reduce_chf", "ss_set_timing", "ss_phase_stats",
-    "ss_reset_stats", "ss_launch_count",
+    "ss_reset_stats", "ss_launch_count", "ss_update_kernel_stats", "ss_probe_dfma_peak",
 )
 
 _lib = None
@@ -66,6 +66,10 @@ def load():
         L.ss_reset_stats.restype = None
         L.ss_launch_count.argtypes = [P]
         L.ss_launch_count.restype = ctypes.c_int64
+        L.ss_update_kernel_stats.argtypes = [P, P, P, P]
+        L.ss_update_kernel_stats.restype = I
+        L.ss_probe_dfma_peak.argtypes = [P, P]
+        L.ss_probe_dfma_peak.restype = I
         _lib = L
     return _lib
 

@@ -131,6 +131,55 @@ const Sched* get_sched(ss_handle* h, int nr, int nc) {
     return &res.first->second;
 }
 
+static cudaEvent_t ev_get(ss_handle* h) {
+    if (!h->ev_pool.empty()) {
+        cudaEvent_t e = h->ev_pool.back();
+        h->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+cudaEvent_t timing_begin(ss_handle* h, cudaStream_t st) {
+    if (!h->timing) return nullptr;
+    cudaEvent_t e = ev_get(h);
+    cudaEventRecord(e, st);
+    return e;
+}
+
+void timing_end(ss_handle* h, cudaStream_t st, cudaEvent_t a, int phase, double fl_batched,
+                double fl_outer, double fl_alg) {
+    if (!h->timing || !a) return;
+    cudaEvent_t b = ev_get(h);
+    cudaEventRecord(b, st);
+    h->pending.push_back(TimeRec{phase, a, b, fl_batched, fl_outer, fl_alg});
+}
+
+void timing_resolve(ss_handle* h) {
+    for (auto& r : h->pending) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        const double sec = ms * 1e-3;
+        if (r.phase == PH_UPDATE) {
+            const double tot = r.fl_batched + r.fl_outer;
+            const double fr = tot > 0 ? r.fl_batched / tot : 0.0;
+            h->sec[PH_BATCHED_GEMM] += sec * fr;
+            h->sec[PH_OUTER_GEMM] += sec * (1.0 - fr);
+            h->upd_launches++;
+            h->upd_sec += sec;
+            h->upd_alg += r.fl_alg;
+        } else if (r.phase >= 0 && r.phase < 5) {
+            h->sec[r.phase] += sec;
+        }
+        h->ev_pool.push_back(r.a);
+        h->ev_pool.push_back(r.b);
+    }
+    h->pending.clear();
+}
+
 }  // namespace ss
 
 extern "C" {
@@ -173,6 +222,11 @@ void ss_destroy(ss_handle* h) {
     if (h->ws) cudaFree(h->ws);
     if (h->ws2) cudaFree(h->ws2);
     if (h->d_scal) cudaFree(h->d_scal);
+    for (auto& r : h->pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->ev_b) cudaEventDestroy(h->ev_b);
     delete h;
@@ -199,8 +253,9 @@ int ss_set_timing(ss_handle* h, int enabled) {
     return SS_OK;
 }
 
-int ss_phase_stats(const ss_handle* h, double* seconds5, double* flops5) {
+int ss_phase_stats(ss_handle* h, double* seconds5, double* flops5) {
     if (!h) return SS_EARG;
+    ss::timing_resolve(h);
     for (int i = 0; i < 5; ++i) {
         if (seconds5) seconds5[i] = h->sec[i];
         if (flops5) flops5[i] = h->flops[i];
@@ -210,7 +265,19 @@ int ss_phase_stats(const ss_handle* h, double* seconds5, double* flops5) {
 
 void ss_reset_stats(ss_handle* h) {
     if (!h) return;
+    ss::timing_resolve(h);
     for (int i = 0; i < 5; ++i) h->sec[i] = h->flops[i] = 0.0;
+    h->upd_launches = 0;
+    h->upd_sec = h->upd_alg = 0.0;
+}
+
+int ss_update_kernel_stats(ss_handle* h, int64_t* launches, double* seconds, double* alg_flops) {
+    if (!h) return SS_EARG;
+    ss::timing_resolve(h);
+    if (launches) *launches = h->upd_launches;
+    if (seconds) *seconds = h->upd_sec;
+    if (alg_flops) *alg_flops = h->upd_alg;
+    return SS_OK;
 }
 
 int64_t ss_launch_count(const ss_handle* h) { return h ? h->launches : 0; }

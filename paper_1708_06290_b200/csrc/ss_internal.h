@@ -32,6 +32,18 @@ int greedy_schedule(int n_rows, int n_cols, std::vector<int64_t>& job,
 
 enum Phase { PH_REDUCTION = 0, PH_RQ = 1, PH_BATCHED_GEMM = 2, PH_OUTER_GEMM = 3, PH_TAIL = 4 };
 
+// Pseudo-phase of k_update: it fuses the reference's batched GEMM and outer
+// GEMM; its time is split between the two by their flop shares.
+constexpr int PH_UPDATE = 100;
+
+// One timed kernel (or kernel group) awaiting resolution.
+struct TimeRec {
+    int phase;
+    cudaEvent_t a, b;
+    double fl_batched, fl_outer;  // reference flops (for the update split)
+    double fl_alg;                // algorithmic flops (roofline accounting)
+};
+
 }  // namespace ss
 
 struct ss_handle {
@@ -52,6 +64,11 @@ struct ss_handle {
     double flops[5] = {0, 0, 0, 0, 0};
     int64_t launches = 0;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    // deferred event timing (ss_set_timing): resolved by ss_phase_stats
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<ss::TimeRec> pending;
+    int64_t upd_launches = 0;  // dominant kernel (k_update) live statistics
+    double upd_sec = 0.0, upd_alg = 0.0;
 };
 
 namespace ss {
@@ -62,6 +79,11 @@ int cuda_err(ss_handle* h, cudaError_t e, const char* what);
 int ensure_ws(ss_handle* h, size_t bytes, int which = 0);
 // Cached device schedule for (nr, nc).
 const Sched* get_sched(ss_handle* h, int nr, int nc);
+// Deferred event timing helpers (no-ops unless h->timing).
+cudaEvent_t timing_begin(ss_handle* h, cudaStream_t st);
+void timing_end(ss_handle* h, cudaStream_t st, cudaEvent_t a, int phase, double fl_batched = 0.0,
+                double fl_outer = 0.0, double fl_alg = 0.0);
+void timing_resolve(ss_handle* h);
 
 }  // namespace ss
 

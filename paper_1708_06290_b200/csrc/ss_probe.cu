@@ -1,0 +1,48 @@
+// Diagnostic: measured FP64 FMA peak of the device (the FP64 roofline
+// denominator; MEASURED_PEAKS.json only carries HBM and bf16 peaks).
+#include "ss_internal.h"
+
+namespace {
+
+// 8 independent DFMA chains per thread, enough warps per SM to cover the
+// pipe latency.  x, y are runtime values so nothing folds.
+__global__ void __launch_bounds__(512) k_dfma_chain(int iters, double x, double y, double* out) {
+    double a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+    double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, x, y); a1 = fma(a1, x, y); a2 = fma(a2, x, y); a3 = fma(a3, x, y);
+            a4 = fma(a4, x, y); a5 = fma(a5, x, y); a6 = fma(a6, x, y); a7 = fma(a7, x, y);
+        }
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[0] = s;  // never true; keeps the chains alive
+}
+
+}  // namespace
+
+extern "C" int ss_probe_dfma_peak(ss_handle* h, double* tflops) {
+    if (!h || !tflops) return SS_EARG;
+    SS_CUDA_TRY(h, cudaSetDevice(h->device));
+    const int blocks = h->num_sms * 4, threads = 512, iters = 2048;
+    cudaEvent_t a, b;
+    SS_CUDA_TRY(h, cudaEventCreate(&a));
+    SS_CUDA_TRY(h, cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a, 0);
+        k_dfma_chain<<<blocks, threads>>>(iters, 0.9999999, 1e-9, h->d_scal + 32);
+        SS_LAUNCH_CHECK(h);
+        cudaEventRecord(b, 0);
+        SS_CUDA_TRY(h, cudaEventSynchronize(b));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0 && ms < best) best = ms;  // rep 0 is warm-up
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8.0 * 16.0 * iters * (double)blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return SS_OK;
+}

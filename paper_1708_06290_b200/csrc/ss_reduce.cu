@@ -401,12 +401,7 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
     SS_CUDA_TRY(h, cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)stream;
     Ctx x{h, st};
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->timing) {
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, st);
-    }
+    cudaEvent_t e0 = ss::timing_begin(h, st);
     const int b = std::min(block_size, 128);
     const int bw_max = std::max(b, m);
     // workspace: V, Y (n x bw), T (bw x bw), W1/W2 (max(n,p) x max(bw, n) as needed), partials
@@ -520,16 +515,18 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
         // task (c): rows 0..kb, right update of columns kb..n via Ytop = A[0:kb, kb:] V T
         if (kb > 0) SS_TRY(apply_right(x, A + (int64_t)kb * lda, lda, kb, V, ldv, T, ldt, nk, bw, W1, W2, ldw));
         // tasks (a)+(b): rows kb..n, trailing columns zc+bw..n
-        const int col0 = zc + bw;
+        // (a) right: columns with reflector support, max(zc+bw, kb).. (hessenberg.py:149-160)
+        const int col0 = std::max(zc + bw, kb);
         if (col0 < n) {
-            const int tcols = n - col0;
             const int vrow0 = col0 - kb;
-            // (a) right: A[kb:, col0:] -= Y V[vrow0:, :]^T
-            SS_TRY(gemm(x, false, true, nk, tcols, bw, -1.0, Y, ldv, V + vrow0, ldv, 1.0,
+            SS_TRY(gemm(x, false, true, nk, n - col0, bw, -1.0, Y, ldv, V + vrow0, ldv, 1.0,
                         A + kb + (int64_t)col0 * lda, lda));
-            // (b) left: A[kb:, col0:] <- (I - V T^T V^T) A[kb:, col0:]
-            SS_TRY(apply_left(x, A + kb + (int64_t)col0 * lda, lda, tcols, V, ldv, T, ldt, nk, bw, L1, L2, ldl));
         }
+        // (b) left: every column right of the panel, zc+bw..n (hessenberg.py:161-164)
+        const int lcol0 = zc + bw;
+        if (lcol0 < n)
+            SS_TRY(apply_left(x, A + kb + (int64_t)lcol0 * lda, lda, n - lcol0, V, ldv, T, ldt, nk, bw,
+                              L1, L2, ldl));
         if (p > 0) SS_TRY(apply_right(x, C + (int64_t)kb * ldc, ldc, p, V, ldv, T, ldt, nk, bw, W1, W2, ldw));
         if (Q) SS_TRY(apply_right(x, Q + (int64_t)kb * ldq, ldq, n, V, ldv, T, ldt, nk, bw, W1, W2, ldw));
     }
@@ -538,15 +535,7 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
         k_zero_mat<<<64, 256, 0, st>>>(B + m, n - m, m, ldb);
         SS_LAUNCH_CHECK(h);
     }
-    if (h->timing) {
-        cudaEventRecord(e1, st);
-        cudaEventSynchronize(e1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        h->sec[ss::PH_REDUCTION] += ms * 1e-3;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    }
+    ss::timing_end(h, st, e0, ss::PH_REDUCTION);
     // reference flop count: 10/3 n^3 + 5/2 n^2 b - 9/2 n^2 m + n^2 m^2/(2b)
     const double dn = n, db = b, dm = m;
     h->flops[ss::PH_REDUCTION] += 10.0 / 3.0 * dn * dn * dn + 2.5 * dn * dn * db - 4.5 * dn * dn * dm +

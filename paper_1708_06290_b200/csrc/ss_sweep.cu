@@ -437,14 +437,24 @@ __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
 // ---------------------------------------------------------------------------
 // host driver
 // ---------------------------------------------------------------------------
+// Opt in to the largest dynamic shared memory the kernel can take
+// (the per-block opt-in limit minus its static shared memory).
+template <typename F>
+cudaError_t allow_max_smem(ss_handle* h, F* fn) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(h->smem_optin - fa.sharedSizeBytes));
+}
+
 template <int CC>
 int launch_update_cc(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const Dims& d,
                      const Step& s, const UpdCfg& u, const double2* zin, double2* zout,
                      const double2* pbuf) {
     static size_t configured = 0;
     if (smem > 48 * 1024 && configured < smem) {
-        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_update<CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)h->smem_optin));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update<CC>));
         configured = h->smem_optin;
     }
     k_update<CC><<<grid, kUpdThreads, smem, st>>>(d, s, u, zin, zout, pbuf);
@@ -472,42 +482,6 @@ int pick_cc(int m) {
         if (m % c == 0) return c;
     return 10;
 }
-
-struct Timer {
-    ss_handle* h;
-    cudaStream_t st;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
-    cudaEvent_t pending = nullptr;
-    int phase = -1;
-    void begin(int ph) {
-        if (!h->timing) return;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, st);
-        pending = e;
-        phase = ph;
-    }
-    void end() {
-        if (!h->timing || !pending) return;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, st);
-        rec.push_back({phase, {pending, e}});
-        pending = nullptr;
-    }
-    void flush() {
-        if (!h->timing) return;
-        cudaStreamSynchronize(st);
-        for (auto& r : rec) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, r.second.first, r.second.second);
-            h->sec[r.first] += ms * 1e-3;
-            cudaEventDestroy(r.second.first);
-            cudaEventDestroy(r.second.second);
-        }
-        rec.clear();
-    }
-};
 
 int max_nb_for(ss_handle* h, int m, int nb_req) {
     int nb = nb_req;
@@ -550,7 +524,6 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const int nb0 = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
     const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
 
-    Timer tm{h, st};
     // fro2 / trace for the per-shift singularity thresholds
     {
         const int parts = std::min(4 * h->num_sms, std::max(n, 1));
@@ -591,10 +564,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     static bool rq_attr = false;
     if (!rq_attr) {
-        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_rq, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)h->smem_optin));
-        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)h->smem_optin));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_head));
         rq_attr = true;
     }
 
@@ -634,11 +605,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             s.rot = sc->d_rot;
             s.joff = sc->d_job_off;
             // block RQ
-            tm.begin(ss::PH_RQ);
+            cudaEvent_t ev = ss::timing_begin(h, st);
             const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
             k_rq<<<sb, rq_threads, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
             SS_LAUNCH_CHECK(h);
-            tm.end();
+            ss::timing_end(h, st, ev, ss::PH_RQ);
             // window update
             UpdCfg u;
             u.rlo = a.mode == 1 ? s.c0 : 0;
@@ -649,17 +620,24 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             const int rows = s.r0 - u.rlo;
             dim3 g((unsigned)((rows + kRows - 1) / kRows), (unsigned)((sb + u.SG - 1) / u.SG));
             const size_t smem_u = align16((size_t)s.nb * kRows * 8) + u.SC * pst;
-            tm.begin(ss::PH_OUTER_GEMM);
-            int rc = launch_update(h, CC, g, smem_u, st, d, s, u, Zbuf[cur], Zbuf[cur ^ 1], Pbuf);
-            if (rc) return rc;
-            tm.end();
             // reference flop accounting (batched.py:58-61, solvers.py:194-199)
             double rq_fl = 0.0;
             for (int qq = 0; qq < sc->rots; ++qq)
                 rq_fl += 20.0 * ((sc->rot[qq] & 0xffu) + s.nc) + 16.0;
             h->flops[ss::PH_RQ] += rq_fl * sb;
-            h->flops[ss::PH_BATCHED_GEMM] += (double)sb * (8.0 * s.r0 * m * m + 8.0 * s.mnb * m);
-            h->flops[ss::PH_OUTER_GEMM] += 8.0 * s.r0 * ((double)sb * m) * s.nb;
+            const double fl_b = (double)sb * (8.0 * s.r0 * m * m + 8.0 * s.mnb * m);
+            const double fl_o = 8.0 * s.r0 * ((double)sb * m) * s.nb;
+            h->flops[ss::PH_BATCHED_GEMM] += fl_b;
+            h->flops[ss::PH_OUTER_GEMM] += fl_o;
+            // algorithmic flops of this launch: every structural
+            // nonzero of the panel rows it updates meets m complex columns once
+            const double nnz = (double)(a.mode == 0 ? (double)a.p * s.nb : (double)s.nb) +
+                               (double)(k - s.nb) * s.nb;
+            const double fl_alg = 4.0 * m * nnz * sb;
+            ev = ss::timing_begin(h, st);
+            int rc = launch_update(h, CC, g, smem_u, st, d, s, u, Zbuf[cur], Zbuf[cur ^ 1], Pbuf);
+            if (rc) return rc;
+            ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
             cur ^= 1;
             k -= s.nb;
         }
@@ -674,14 +652,13 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         ho.out = a.mode == 0 ? a.out + lo * m * a.ldo : a.out + lo * a.ldo;
         ho.ldo = a.ldo;
         ho.fail = a.fail + lo;
-        tm.begin(ss::PH_TAIL);
+        cudaEvent_t evh = ss::timing_begin(h, st);
         const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
         k_head<<<sb, 128, smem_h, st>>>(d, ho, Zbuf[cur]);
         SS_LAUNCH_CHECK(h);
-        tm.end();
+        ss::timing_end(h, st, evh, ss::PH_TAIL);
         h->flops[ss::PH_TAIL] += a.mode == 0 ? (double)sb * 8.0 * a.p * m * m : (double)sb * 8.0 * n * m;
     }
-    tm.flush();
     return SS_OK;
 }
 
