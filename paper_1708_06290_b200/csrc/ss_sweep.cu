@@ -30,13 +30,12 @@
 
 #include "ss_device.cuh"
 #include "ss_internal.h"
+#include "ss_update.cuh"
 
 using namespace ssd;
 
 namespace {
 
-constexpr int kRows = 64;        // rows per k_update tile (2 per lane)
-constexpr int kUpdThreads = 256;  // 8 warps
 
 struct Dims {
     int n, m, ptop;
@@ -196,106 +195,6 @@ __global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* _
 }
 
 // ---------------------------------------------------------------------------
-// per-step window update (solvers.py:186-199):
-//   Z2out_l[i] = Z2in_l[i] P_l[nb:nb+m] + Z1[i] P_l[0:nb] - sigma_l P_l[i-(r0-m)]
-// ---------------------------------------------------------------------------
-struct UpdCfg {
-    int rlo;   // first row updated (0, or c0 for the identity top)
-    int SG;    // shifts per CTA
-    int SC;    // shifts staged concurrently
-};
-
-template <int CC>
-__global__ void __launch_bounds__(kUpdThreads)
-    k_update(Dims d, Step st, UpdCfg u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
-             const double2* __restrict__ Pbuf) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int nb = st.nb, m = d.m, nc = st.nc, r0 = st.r0;
-    double* Pan = (double*)smem;                                  // [nb][kRows]
-    double2* Pst = (double2*)(smem + align16((size_t)nb * kRows * 8));  // [SC][nc*m]
-    const int i0 = u.rlo + blockIdx.x * kRows;
-    const int l0 = blockIdx.y * u.SG;
-    const int lend = min(l0 + u.SG, d.sb);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    for (int v = threadIdx.x; v < nb * kRows; v += blockDim.x) {
-        const int j = v / kRows, ii = v - j * kRows;
-        const int i = i0 + ii;
-        Pan[v] = (i < r0) ? panel_val(d, i, st.c0 + j) : 0.0;
-    }
-    const int ncg = (m + CC - 1) / CC;
-    const int row_a = i0 + lane, row_b = i0 + lane + 32;
-    const bool ok_a = row_a < r0, ok_b = row_b < r0;
-    const int dlo = r0 - m;  // first row receiving the lazy-shift correction
-
-    for (int lc = l0; lc < lend; lc += u.SC) {
-        const int nsc = min(u.SC, lend - lc);
-        __syncthreads();
-        {
-            const double2* src = Pbuf + (int64_t)lc * nc * m;
-            const int tot = nsc * nc * m;
-            for (int v = threadIdx.x; v < tot; v += blockDim.x) Pst[v] = src[v];
-        }
-        __syncthreads();
-        for (int unit = warp; unit < nsc * ncg; unit += kUpdThreads / 32) {
-            const int ls = unit / ncg, g = unit - ls * ncg;
-            const int l = lc + ls;
-            const double2* Pl = Pst + (int64_t)ls * nc * m;
-            const int cb = g * CC;
-            const int ncol = min(CC, m - cb);
-            double2 acc0[CC], acc1[CC];
-#pragma unroll
-            for (int c = 0; c < CC; ++c) acc0[c] = acc1[c] = cz();
-            // Z1 (real panel) part: the shared "outer GEMM"
-            for (int j = 0; j < nb; ++j) {
-                const double a0 = Pan[j * kRows + lane], a1 = Pan[j * kRows + lane + 32];
-#pragma unroll
-                for (int c = 0; c < CC; ++c) {
-                    if (c < ncol) {
-                        const double2 p = Pl[j + (cb + c) * nc];
-                        acc0[c] = rfma(a0, p, acc0[c]);
-                        acc1[c] = rfma(a1, p, acc1[c]);
-                    }
-                }
-            }
-            // Z2 part: the per-shift "batched GEMM"
-            const double2* zin = Zin + (int64_t)l * m * d.LDZ;
-            for (int j = 0; j < m; ++j) {
-                const double2 z0 = ok_a ? zin[(int64_t)j * d.LDZ + row_a] : cz();
-                const double2 z1 = ok_b ? zin[(int64_t)j * d.LDZ + row_b] : cz();
-#pragma unroll
-                for (int c = 0; c < CC; ++c) {
-                    if (c < ncol) {
-                        const double2 p = Pl[nb + j + (cb + c) * nc];
-                        acc0[c] = cfma(z0, p, acc0[c]);
-                        acc1[c] = cfma(z1, p, acc1[c]);
-                    }
-                }
-            }
-            const double2 sig = d.shifts[l];
-            double2* zo = Zout + ((int64_t)l * m + cb) * d.LDZ;
-#pragma unroll
-            for (int c = 0; c < CC; ++c) {
-                if (c < ncol) {
-                    if (ok_a) {
-                        double2 v = acc0[c];
-                        const int dd = row_a - dlo;
-                        if (dd >= 0 && dd < st.mnb) v = csub(v, cmul(sig, Pl[dd + (cb + c) * nc]));
-                        zo[(int64_t)c * d.LDZ + row_a] = v;
-                    }
-                    if (ok_b) {
-                        double2 v = acc1[c];
-                        const int dd = row_b - dlo;
-                        if (dd >= 0 && dd < st.mnb) v = csub(v, cmul(sig, Pl[dd + (cb + c) * nc]));
-                        zo[(int64_t)c * d.LDZ + row_b] = v;
-                    }
-                }
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // head (solvers.py:204-231 + :262-268 / :303-310): one CTA per shift.
 // Warp 0 reduces the m x m head with the reference's rotation order,
 // accumulating the rotations in Qh (m x m) instead of rotating every top
@@ -357,7 +256,7 @@ __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
                 const double2 a = Hh[i + i * m], b = Hh[i + jj * m];
                 double c;
                 double2 s, rho;
-                givens(a, b, c, s, rho);
+                givens_fast(a, b, c, s, rho);
                 for (int r = lane; r < m; r += 32) {
                     if (r != i) {
                         double2 hh = Hh[r + i * m], tt = Hh[r + jj * m];
@@ -448,46 +347,56 @@ cudaError_t allow_max_smem(ss_handle* h, F* fn) {
                                 (int)(h->smem_optin - fa.sharedSizeBytes));
 }
 
-template <int CC>
-int launch_update_cc(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const Dims& d,
-                     const Step& s, const UpdCfg& u, const double2* zin, double2* zout,
-                     const double2* pbuf) {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && configured < smem) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_update<CC>));
-        configured = h->smem_optin;
+template <int C, bool EXACT>
+int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStream_t st,
+                    const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
+    static bool configured = false;
+    if (!configured) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update<C, EXACT>));
+        configured = true;
     }
-    k_update<CC><<<grid, kUpdThreads, smem, st>>>(d, s, u, zin, zout, pbuf);
+    k_update<C, EXACT><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
 
-int launch_update(ss_handle* h, int CC, dim3 grid, size_t smem, cudaStream_t st, const Dims& d,
-                  const Step& s, const UpdCfg& u, const double2* zin, double2* zout,
+int launch_update(ss_handle* h, int C, bool exact, dim3 grid, int threads, size_t smem,
+                  cudaStream_t st, const UpdDims& u, const double2* zin, double2* zout,
                   const double2* pbuf) {
-    switch (CC) {
-#define SS_CASE(K) \
-    case K: return launch_update_cc<K>(h, grid, smem, st, d, s, u, zin, zout, pbuf);
-        SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6)
-        SS_CASE(7) SS_CASE(8) SS_CASE(9) SS_CASE(10) SS_CASE(11) SS_CASE(12)
-#undef SS_CASE
+#define SS_CASE(K)                                                                           \
+    case K:                                                                                  \
+        return exact ? launch_update_t<K, true>(h, grid, threads, smem, st, u, zin, zout, pbuf) \
+                     : launch_update_t<K, false>(h, grid, threads, smem, st, u, zin, zout, pbuf);
+    switch (C) {
+        SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
         default: return ss::set_err(h, SS_EARG, "unsupported column tile");
     }
+#undef SS_CASE
 }
 
-// columns per thread tile: m itself when small, else a divisor in [8, 12]
-int pick_cc(int m) {
-    if (m <= 12) return m;
-    for (int c = 12; c >= 8; --c)
-        if (m % c == 0) return c;
-    return 10;
+// Columns per thread: the largest divisor of m in [4, 8] (exact tiles, no
+// predication); m < 4 -> m; otherwise 5 with a predicated last group.
+void pick_cols(int m, int& C, bool& exact) {
+    if (m <= 8 && (m <= 4 || m == 5 || m == 6 || m == 8)) {
+        C = m;
+        exact = true;
+        return;
+    }
+    for (int c = 8; c >= 4; --c)
+        if (m % c == 0) {
+            C = c;
+            exact = true;
+            return;
+        }
+    C = 5;
+    exact = false;
 }
 
 int max_nb_for(ss_handle* h, int m, int nb_req) {
     int nb = nb_req;
     while (nb > 1) {
         const size_t need = rq_smem_bytes(nb, m, nb * m, nb * m);
-        const size_t upd = align16((size_t)nb * kRows * 8) + (size_t)(nb + m) * m * 16;
+        const size_t upd = upd_smem_bytes(nb, m, 1);
         if (need <= h->smem_optin && upd <= h->smem_optin && nb + m <= 255) break;
         nb = nb > 8 ? nb - 8 : nb - 1;
     }
@@ -558,9 +467,10 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     Zbuf[1] = Zbuf[0] + (size_t)sb_max * m * LDZ;
     double2* Pbuf = Zbuf[1] + (size_t)sb_max * m * LDZ;
 
-    const int CC = pick_cc(m);
-    const int ncg = (m + CC - 1) / CC;
-    const int rq_threads = m <= 16 ? 256 : 512;
+    int C = 1;
+    bool exact = true;
+    pick_cols(m, C, exact);
+    const int ncg = (m + C - 1) / C;
 
     static bool rq_attr = false;
     if (!rq_attr) {
@@ -607,19 +517,38 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             // block RQ
             cudaEvent_t ev = ss::timing_begin(h, st);
             const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
+            // one warp per concurrent rotation of the schedule (<= 16 warps)
+            const int rq_threads = 32 * std::max(1, std::min(sc->max_job, 16));
             k_rq<<<sb, rq_threads, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
             SS_LAUNCH_CHECK(h);
             ss::timing_end(h, st, ev, ss::PH_RQ);
-            // window update
-            UpdCfg u;
+            // window update: S shifts per chunk, one warp per (shift, column group),
+            // smem sized for two resident CTAs per SM when it fits
+            UpdDims u;
+            u.n = n;
+            u.m = m;
+            u.ptop = ptop;
+            u.ident_top = d.ident_top;
+            u.A = a.A;
+            u.lda = a.lda;
+            u.T = a.C;
+            u.ldt = a.ldc;
+            u.shifts = d.shifts;
+            u.sb = sb;
+            u.LDZ = LDZ;
+            u.nb = s.nb;
+            u.mnb = s.mnb;
+            u.r0 = s.r0;
+            u.c0 = s.c0;
+            u.nc = s.nc;
             u.rlo = a.mode == 1 ? s.c0 : 0;
-            u.SC = std::max(1, (kUpdThreads / 32) / ncg);
-            const size_t pst = (size_t)s.nc * m * 16;
-            while (u.SC > 1 && align16((size_t)s.nb * kRows * 8) + u.SC * pst > 96 * 1024) u.SC--;
-            u.SG = u.SC * 2;
+            u.S = std::max(1, 8 / ncg);
+            const size_t two_per_sm = h->smem_optin / 2 - 1024;
+            while (u.S > 1 && upd_smem_bytes(s.nb, m, u.S) > two_per_sm) u.S--;
+            u.SG = u.S * 4;
             const int rows = s.r0 - u.rlo;
-            dim3 g((unsigned)((rows + kRows - 1) / kRows), (unsigned)((sb + u.SG - 1) / u.SG));
-            const size_t smem_u = align16((size_t)s.nb * kRows * 8) + u.SC * pst;
+            dim3 g((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
+            const size_t smem_u = upd_smem_bytes(s.nb, m, u.S);
             // reference flop accounting (batched.py:58-61, solvers.py:194-199)
             double rq_fl = 0.0;
             for (int qq = 0; qq < sc->rots; ++qq)
@@ -635,7 +564,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
                                (double)(k - s.nb) * s.nb;
             const double fl_alg = 4.0 * m * nnz * sb;
             ev = ss::timing_begin(h, st);
-            int rc = launch_update(h, CC, g, smem_u, st, d, s, u, Zbuf[cur], Zbuf[cur ^ 1], Pbuf);
+            int rc = launch_update(h, C, exact, g, 32 * u.S * ncg, smem_u, st, u, Zbuf[cur],
+                                   Zbuf[cur ^ 1], Pbuf);
             if (rc) return rc;
             ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
             cur ^= 1;
