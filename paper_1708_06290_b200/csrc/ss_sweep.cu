@@ -128,6 +128,7 @@ __global__ void k_seed(Dims d, double2* __restrict__ Za, double2* __restrict__ Z
 // ---------------------------------------------------------------------------
 struct Step {
     int k, nb, mnb, r0, c0, nc;
+    int lmp;  // log2 of the smallest power of two >= m
     int steps, rots;
     const uint32_t* rot;
     const int32_t* joff;
@@ -147,6 +148,7 @@ __host__ __device__ inline size_t rq_smem_bytes(int nb, int m, int steps, int ro
     return b;
 }
 
+template <int TPR>
 __global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* __restrict__ Pbuf) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int l = blockIdx.x;
@@ -188,8 +190,8 @@ __global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* _
         }
     }
     __syncthreads();
-    block_rq_forward(Zb, nb, rot, joff, st.steps, rc, rs);
-    block_rq_reverse(Zb, nc, m, rot, joff, st.steps, rc, rs);  // W aliases the block
+    block_rq_forward2<TPR>(Zb, nb, rot, joff, st.steps, rc, rs);
+    block_rq_reverse2(Zb, nc, m, st.lmp, rot, joff, st.steps, rc, rs);  // W aliases the block
     double2* dstP = Pbuf + (int64_t)l * nc * m;
     for (int u = threadIdx.x; u < nc * m; u += blockDim.x) dstP[u] = Zb[u];
 }
@@ -474,7 +476,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     static bool rq_attr = false;
     if (!rq_attr) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<8>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_head));
         rq_attr = true;
     }
@@ -518,8 +520,12 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             cudaEvent_t ev = ss::timing_begin(h, st);
             const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
             // one warp per concurrent rotation of the schedule (<= 16 warps)
-            const int rq_threads = 32 * std::max(1, std::min(sc->max_job, 16));
-            k_rq<<<sb, rq_threads, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            // phase B of the block RQ: 8 threads per rotation, all rotations of a
+            // step in one round when possible
+            const int rq_threads = std::min(256, std::max(32, ((sc->max_job * 8 + 31) / 32) * 32));
+            s.lmp = 0;
+            while ((1 << s.lmp) < m) s.lmp++;
+            k_rq<8><<<sb, rq_threads, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
             SS_LAUNCH_CHECK(h);
             ss::timing_end(h, st, ev, ss::PH_RQ);
             // window update: S shifts per chunk, one warp per (shift, column group),

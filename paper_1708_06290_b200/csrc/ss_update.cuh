@@ -10,8 +10,8 @@
 // memory, reused by all SG shifts the CTA processes) and walks its shifts in
 // chunks of S.  Per chunk, P_l (nc x m) and the 64 x m tile of Zin_l for the
 // S shifts are staged with cp.async (zero-filled past r0).  Warp w owns one
-// (shift, C-column group) unit of the chunk: lane L computes rows L and L+32
-// x C complex columns in registers; P_l entries are warp-uniform shared
+// (shift, C-column group) unit of the chunk: lane L computes rows
+// (2L, 2L+1) x C complex columns in registers; P_l entries are warp-uniform shared
 // memory broadcasts, panel / Zin entries are per-lane conflict-free loads.
 #pragma once
 
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256)
 
     const int s_w = warp / ncg, g = warp - s_w * ncg;  // this warp's unit
     const int cb = g * C;
-    const int row_a = i0 + lane, row_b = row_a + 32;
+    const int row_a = i0 + 2 * lane, row_b = row_a + 1;  // adjacent rows: 16-byte panel loads
     const int dlo = r0 - m;
 
     for (int lc = l0; lc < lend; lc += u.S) {
@@ -123,11 +123,12 @@ __global__ void __launch_bounds__(256)
         // Z1 (real panel) part -- the reference's outer GEMM
 #pragma unroll 4
         for (int j = 0; j < nb; ++j) {
-            const double a0 = Pan[j * kUpdRows + lane], a1 = Pan[j * kUpdRows + lane + 32];
+            const double2 a01 = *reinterpret_cast<const double2*>(Pan + j * kUpdRows + 2 * lane);
+            const double a0 = a01.x, a1 = a01.y;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (EXACT || c < ncol) {
-                    const double2 p = Pl[j + (cb + c) * nc];
+                    const double2 p = Pl[j * m + cb + c];
                     acc0[c] = rfma(a0, p, acc0[c]);
                     acc1[c] = rfma(a1, p, acc1[c]);
                 }
@@ -136,11 +137,11 @@ __global__ void __launch_bounds__(256)
         // Z2 part -- the reference's per-shift batched GEMM
 #pragma unroll 2
         for (int j = 0; j < m; ++j) {
-            const double2 z0 = Zl[j * kUpdRows + lane], z1 = Zl[j * kUpdRows + lane + 32];
+            const double2 z0 = Zl[j * kUpdRows + 2 * lane], z1 = Zl[j * kUpdRows + 2 * lane + 1];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (EXACT || c < ncol) {
-                    const double2 p = Pl[nb + j + (cb + c) * nc];
+                    const double2 p = Pl[(nb + j) * m + cb + c];
                     acc0[c] = cfma(z0, p, acc0[c]);
                     acc1[c] = cfma(z1, p, acc1[c]);
                 }
@@ -154,12 +155,12 @@ __global__ void __launch_bounds__(256)
             if (EXACT || c < ncol) {
                 if (row_a < r0) {
                     double2 v = acc0[c];
-                    if (da >= 0 && da < u.mnb) v = csub(v, cmul(sig, Pl[da + (cb + c) * nc]));
+                    if (da >= 0 && da < u.mnb) v = csub(v, cmul(sig, Pl[da * m + cb + c]));
                     zo[(int64_t)c * u.LDZ + row_a] = v;
                 }
                 if (row_b < r0) {
                     double2 v = acc1[c];
-                    if (db >= 0 && db < u.mnb) v = csub(v, cmul(sig, Pl[db + (cb + c) * nc]));
+                    if (db >= 0 && db < u.mnb) v = csub(v, cmul(sig, Pl[db * m + cb + c]));
                     zo[(int64_t)c * u.LDZ + row_b] = v;
                 }
             }
