@@ -141,14 +141,12 @@ __host__ __device__ inline size_t rq_smem_bytes(int nb, int m, int steps, int ro
     size_t b = 0;
     b += align16((size_t)rots * 4);           // rot
     b += align16((size_t)(steps + 1) * 4);    // joff
-    b += align16((size_t)rots * 8);           // rc
-    b += align16((size_t)rots * 16);          // rs
     const int zw = pk_size(nb, m) > nc * m ? pk_size(nb, m) : nc * m;
     b += (size_t)zw * 16;                     // Zb / W
     return b;
 }
 
-template <int TPR>
+template <int SLOTS>
 __global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* __restrict__ Pbuf) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int l = blockIdx.x;
@@ -158,10 +156,6 @@ __global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* _
     off += align16((size_t)st.rots * 4);
     int* joff = (int*)(smem + off);
     off += align16((size_t)(st.steps + 1) * 4);
-    double* rc = (double*)(smem + off);
-    off += align16((size_t)st.rots * 8);
-    double2* rs = (double2*)(smem + off);
-    off += align16((size_t)st.rots * 16);
     double2* Zb = (double2*)(smem + off);
 
     for (int u = threadIdx.x; u < st.rots; u += blockDim.x) rot[u] = st.rot[u];
@@ -190,8 +184,7 @@ __global__ void k_rq(Dims d, Step st, const double2* __restrict__ Z2, double2* _
         }
     }
     __syncthreads();
-    block_rq_forward2<TPR>(Zb, nb, rot, joff, st.steps, rc, rs);
-    block_rq_reverse2(Zb, nc, m, st.lmp, rot, joff, st.steps, rc, rs);  // W aliases the block
+    block_rq_fused<SLOTS>(Zb, nb, nc, m, rot, joff, st.steps);  // W (j-major) over the block
     double2* dstP = Pbuf + (int64_t)l * nc * m;
     for (int u = threadIdx.x; u < nc * m; u += blockDim.x) dstP[u] = Zb[u];
 }
@@ -476,6 +469,9 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     static bool rq_attr = false;
     if (!rq_attr) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<1>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<2>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<4>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<8>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_head));
         rq_attr = true;
@@ -520,12 +516,20 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             cudaEvent_t ev = ss::timing_begin(h, st);
             const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
             // one warp per concurrent rotation of the schedule (<= 16 warps)
-            // phase B of the block RQ: 8 threads per rotation, all rotations of a
-            // step in one round when possible
-            const int rq_threads = std::min(256, std::max(32, ((sc->max_job * 8 + 31) / 32) * 32));
-            s.lmp = 0;
-            while ((1 << s.lmp) < m) s.lmp++;
-            k_rq<8><<<sb, rq_threads, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            // one warp per concurrent rotation (<= 16 warps); rotation
+            // parameters live in registers: SLOTS x 32 per warp
+            const int nw = std::max(1, std::min(sc->max_job, 16));
+            int per_warp = 0;
+            for (int t = 0; t < sc->steps; ++t) {
+                const int J = sc->job_off[t + 1] - sc->job_off[t];
+                per_warp += (J + nw - 1) / nw;
+            }
+            const int slots = (per_warp + 31) / 32;
+            if (slots <= 1) k_rq<1><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            else if (slots <= 2) k_rq<2><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            else if (slots <= 4) k_rq<4><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            else if (slots <= 8) k_rq<8><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
+            else return ss::set_err(h, SS_EARG, "window block too large for the register rotation store");
             SS_LAUNCH_CHECK(h);
             ss::timing_end(h, st, ev, ss::PH_RQ);
             // window update: S shifts per chunk, one warp per (shift, column group),
