@@ -27,9 +27,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "ss_device.cuh"
 #include "ss_internal.h"
+#include "ss_rq_house.cuh"
 #include "ss_update.cuh"
 
 using namespace ssd;
@@ -462,6 +465,10 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     Zbuf[1] = Zbuf[0] + (size_t)sb_max * m * LDZ;
     double2* Pbuf = Zbuf[1] + (size_t)sb_max * m * LDZ;
 
+    // block RQ flavour: row Householder (one warp per shift) unless m+1 > 32
+    // or SS_BLOCK_RQ=givens selects the reference's scheduled Givens batch
+    const char* rqenv = getenv("SS_BLOCK_RQ");
+    const bool use_house = (m + 1 <= 32) && !(rqenv && strcmp(rqenv, "givens") == 0);
     int C = 1;
     bool exact = true;
     pick_cols(m, C, exact);
@@ -473,6 +480,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<2>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<4>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<8>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<2>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<4>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<8>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<16>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<32>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_head));
         rq_attr = true;
     }
@@ -516,6 +528,28 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             cudaEvent_t ev = ss::timing_begin(h, st);
             const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
             // one warp per concurrent rotation of the schedule (<= 16 warps)
+            if (use_house) {
+                // one warp per shift: row-Householder block RQ (ss_rq_house.cuh)
+                RqDims rd;
+                rd.m = m;
+                rd.ptop = ptop;
+                rd.nb = s.nb;
+                rd.k = s.k;
+                rd.c0 = s.c0;
+                rd.r0 = s.r0;
+                rd.nc = s.nc;
+                rd.sb = sb;
+                rd.A = a.A;
+                rd.lda = a.lda;
+                rd.shifts = d.shifts;
+                rd.LDZ = LDZ;
+                const size_t sm = rqh_warp_smem(s.nb, m);
+                if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
+                else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
+                else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
+                else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
+                else k_rq_house<32><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
+            } else {
             // one warp per concurrent rotation (<= 16 warps); rotation
             // parameters live in registers: SLOTS x 32 per warp
             const int nw = std::max(1, std::min(sc->max_job, 16));
@@ -530,6 +564,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             else if (slots <= 4) k_rq<4><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
             else if (slots <= 8) k_rq<8><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
             else return ss::set_err(h, SS_EARG, "window block too large for the register rotation store");
+            }
             SS_LAUNCH_CHECK(h);
             ss::timing_end(h, st, ev, ss::PH_RQ);
             // window update: S shifts per chunk, one warp per (shift, column group),

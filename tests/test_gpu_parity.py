@@ -357,3 +357,20 @@ def test_medium_sizes_vs_oracle(n, m, p, nb):
     red = ss.solve_shifted_reduced(chf, shifts[3:4], bd, nb=nb)
     cert = ss.residual_certificate(chf, shifts[3], red.x[:, 0], chf.Bhat @ bd[:, 0])
     assert cert <= 1e3 * n * EPS
+
+
+@pytest.mark.parametrize("case", [0, 9, 15, 16])
+def test_block_rq_flavours_agree(case, monkeypatch):
+    """The row-Householder block RQ (default) and the reference's scheduled
+    Givens batch (SS_BLOCK_RQ=givens) give the same G to rounding: P differs
+    by an m x m unitary on the active columns, G is invariant."""
+    S = golden("systems.npz")
+    pre = f"s{case}_"
+    m, nb = int(S[pre + "dims"][1]), int(S[pre + "dims"][4])
+    chf = chf_of(S, pre)
+    shifts = S[pre + "shifts"]
+    Gh = ss.eval_transfer_function(chf, shifts, nb=nb).G
+    monkeypatch.setenv("SS_BLOCK_RQ", "givens")
+    Gg = ss.eval_transfer_function(chf, shifts, nb=nb).G
+    assert per_shift_rel(Gh, Gg, m, len(shifts)) <= 1e-12
+    assert per_shift_rel(Gg, S[pre + "G"], m, len(shifts)) <= 1e-10
