@@ -227,6 +227,7 @@ void ss_destroy(ss_handle* h) {
         cudaEventDestroy(r.b);
     }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
     if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->ev_b) cudaEventDestroy(h->ev_b);
     delete h;

@@ -63,7 +63,8 @@ struct ss_handle {
     double sec[5] = {0, 0, 0, 0, 0};
     double flops[5] = {0, 0, 0, 0, 0};
     int64_t launches = 0;
-    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // fork / join events
+    cudaStream_t aux_stream = nullptr;             // second stream of the sweep
     // deferred event timing (ss_set_timing): resolved by ss_phase_stats
     std::vector<cudaEvent_t> ev_pool;
     std::vector<ss::TimeRec> pending;

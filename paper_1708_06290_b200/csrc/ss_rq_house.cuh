@@ -61,92 +61,123 @@ __global__ void __launch_bounds__(128)
     const double2 sig = d.shifts[l];
     const int arow0 = d.k - nb;  // A row of block row 0
 
-    // panel column j (block coords, j < nb) into its slot, rows 0..hi-1
-    auto load_z1 = [&](int j, int hi) {
-        double2* dst = Win + (size_t)(j % L) * nb;
-        const double* src = d.A + arow0 + (int64_t)(d.c0 + j) * d.lda;
-        for (int i = lane; i < hi; i += 32) {
+    // initial window: columns nb-1 .. nb-1+m  (Z1 column nb-1 and the m Z2 columns)
+    {
+        double2* dst = Win + (size_t)((nb - 1) % L) * nb;
+        const double* src = d.A + arow0 + (int64_t)(d.c0 + nb - 1) * d.lda;
+        for (int i = lane; i < nb; i += 32) {
             double2 v = make_double2(src[i], 0.0);
-            if (i + m == j) {  // Ahat's main diagonal inside the panel: lazy -sigma
-                v.x -= sig.x;
-                v.y -= sig.y;
-            }
+            if (i + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
             dst[i] = v;
         }
-    };
-    // initial window: columns nb-1 .. nb-1+m  (Z1 column nb-1 and the m Z2 columns)
-    load_z1(nb - 1, nb);
+    }
     for (int c = 0; c < m; ++c) {
         const int j = nb + c;
         double2* dst = Win + (size_t)(j % L) * nb;
         const double2* src = Z2 + ((int64_t)l * m + c) * d.LDZ + d.r0;
         for (int i = lane; i < nb; i += 32) dst[i] = src[i];
     }
+    // prefetch of the panel column entering next (rows lane, lane+32)
+    double pf0 = 0.0, pf1 = 0.0;
+    auto prefetch = [&](int j) {  // column j, rows 0..j
+        const double* src = d.A + arow0 + (int64_t)(d.c0 + j) * d.lda;
+        pf0 = (lane <= j) ? src[lane] : 0.0;
+        pf1 = (lane + 32 <= j) ? src[lane + 32] : 0.0;
+    };
+    if (nb >= 2) prefetch(nb - 2);
     __syncwarp();
 
     for (int t = nb - 1; t >= 0; --t) {
         const int base = t % L;  // slot of column t; column t+j sits in slot (base+j) mod L
-        // ---- reflector from row t of the window (lane j holds entry j) ----
-        double2 y = cz();
-        if (lane < L) {
-            int sj = base + lane;
-            if (sj >= L) sj -= L;
-            const double2 x = Win[(size_t)sj * nb + t];
-            y = make_double2(x.x, -x.y);  // conj
+        // ---- every lane builds the reflector of row t from broadcast loads ----
+        double2 y[LMAX];
+        double s2a = 0.0, s2b = 0.0;
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) {
+            if (j < L) {
+                int sj = base + j;
+                if (sj >= L) sj -= L;
+                const double2 x = Win[(size_t)sj * nb + t];
+                y[j] = make_double2(x.x, -x.y);  // conj(row t)
+                if (j < L - 1) {
+                    if (j & 1) s2b = fma(y[j].x, y[j].x, fma(y[j].y, y[j].y, s2b));
+                    else s2a = fma(y[j].x, y[j].x, fma(y[j].y, y[j].y, s2a));
+                }
+            }
         }
-        const double2 alpha = shfl2(y, L - 1);
-        const double s2 = warp_sum(lane < L - 1 ? y.x * y.x + y.y * y.y : 0.0);
+        double2 alpha = cz();
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j)
+            if (j == L - 1) alpha = y[j];
+        const double s2 = s2a + s2b;
         double2 tau = cz(), scale = cz();
         if (!(s2 == 0.0 && alpha.y == 0.0)) {
-            const double nrm2 = alpha.x * alpha.x + alpha.y * alpha.y + s2;
+            const double nrm2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
             const double rn = rsqrt(nrm2);
             const double sg = alpha.x >= 0.0 ? -1.0 : 1.0;
             const double beta = sg * nrm2 * rn;  // -sign(Re alpha) ||y||
             const double ib = sg * rn;           // 1 / beta
             tau = make_double2(1.0 - alpha.x * ib, -alpha.y * ib);  // (beta - alpha) / beta
             const double zx = alpha.x - beta, zy = alpha.y;
-            const double iz = 1.0 / (zx * zx + zy * zy);
+            const double rz = rsqrt(fma(zx, zx, zy * zy));
+            const double iz = rz * rz;
             scale = make_double2(zx * iz, -zy * iz);  // 1 / (alpha - beta)
         }
-        double2 u = cmul(y, scale);
-        if (lane == L - 1) u = make_double2(1.0, 0.0);
-        if (lane < L) U[(size_t)t * L + lane] = u;
+        double2 uu[LMAX];
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) uu[j] = (j < L - 1) ? cmul(y[j], scale) : (j == L - 1 ? make_double2(1.0, 0.0) : cz());
+        if (lane < L) {
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j == lane) U[(size_t)t * L + j] = uu[j];
+        }
         if (lane == 0) Tau[t] = tau;
-        __syncwarp();
-        // ---- rows 0..t-1: z <- z - tau (z u) u^H ----
-        if (t > 0 && (tau.x != 0.0 || tau.y != 0.0)) {
-            double2 uu[LMAX];
+        // ---- rows 0..t-1 (lanes own rows lane, lane+32): z <- z - tau (z u) u^H ----
+        const bool act = t > 0 && (tau.x != 0.0 || tau.y != 0.0);
+        if (act) {
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j) uu[j] = (j < L) ? U[(size_t)t * L + j] : cz();
-            for (int i = lane; i < t; i += 32) {
-                double2 z[LMAX];
-                double2 w0 = cz(), w1 = cz();
+            for (int rr = 0; rr < 2; ++rr) {
+                const int i = lane + 32 * rr;
+                if (rr == 1 && nb <= 32) break;
+                if (i < t) {
+                    double2 z[LMAX];
+                    double2 w0 = cz(), w1 = cz();
 #pragma unroll
-                for (int j = 0; j < LMAX; ++j) {
-                    if (j < L) {
-                        int sj = base + j;
-                        if (sj >= L) sj -= L;
-                        z[j] = Win[(size_t)sj * nb + i];
-                        if (j & 1) w1 = cfma(z[j], uu[j], w1);
-                        else w0 = cfma(z[j], uu[j], w0);
+                    for (int j = 0; j < LMAX; ++j) {
+                        if (j < L) {
+                            int sj = base + j;
+                            if (sj >= L) sj -= L;
+                            z[j] = Win[(size_t)sj * nb + i];
+                            if (j & 1) w1 = cfma(z[j], uu[j], w1);
+                            else w0 = cfma(z[j], uu[j], w0);
+                        }
                     }
-                }
-                const double2 tw = cmul(tau, cadd(w0, w1));
+                    const double2 tw = cmul(tau, cadd(w0, w1));
 #pragma unroll
-                for (int j = 0; j < LMAX; ++j) {
-                    if (j < L) {
-                        // z_j -= tau w conj(u_j)
-                        const double2 cu = make_double2(uu[j].x, -uu[j].y);
-                        int sj = base + j;
-                        if (sj >= L) sj -= L;
-                        Win[(size_t)sj * nb + i] = csub(z[j], cmul(tw, cu));
+                    for (int j = 0; j < LMAX; ++j) {
+                        if (j < L) {
+                            // z_j -= tau w conj(u_j)
+                            const double2 cu = make_double2(uu[j].x, -uu[j].y);
+                            int sj = base + j;
+                            if (sj >= L) sj -= L;
+                            Win[(size_t)sj * nb + i] = csub(z[j], cmul(tw, cu));
+                        }
                     }
                 }
             }
         }
-        __syncwarp();
         // ---- slide: column t+m retires, panel column t-1 enters its slot ----
-        if (t > 0) load_z1(t - 1, t);
+        if (t > 0) {
+            const int sl = base == 0 ? L - 1 : base - 1;  // slot of column t-1
+            double2* dst = Win + (size_t)sl * nb;
+            const int j = t - 1;
+            double2 v0 = make_double2(pf0, 0.0), v1 = make_double2(pf1, 0.0);
+            if (lane + m == j) v0 = csub(v0, sig);
+            if (lane + 32 + m == j) v1 = csub(v1, sig);
+            if (lane <= j) dst[lane] = v0;
+            if (lane + 32 <= j) dst[lane + 32] = v1;
+            if (t >= 2) prefetch(t - 2);
+        }
         __syncwarp();
     }
 

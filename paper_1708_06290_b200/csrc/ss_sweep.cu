@@ -422,6 +422,163 @@ struct SweepArgs {
     int32_t* fail;
 };
 
+// Per-part device buffers: Z2 ping-pong + P for the part's shifts.
+struct PartBufs {
+    double2* Z[2];
+    double2* P;
+};
+
+// Enqueue the whole sweep (seed, window steps, head) for shifts
+// [lo, lo + sb) of the call on stream `st`.
+int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs B, int nb0,
+                 int64_t LDZ, double rtol, bool use_house, int C, bool exact, cudaStream_t st) {
+    const int n = a.n, m = a.m;
+    const int ptop = a.mode == 0 ? a.p : n;
+    const int ncg = (m + C - 1) / C;
+    Dims d;
+    d.n = n;
+    d.m = m;
+    d.ptop = ptop;
+    d.ident_top = a.mode == 1;
+    d.A = a.A;
+    d.lda = a.lda;
+    d.T = a.C;
+    d.ldt = a.ldc;
+    d.shifts = a.shifts + lo;
+    d.sb = sb;
+    d.LDZ = LDZ;
+    {
+        dim3 g((unsigned)((LDZ + 255) / 256), (unsigned)sb);
+        k_seed<<<g, 256, 0, st>>>(d, B.Z[0], B.Z[1]);
+        SS_LAUNCH_CHECK(h);
+    }
+    int cur = 0;
+    int k = n;
+    while (k >= m + 1) {
+        Step s;
+        s.k = k;
+        s.nb = std::min(nb0, k - m);
+        s.mnb = std::min(m, s.nb);
+        s.r0 = ptop + k - s.nb;
+        s.c0 = k - m - s.nb;
+        s.nc = s.nb + m;
+        s.lmp = 0;
+        const ss::Sched* sc = ss::get_sched(h, s.nb, s.nc);
+        if (!sc) return ss::set_err(h, SS_ENOMEM, "schedule allocation failed");
+        s.steps = sc->steps;
+        s.rots = sc->rots;
+        s.rot = sc->d_rot;
+        s.joff = sc->d_job_off;
+        // ---- block RQ -> P (nc x m per shift, j-major) ----
+        cudaEvent_t ev = ss::timing_begin(h, st);
+        if (use_house) {
+            // one warp per shift: row-Householder block RQ (ss_rq_house.cuh)
+            RqDims rd;
+            rd.m = m;
+            rd.ptop = ptop;
+            rd.nb = s.nb;
+            rd.k = s.k;
+            rd.c0 = s.c0;
+            rd.r0 = s.r0;
+            rd.nc = s.nc;
+            rd.sb = sb;
+            rd.A = a.A;
+            rd.lda = a.lda;
+            rd.shifts = d.shifts;
+            rd.LDZ = LDZ;
+            const size_t sm = rqh_warp_smem(s.nb, m);
+            if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+        } else {
+            // the reference's scheduled Givens batch: one warp per concurrent
+            // rotation (<= 16 warps), rotation parameters in registers
+            const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
+            const int nw = std::max(1, std::min(sc->max_job, 16));
+            int per_warp = 0;
+            for (int t = 0; t < sc->steps; ++t) {
+                const int J = sc->job_off[t + 1] - sc->job_off[t];
+                per_warp += (J + nw - 1) / nw;
+            }
+            const int slots = (per_warp + 31) / 32;
+            if (slots <= 1) k_rq<1><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
+            else if (slots <= 2) k_rq<2><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
+            else if (slots <= 4) k_rq<4><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
+            else if (slots <= 8) k_rq<8><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
+            else return ss::set_err(h, SS_EARG, "window block too large for the register rotation store");
+        }
+        SS_LAUNCH_CHECK(h);
+        ss::timing_end(h, st, ev, ss::PH_RQ);
+        // ---- window update: S shifts per chunk, one warp per (shift, column
+        // group); smem sized for two resident CTAs per SM when it fits ----
+        UpdDims u;
+        u.n = n;
+        u.m = m;
+        u.ptop = ptop;
+        u.ident_top = d.ident_top;
+        u.A = a.A;
+        u.lda = a.lda;
+        u.T = a.C;
+        u.ldt = a.ldc;
+        u.shifts = d.shifts;
+        u.sb = sb;
+        u.LDZ = LDZ;
+        u.nb = s.nb;
+        u.mnb = s.mnb;
+        u.r0 = s.r0;
+        u.c0 = s.c0;
+        u.nc = s.nc;
+        u.rlo = a.mode == 1 ? s.c0 : 0;
+        u.S = std::max(1, 8 / ncg);
+        const size_t two_per_sm = h->smem_optin / 2 - 1024;
+        while (u.S > 1 && upd_smem_bytes(s.nb, m, u.S) > two_per_sm) u.S--;
+        u.SG = u.S * 4;
+        const int rows = s.r0 - u.rlo;
+        dim3 g((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
+        const size_t smem_u = upd_smem_bytes(s.nb, m, u.S);
+        // reference flop accounting (batched.py:58-61, solvers.py:194-199)
+        double rq_fl = 0.0;
+        for (int qq = 0; qq < sc->rots; ++qq) rq_fl += 20.0 * ((sc->rot[qq] & 0xffu) + s.nc) + 16.0;
+        h->flops[ss::PH_RQ] += rq_fl * sb;
+        const double fl_b = (double)sb * (8.0 * s.r0 * m * m + 8.0 * s.mnb * m);
+        const double fl_o = 8.0 * s.r0 * ((double)sb * m) * s.nb;
+        h->flops[ss::PH_BATCHED_GEMM] += fl_b;
+        h->flops[ss::PH_OUTER_GEMM] += fl_o;
+        // algorithmic flops of this launch: every structural
+        // nonzero of the panel rows it updates meets m complex columns once
+        const double nnz =
+            (a.mode == 0 ? (double)a.p * s.nb : (double)s.nb) + (double)(k - s.nb) * s.nb;
+        const double fl_alg = 4.0 * m * nnz * sb;
+        ev = ss::timing_begin(h, st);
+        int rc = launch_update(h, C, exact, g, 32 * u.S * ncg, smem_u, st, u, B.Z[cur],
+                               B.Z[cur ^ 1], B.P);
+        if (rc) return rc;
+        ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
+        cur ^= 1;
+        k -= s.nb;
+    }
+    HeadOut ho;
+    ho.mode = a.mode;
+    ho.B = a.B;
+    ho.ldb = a.ldb;
+    ho.bd = a.bd ? a.bd + lo * a.ldbd : nullptr;
+    ho.ldbd = a.ldbd;
+    ho.rtol = rtol;
+    ho.scal = h->d_scal;
+    ho.out = a.mode == 0 ? a.out + lo * m * a.ldo : a.out + lo * a.ldo;
+    ho.ldo = a.ldo;
+    ho.fail = a.fail + lo;
+    cudaEvent_t evh = ss::timing_begin(h, st);
+    const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
+    k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z[cur]);
+    SS_LAUNCH_CHECK(h);
+    ss::timing_end(h, st, evh, ss::PH_TAIL);
+    h->flops[ss::PH_TAIL] += a.mode == 0 ? (double)sb * 8.0 * a.p * m * m : (double)sb * 8.0 * n * m;
+    return SS_OK;
+}
+
 int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : n;
@@ -430,6 +587,28 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const double rtol = a.rtol > 0.0 ? a.rtol : 1e3 * n * 2.220446049250313e-16;
     const int nb0 = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
     const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
+
+    static bool attrs = false;
+    if (!attrs) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<1>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<2>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<4>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<8>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<2>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<4>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<8>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<16>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<32>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_head));
+        attrs = true;
+    }
+    // block RQ flavour: row Householder (one warp per shift) unless m+1 > 32
+    // or SS_BLOCK_RQ=givens selects the reference's scheduled Givens batch
+    const char* rqenv = getenv("SS_BLOCK_RQ");
+    const bool use_house = (m + 1 <= 32) && !(rqenv && strcmp(rqenv, "givens") == 0);
+    int C = 1;
+    bool exact = true;
+    pick_cols(m, C, exact);
 
     // fro2 / trace for the per-shift singularity thresholds
     {
@@ -460,179 +639,48 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256, 0);
         if (rc) return rc;
     }
-    double2* Zbuf[2];
-    Zbuf[0] = (double2*)h->ws;
-    Zbuf[1] = Zbuf[0] + (size_t)sb_max * m * LDZ;
-    double2* Pbuf = Zbuf[1] + (size_t)sb_max * m * LDZ;
+    double2* Z0 = (double2*)h->ws;
+    double2* Z1 = Z0 + (size_t)sb_max * m * LDZ;
+    double2* P0 = Z1 + (size_t)sb_max * m * LDZ;
 
-    // block RQ flavour: row Householder (one warp per shift) unless m+1 > 32
-    // or SS_BLOCK_RQ=givens selects the reference's scheduled Givens batch
-    const char* rqenv = getenv("SS_BLOCK_RQ");
-    const bool use_house = (m + 1 <= 32) && !(rqenv && strcmp(rqenv, "givens") == 0);
-    int C = 1;
-    bool exact = true;
-    pick_cols(m, C, exact);
-    const int ncg = (m + C - 1) / C;
-
-    static bool rq_attr = false;
-    if (!rq_attr) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<1>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<2>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<4>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq<8>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<2>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<4>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<8>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<16>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<32>));
-        SS_CUDA_TRY(h, allow_max_smem(h, k_head));
-        rq_attr = true;
+    // Independent halves of a batch on two streams: the latency-bound block
+    // RQ of one half overlaps the FP64-bound window update of the other.
+    const char* sv = getenv("SS_STREAMS");
+    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : 2;
+    if (sb_max < 64) NS = 1;
+    cudaStream_t streams[2] = {st, st};
+    if (NS == 2) {
+        if (!h->aux_stream) SS_CUDA_TRY(h, cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
+        streams[1] = h->aux_stream;
+        SS_CUDA_TRY(h, cudaEventRecord(h->ev_a, st));
+        SS_CUDA_TRY(h, cudaStreamWaitEvent(streams[1], h->ev_a, 0));
     }
-
     for (int64_t lo = 0; lo < a.s; lo += sb_max) {
         const int sb = (int)std::min<int64_t>(sb_max, a.s - lo);
-        Dims d;
-        d.n = n;
-        d.m = m;
-        d.ptop = ptop;
-        d.ident_top = a.mode == 1;
-        d.A = a.A;
-        d.lda = a.lda;
-        d.T = a.C;
-        d.ldt = a.ldc;
-        d.shifts = a.shifts + lo;
-        d.sb = sb;
-        d.LDZ = LDZ;
-        {
-            dim3 g((unsigned)((LDZ + 255) / 256), (unsigned)sb);
-            k_seed<<<g, 256, 0, st>>>(d, Zbuf[0], Zbuf[1]);
-            SS_LAUNCH_CHECK(h);
-        }
-        int cur = 0;
-        int k = n;
-        while (k >= m + 1) {
-            Step s;
-            s.k = k;
-            s.nb = std::min(nb0, k - m);
-            s.mnb = std::min(m, s.nb);
-            s.r0 = ptop + k - s.nb;
-            s.c0 = k - m - s.nb;
-            s.nc = s.nb + m;
-            const ss::Sched* sc = ss::get_sched(h, s.nb, s.nc);
-            if (!sc) return ss::set_err(h, SS_ENOMEM, "schedule allocation failed");
-            s.steps = sc->steps;
-            s.rots = sc->rots;
-            s.rot = sc->d_rot;
-            s.joff = sc->d_job_off;
-            // block RQ
-            cudaEvent_t ev = ss::timing_begin(h, st);
-            const size_t smem_rq = rq_smem_bytes(s.nb, m, s.steps, s.rots);
-            // one warp per concurrent rotation of the schedule (<= 16 warps)
-            if (use_house) {
-                // one warp per shift: row-Householder block RQ (ss_rq_house.cuh)
-                RqDims rd;
-                rd.m = m;
-                rd.ptop = ptop;
-                rd.nb = s.nb;
-                rd.k = s.k;
-                rd.c0 = s.c0;
-                rd.r0 = s.r0;
-                rd.nc = s.nc;
-                rd.sb = sb;
-                rd.A = a.A;
-                rd.lda = a.lda;
-                rd.shifts = d.shifts;
-                rd.LDZ = LDZ;
-                const size_t sm = rqh_warp_smem(s.nb, m);
-                if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
-                else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
-                else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
-                else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
-                else k_rq_house<32><<<sb, 32, sm, st>>>(rd, Zbuf[cur], Pbuf);
-            } else {
-            // one warp per concurrent rotation (<= 16 warps); rotation
-            // parameters live in registers: SLOTS x 32 per warp
-            const int nw = std::max(1, std::min(sc->max_job, 16));
-            int per_warp = 0;
-            for (int t = 0; t < sc->steps; ++t) {
-                const int J = sc->job_off[t + 1] - sc->job_off[t];
-                per_warp += (J + nw - 1) / nw;
-            }
-            const int slots = (per_warp + 31) / 32;
-            if (slots <= 1) k_rq<1><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
-            else if (slots <= 2) k_rq<2><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
-            else if (slots <= 4) k_rq<4><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
-            else if (slots <= 8) k_rq<8><<<sb, 32 * nw, smem_rq, st>>>(d, s, Zbuf[cur], Pbuf);
-            else return ss::set_err(h, SS_EARG, "window block too large for the register rotation store");
-            }
-            SS_LAUNCH_CHECK(h);
-            ss::timing_end(h, st, ev, ss::PH_RQ);
-            // window update: S shifts per chunk, one warp per (shift, column group),
-            // smem sized for two resident CTAs per SM when it fits
-            UpdDims u;
-            u.n = n;
-            u.m = m;
-            u.ptop = ptop;
-            u.ident_top = d.ident_top;
-            u.A = a.A;
-            u.lda = a.lda;
-            u.T = a.C;
-            u.ldt = a.ldc;
-            u.shifts = d.shifts;
-            u.sb = sb;
-            u.LDZ = LDZ;
-            u.nb = s.nb;
-            u.mnb = s.mnb;
-            u.r0 = s.r0;
-            u.c0 = s.c0;
-            u.nc = s.nc;
-            u.rlo = a.mode == 1 ? s.c0 : 0;
-            u.S = std::max(1, 8 / ncg);
-            const size_t two_per_sm = h->smem_optin / 2 - 1024;
-            while (u.S > 1 && upd_smem_bytes(s.nb, m, u.S) > two_per_sm) u.S--;
-            u.SG = u.S * 4;
-            const int rows = s.r0 - u.rlo;
-            dim3 g((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
-            const size_t smem_u = upd_smem_bytes(s.nb, m, u.S);
-            // reference flop accounting (batched.py:58-61, solvers.py:194-199)
-            double rq_fl = 0.0;
-            for (int qq = 0; qq < sc->rots; ++qq)
-                rq_fl += 20.0 * ((sc->rot[qq] & 0xffu) + s.nc) + 16.0;
-            h->flops[ss::PH_RQ] += rq_fl * sb;
-            const double fl_b = (double)sb * (8.0 * s.r0 * m * m + 8.0 * s.mnb * m);
-            const double fl_o = 8.0 * s.r0 * ((double)sb * m) * s.nb;
-            h->flops[ss::PH_BATCHED_GEMM] += fl_b;
-            h->flops[ss::PH_OUTER_GEMM] += fl_o;
-            // algorithmic flops of this launch: every structural
-            // nonzero of the panel rows it updates meets m complex columns once
-            const double nnz = (double)(a.mode == 0 ? (double)a.p * s.nb : (double)s.nb) +
-                               (double)(k - s.nb) * s.nb;
-            const double fl_alg = 4.0 * m * nnz * sb;
-            ev = ss::timing_begin(h, st);
-            int rc = launch_update(h, C, exact, g, 32 * u.S * ncg, smem_u, st, u, Zbuf[cur],
-                                   Zbuf[cur ^ 1], Pbuf);
+        const int parts = (NS == 2 && sb >= 64) ? 2 : 1;
+        int off = 0;
+        for (int p = 0; p < parts; ++p) {
+            const int cnt = sb / parts + (p < sb % parts ? 1 : 0);
+            PartBufs B;
+            B.Z[0] = Z0 + (size_t)off * m * LDZ;
+            B.Z[1] = Z1 + (size_t)off * m * LDZ;
+            B.P = P0 + (size_t)off * ncmax * m;
+            int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, C, exact,
+                                  streams[p]);
             if (rc) return rc;
-            ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
-            cur ^= 1;
-            k -= s.nb;
+            off += cnt;
         }
-        HeadOut ho;
-        ho.mode = a.mode;
-        ho.B = a.B;
-        ho.ldb = a.ldb;
-        ho.bd = a.bd ? a.bd + lo * a.ldbd : nullptr;
-        ho.ldbd = a.ldbd;
-        ho.rtol = rtol;
-        ho.scal = h->d_scal;
-        ho.out = a.mode == 0 ? a.out + lo * m * a.ldo : a.out + lo * a.ldo;
-        ho.ldo = a.ldo;
-        ho.fail = a.fail + lo;
-        cudaEvent_t evh = ss::timing_begin(h, st);
-        const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
-        k_head<<<sb, 128, smem_h, st>>>(d, ho, Zbuf[cur]);
-        SS_LAUNCH_CHECK(h);
-        ss::timing_end(h, st, evh, ss::PH_TAIL);
-        h->flops[ss::PH_TAIL] += a.mode == 0 ? (double)sb * 8.0 * a.p * m * m : (double)sb * 8.0 * n * m;
+        if (NS == 2 && lo + sb_max < a.s) {
+            // the next batch reuses both parts' buffers: join before reuse
+            SS_CUDA_TRY(h, cudaEventRecord(h->ev_b, streams[1]));
+            SS_CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_b, 0));
+            SS_CUDA_TRY(h, cudaEventRecord(h->ev_a, st));
+            SS_CUDA_TRY(h, cudaStreamWaitEvent(streams[1], h->ev_a, 0));
+        }
+    }
+    if (NS == 2) {
+        SS_CUDA_TRY(h, cudaEventRecord(h->ev_b, streams[1]));
+        SS_CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_b, 0));
     }
     return SS_OK;
 }
