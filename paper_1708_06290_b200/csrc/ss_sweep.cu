@@ -646,7 +646,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // Independent halves of a batch on two streams: the latency-bound block
     // RQ of one half overlaps the FP64-bound window update of the other.
     const char* sv = getenv("SS_STREAMS");
-    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : 2;
+    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : 1;
     if (sb_max < 64) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
