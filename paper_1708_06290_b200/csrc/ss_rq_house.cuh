@@ -46,15 +46,18 @@ __host__ __device__ inline size_t rqh_warp_smem(int nb, int m) {
     return (size_t)L * nb * 16 + (size_t)nb * L * 16 + (size_t)nb * 16;
 }
 
-// LMAX >= m+1, <= 32.  One warp per shift; WPC warps per CTA.
-template <int LMAX>
+// LMAX >= m+1, <= 32.  LFIX > 0 fixes L = m+1 at compile time (exact,
+// predicate-free unrolling for the common m); LFIX = 0 reads it at run time.
+template <int LMAX, int LFIX = 0>
 __global__ void __launch_bounds__(128)
     k_rq_house(RqDims d, const double2* __restrict__ Z2, double2* __restrict__ Pbuf) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int l = blockIdx.x * (blockDim.x >> 5) + warp;
     if (l >= d.sb) return;
-    const int nb = d.nb, m = d.m, L = m + 1;
+    const int nb = d.nb;
+    const int L = LFIX > 0 ? LFIX : d.m + 1;
+    const int m = L - 1;
     double2* Win = (double2*)(smem + (size_t)warp * rqh_warp_smem(nb, m));  // [L slots][nb rows]
     double2* U = Win + (size_t)L * nb;                                       // [nb][L]
     double2* Tau = U + (size_t)nb * L;                                       // [nb]

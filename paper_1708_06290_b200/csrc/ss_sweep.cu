@@ -345,49 +345,52 @@ cudaError_t allow_max_smem(ss_handle* h, F* fn) {
                                 (int)(h->smem_optin - fa.sharedSizeBytes));
 }
 
-template <int C, bool EXACT>
+// Register tile of the update kernel: lane = (row group, column group q < G),
+// R = 2G rows x C columns; a warp covers 64 rows x G*C columns.
+struct UpdTile {
+    int G = 1, C = 1;
+    bool exact = true;
+};
+
+UpdTile pick_tile(int m) {
+    UpdTile t;
+    if (m % 10 == 0) { t.G = 2; t.C = 5; }
+    else if (m % 8 == 0) { t.G = 2; t.C = 4; }
+    else if (m <= 8) { t.G = 1; t.C = m; }
+    else if (m % 5 == 0) { t.G = 1; t.C = 5; }
+    else { t.G = 2; t.C = 5; t.exact = false; }
+    return t;
+}
+
+template <int G, int C, bool EXACT>
 int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStream_t st,
                     const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
     static bool configured = false;
     if (!configured) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_update<C, EXACT>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT>));
         configured = true;
     }
-    k_update<C, EXACT><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
+    k_update<G, C, EXACT><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
 
-int launch_update(ss_handle* h, int C, bool exact, dim3 grid, int threads, size_t smem,
+int launch_update(ss_handle* h, const UpdTile& t, dim3 grid, int threads, size_t smem,
                   cudaStream_t st, const UpdDims& u, const double2* zin, double2* zout,
                   const double2* pbuf) {
-#define SS_CASE(K)                                                                           \
-    case K:                                                                                  \
-        return exact ? launch_update_t<K, true>(h, grid, threads, smem, st, u, zin, zout, pbuf) \
-                     : launch_update_t<K, false>(h, grid, threads, smem, st, u, zin, zout, pbuf);
-    switch (C) {
-        SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
-        default: return ss::set_err(h, SS_EARG, "unsupported column tile");
-    }
+    if (t.G == 2 && t.C == 5 && t.exact) return launch_update_t<2, 5, true>(h, grid, threads, smem, st, u, zin, zout, pbuf);
+    if (t.G == 2 && t.C == 5) return launch_update_t<2, 5, false>(h, grid, threads, smem, st, u, zin, zout, pbuf);
+    if (t.G == 2 && t.C == 4) return launch_update_t<2, 4, true>(h, grid, threads, smem, st, u, zin, zout, pbuf);
+    if (t.G == 1) {
+        switch (t.C) {
+#define SS_CASE(K) \
+    case K: return launch_update_t<1, K, true>(h, grid, threads, smem, st, u, zin, zout, pbuf);
+            SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
 #undef SS_CASE
-}
-
-// Columns per thread: the largest divisor of m in [4, 8] (exact tiles, no
-// predication); m < 4 -> m; otherwise 5 with a predicated last group.
-void pick_cols(int m, int& C, bool& exact) {
-    if (m <= 8 && (m <= 4 || m == 5 || m == 6 || m == 8)) {
-        C = m;
-        exact = true;
-        return;
-    }
-    for (int c = 8; c >= 4; --c)
-        if (m % c == 0) {
-            C = c;
-            exact = true;
-            return;
+            default: break;
         }
-    C = 5;
-    exact = false;
+    }
+    return ss::set_err(h, SS_EARG, "unsupported update tile");
 }
 
 int max_nb_for(ss_handle* h, int m, int nb_req) {
@@ -431,10 +434,10 @@ struct PartBufs {
 // Enqueue the whole sweep (seed, window steps, head) for shifts
 // [lo, lo + sb) of the call on stream `st`.
 int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs B, int nb0,
-                 int64_t LDZ, double rtol, bool use_house, int C, bool exact, cudaStream_t st) {
+                 int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, cudaStream_t st) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : n;
-    const int ncg = (m + C - 1) / C;
+    const int nws = (m + tile.G * tile.C - 1) / (tile.G * tile.C);  // warps per shift
     Dims d;
     d.n = n;
     d.m = m;
@@ -487,7 +490,11 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             rd.shifts = d.shifts;
             rd.LDZ = LDZ;
             const size_t sm = rqh_warp_smem(s.nb, m);
-            if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 5) k_rq_house<6, 6><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 10) k_rq_house<11, 11><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 20) k_rq_house<21, 21><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
             else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
             else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
             else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
@@ -531,7 +538,8 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         u.c0 = s.c0;
         u.nc = s.nc;
         u.rlo = a.mode == 1 ? s.c0 : 0;
-        u.S = std::max(1, 8 / ncg);
+        u.nws = nws;
+        u.S = std::max(1, 8 / nws);
         const size_t two_per_sm = h->smem_optin / 2 - 1024;
         while (u.S > 1 && upd_smem_bytes(s.nb, m, u.S) > two_per_sm) u.S--;
         u.SG = u.S * 4;
@@ -552,7 +560,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             (a.mode == 0 ? (double)a.p * s.nb : (double)s.nb) + (double)(k - s.nb) * s.nb;
         const double fl_alg = 4.0 * m * nnz * sb;
         ev = ss::timing_begin(h, st);
-        int rc = launch_update(h, C, exact, g, 32 * u.S * ncg, smem_u, st, u, B.Z[cur],
+        int rc = launch_update(h, tile, g, 32 * u.S * nws, smem_u, st, u, B.Z[cur],
                                B.Z[cur ^ 1], B.P);
         if (rc) return rc;
         ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
@@ -599,6 +607,10 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<8>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<16>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<32>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<2, 2>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<6, 6>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<11, 11>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<21, 21>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_head));
         attrs = true;
     }
@@ -606,9 +618,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // or SS_BLOCK_RQ=givens selects the reference's scheduled Givens batch
     const char* rqenv = getenv("SS_BLOCK_RQ");
     const bool use_house = (m + 1 <= 32) && !(rqenv && strcmp(rqenv, "givens") == 0);
-    int C = 1;
-    bool exact = true;
-    pick_cols(m, C, exact);
+    const UpdTile tile = pick_tile(m);
 
     // fro2 / trace for the per-shift singularity thresholds
     {
@@ -665,7 +675,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             B.Z[0] = Z0 + (size_t)off * m * LDZ;
             B.Z[1] = Z1 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * ncmax * m;
-            int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, C, exact,
+            int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, tile,
                                   streams[p]);
             if (rc) return rc;
             off += cnt;

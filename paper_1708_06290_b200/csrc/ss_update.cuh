@@ -4,15 +4,20 @@
 //                  - sigma_l P_l[i - (r0 - m), :]        (lazy-shift rows only)
 //
 // reference solvers.py:186-199 (update_shift + gemm_acc).  Pan is the real,
-// shift-independent panel [top; Ahat][0:r0, c0:c0+nb].
+// shift-independent panel [top; Ahat][0:r0, c0:c0+nb]; P_l is j-major.
 //
-// Tiling: a CTA owns one 64-row tile of the panel (staged once in shared
-// memory, reused by all SG shifts the CTA processes) and walks its shifts in
-// chunks of S.  Per chunk, P_l (nc x m) and the 64 x m tile of Zin_l for the
-// S shifts are staged with cp.async (zero-filled past r0).  Warp w owns one
-// (shift, C-column group) unit of the chunk: lane L computes rows
-// (2L, 2L+1) x C complex columns in registers; P_l entries are warp-uniform shared
-// memory broadcasts, panel / Zin entries are per-lane conflict-free loads.
+// Tiling (sized from measured B200 shared-memory costs: a per-lane LDS.128
+// is 4 LSU cycles, a broadcast LDS.128 2 cycles, 64 DFMA/clk/SM):
+//  * a CTA owns one 64-row tile of the panel, staged once (cp.async) and
+//    reused by every shift of its group (SG shifts, chunks of S);
+//  * per chunk, P_l and the 64 x m tile of Zin_l of the S shifts are staged
+//    with cp.async (zero-filled past r0);
+//  * a warp owns one (shift, column block of G*C columns) unit; lane =
+//    (row group rg, column group q): R = 2G consecutive rows x C columns in
+//    registers.  For m = 10: G = 2, C = 5, R = 4 -> per panel column j a
+//    warp issues 2 panel LDS.128 (pair-interleaved layout, 2 wavefronts
+//    each), 5 P LDS.128 (two broadcast addresses) and 40 DFMA: 14 LSU
+//    cycles per 20 FP64-pipe cycles.
 #pragma once
 
 #include "ss_device.cuh"
@@ -34,7 +39,7 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
     asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-constexpr int kUpdRows = 64;  // rows per tile: 2 per lane
+constexpr int kUpdRows = 64;  // rows per tile
 
 struct UpdDims {
     int n, m, ptop, ident_top;
@@ -51,6 +56,7 @@ struct UpdDims {
     int rlo;  // first row of tile 0
     int S;    // shifts per chunk
     int SG;   // shifts per CTA
+    int nws;  // warps (column blocks) per shift
 };
 
 __host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S) {
@@ -58,39 +64,52 @@ __host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S) {
     return (size_t)nb * kUpdRows * 8 + (size_t)S * nc * m * 16 + (size_t)S * m * kUpdRows * 16;
 }
 
-template <int C, bool EXACT>
+// panel position of tile row `row` (0..63) inside one panel column: rows of
+// a lane's row group are stored as R/2 pairs; pair p of every row group is
+// contiguous across row groups so one LDS.128 touches 256 contiguous bytes.
+template <int G>
+__device__ __forceinline__ int pan_index(int row) {
+    constexpr int R = 2 * G, RG = 32 / G;
+    const int rg = row / R, w = row - rg * R, p = w >> 1, e = w & 1;
+    return p * (2 * RG) + rg * 2 + e;
+}
+
+template <int G, int C, bool EXACT>
 __global__ void __launch_bounds__(256)
     k_update(UpdDims u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
              const double2* __restrict__ Pbuf) {
+    constexpr int R = 2 * G, RG = 32 / G;
     extern __shared__ __align__(16) unsigned char smem[];
     const int nb = u.nb, m = u.m, nc = u.nc, r0 = u.r0;
-    double* Pan = (double*)smem;                                        // [nb][64]
-    double2* Pst = (double2*)(smem + (size_t)nb * kUpdRows * 8);        // [S][nc*m]
+    double* Pan = (double*)smem;                                        // [nb][64] (pair-interleaved)
+    double2* Pst = (double2*)(smem + (size_t)nb * kUpdRows * 8);        // [S][nc*m], j-major
     double2* Zst = Pst + (size_t)u.S * nc * m;                          // [S][m][64]
     const int i0 = u.rlo + blockIdx.x * kUpdRows;
     const int l0 = blockIdx.y * u.SG;
     const int lend = min(l0 + u.SG, u.sb);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ncg = (m + C - 1) / C;
 
     // ---- panel tile (once per CTA) ----
     for (int v = tid; v < nb * kUpdRows; v += blockDim.x) {
-        const int j = v >> 6, ii = v & 63;
-        const int i = i0 + ii, col = u.c0 + j;
+        const int j = v >> 6, rr = v & 63;
+        const int i = i0 + rr, col = u.c0 + j;
+        double* dst = Pan + j * kUpdRows + pan_index<G>(rr);
         if (i >= r0) {
-            Pan[v] = 0.0;
+            *dst = 0.0;
         } else if (i >= u.ptop) {
-            cp_async8(Pan + v, u.A + (i - u.ptop) + (int64_t)col * u.lda, true);
+            cp_async8(dst, u.A + (i - u.ptop) + (int64_t)col * u.lda, true);
         } else if (u.ident_top) {
-            Pan[v] = (i == col) ? 1.0 : 0.0;
+            *dst = (i == col) ? 1.0 : 0.0;
         } else {
-            cp_async8(Pan + v, u.T + i + (int64_t)col * u.ldt, true);
+            cp_async8(dst, u.T + i + (int64_t)col * u.ldt, true);
         }
     }
 
-    const int s_w = warp / ncg, g = warp - s_w * ncg;  // this warp's unit
-    const int cb = g * C;
-    const int row_a = i0 + 2 * lane, row_b = row_a + 1;  // adjacent rows: 16-byte panel loads
+    const int s_w = warp / u.nws, blk = warp - s_w * u.nws;  // this warp's unit
+    const int rg = lane / G, q = lane - rg * G;
+    const int cb = blk * (G * C) + q * C;                     // first output column of this lane
+    const int ncol = EXACT ? C : max(0, min(C, m - cb));
+    const int rbase = rg * R;                                 // first tile row of this lane
     const int dlo = r0 - m;
 
     for (int lc = l0; lc < lend; lc += u.S) {
@@ -114,54 +133,61 @@ __global__ void __launch_bounds__(256)
         __syncthreads();
         if (s_w >= nsc) continue;
         const int l = lc + s_w;
-        const double2* Pl = Pst + (size_t)s_w * nc * m;
-        const double2* Zl = Zst + (size_t)s_w * m * kUpdRows;
-        const int ncol = EXACT ? C : min(C, m - cb);
-        double2 acc0[C], acc1[C];
+        const double2* Pl = Pst + (size_t)s_w * nc * m + cb;
+        const double2* Zl = Zst + (size_t)s_w * m * kUpdRows + rbase;
+        double2 acc[R][C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) acc0[c] = acc1[c] = cz();
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[r][c] = cz();
         // Z1 (real panel) part -- the reference's outer GEMM
-#pragma unroll 4
+        const double* pan_l = Pan + rg * 2;
+#pragma unroll 2
         for (int j = 0; j < nb; ++j) {
-            const double2 a01 = *reinterpret_cast<const double2*>(Pan + j * kUpdRows + 2 * lane);
-            const double a0 = a01.x, a1 = a01.y;
+            double a[R];
+#pragma unroll
+            for (int p = 0; p < R / 2; ++p) {
+                const double2 v = *reinterpret_cast<const double2*>(pan_l + j * kUpdRows + p * (2 * RG));
+                a[2 * p] = v.x;
+                a[2 * p + 1] = v.y;
+            }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (EXACT || c < ncol) {
-                    const double2 p = Pl[j * m + cb + c];
-                    acc0[c] = rfma(a0, p, acc0[c]);
-                    acc1[c] = rfma(a1, p, acc1[c]);
+                    const double2 pv = Pl[j * m + c];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
                 }
             }
         }
         // Z2 part -- the reference's per-shift batched GEMM
-#pragma unroll 2
         for (int j = 0; j < m; ++j) {
-            const double2 z0 = Zl[j * kUpdRows + 2 * lane], z1 = Zl[j * kUpdRows + 2 * lane + 1];
+            double2 z[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) z[r] = Zl[j * kUpdRows + r];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (EXACT || c < ncol) {
-                    const double2 p = Pl[(nb + j) * m + cb + c];
-                    acc0[c] = cfma(z0, p, acc0[c]);
-                    acc1[c] = cfma(z1, p, acc1[c]);
+                    const double2 pv = Pl[(nb + j) * m + c];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
                 }
             }
         }
         const double2 sig = u.shifts[l];
         double2* zo = Zout + ((int64_t)l * m + cb) * u.LDZ;
-        const int da = row_a - dlo, db = row_b - dlo;
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            if (EXACT || c < ncol) {
-                if (row_a < r0) {
-                    double2 v = acc0[c];
-                    if (da >= 0 && da < u.mnb) v = csub(v, cmul(sig, Pl[da * m + cb + c]));
-                    zo[(int64_t)c * u.LDZ + row_a] = v;
-                }
-                if (row_b < r0) {
-                    double2 v = acc1[c];
-                    if (db >= 0 && db < u.mnb) v = csub(v, cmul(sig, Pl[db * m + cb + c]));
-                    zo[(int64_t)c * u.LDZ + row_b] = v;
+        for (int r = 0; r < R; ++r) {
+            const int row = i0 + rbase + r;
+            if (row >= r0) continue;
+            const int dd = row - dlo;
+            const bool corr = dd >= 0 && dd < u.mnb;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (EXACT || c < ncol) {
+                    double2 v = acc[r][c];
+                    if (corr) v = csub(v, cmul(sig, Pl[dd * m + c]));
+                    zo[(int64_t)c * u.LDZ + row] = v;
                 }
             }
         }
