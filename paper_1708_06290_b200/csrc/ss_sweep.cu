@@ -539,7 +539,11 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         u.nc = s.nc;
         u.rlo = a.mode == 1 ? s.c0 : 0;
         u.nws = nws;
-        u.S = std::max(1, 8 / nws);
+        // a warp pair splits the panel K range of one (shift, column block) when
+        // one block covers all m columns: twice the warps on the same staging
+        u.ksplit = (nws == 1) ? 2 : 1;
+        u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2));
+        u.S = std::max(1, 8 / (nws * u.ksplit));
         const size_t two_per_sm = h->smem_optin / 2 - 1024;
         while (u.S > 1 && upd_smem_bytes(s.nb, m, u.S) > two_per_sm) u.S--;
         u.SG = u.S * 4;
@@ -560,7 +564,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             (a.mode == 0 ? (double)a.p * s.nb : (double)s.nb) + (double)(k - s.nb) * s.nb;
         const double fl_alg = 4.0 * m * nnz * sb;
         ev = ss::timing_begin(h, st);
-        int rc = launch_update(h, tile, g, 32 * u.S * nws, smem_u, st, u, B.Z[cur],
+        int rc = launch_update(h, tile, g, 32 * u.S * nws * u.ksplit, smem_u, st, u, B.Z[cur],
                                B.Z[cur ^ 1], B.P);
         if (rc) return rc;
         ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);

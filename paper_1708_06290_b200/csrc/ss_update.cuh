@@ -56,7 +56,9 @@ struct UpdDims {
     int rlo;  // first row of tile 0
     int S;    // shifts per chunk
     int SG;   // shifts per CTA
-    int nws;  // warps (column blocks) per shift
+    int nws;     // column blocks per shift
+    int ksplit;  // warps per (shift, column block): 1, or 2 = panel K range split
+    int jh;      // ksplit == 2: warp half 0 takes panel columns [0, jh) + the Z2 part
 };
 
 __host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S) {
@@ -105,12 +107,15 @@ __global__ void __launch_bounds__(256)
         }
     }
 
-    const int s_w = warp / u.nws, blk = warp - s_w * u.nws;  // this warp's unit
+    const int unit = warp / u.ksplit, half = warp - unit * u.ksplit;
+    const int s_w = unit / u.nws, blk = unit - s_w * u.nws;  // this warp's (shift, column block)
     const int rg = lane / G, q = lane - rg * G;
     const int cb = blk * (G * C) + q * C;                     // first output column of this lane
     const int ncol = EXACT ? C : max(0, min(C, m - cb));
     const int rbase = rg * R;                                 // first tile row of this lane
     const int dlo = r0 - m;
+    const int jlo = half == 0 ? 0 : u.jh;
+    const int jhi = (u.ksplit == 1 || half == 1) ? nb : u.jh;
 
     for (int lc = l0; lc < lend; lc += u.S) {
         const int nsc = min(u.S, lend - lc);
@@ -134,7 +139,8 @@ __global__ void __launch_bounds__(256)
         if (s_w >= nsc) continue;
         const int l = lc + s_w;
         const double2* Pl = Pst + (size_t)s_w * nc * m + cb;
-        const double2* Zl = Zst + (size_t)s_w * m * kUpdRows + rbase;
+        double2* Zs = Zst + (size_t)s_w * m * kUpdRows;
+        const double2* Zl = Zs + rbase;
         double2 acc[R][C];
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(256)
         // Z1 (real panel) part -- the reference's outer GEMM
         const double* pan_l = Pan + rg * 2;
 #pragma unroll 2
-        for (int j = 0; j < nb; ++j) {
+        for (int j = jlo; j < jhi; ++j) {
             double a[R];
 #pragma unroll
             for (int p = 0; p < R / 2; ++p) {
@@ -160,19 +166,42 @@ __global__ void __launch_bounds__(256)
                 }
             }
         }
-        // Z2 part -- the reference's per-shift batched GEMM
-        for (int j = 0; j < m; ++j) {
-            double2 z[R];
+        // Z2 part -- the reference's per-shift batched GEMM (warp half 0)
+        if (half == 0) {
+            for (int j = 0; j < m; ++j) {
+                double2 z[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) z[r] = Zl[j * kUpdRows + r];
+                for (int r = 0; r < R; ++r) z[r] = Zl[j * kUpdRows + r];
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                if (EXACT || c < ncol) {
-                    const double2 pv = Pl[(nb + j) * m + c];
+                for (int c = 0; c < C; ++c) {
+                    if (EXACT || c < ncol) {
+                        const double2 pv = Pl[(nb + j) * m + c];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
+                        for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
+                    }
                 }
             }
+        }
+        if (u.ksplit == 2) {
+            // half 1 hands its partial sums to half 0 through this shift's (now
+            // consumed) Z2 staging tile: [c][64 rows] per column block
+            const int bar = 1 + unit;
+            asm volatile("bar.sync %0, 64;\n" ::"r"(bar));   // half 0 done reading Zs
+            double2* red = Zs + (size_t)blk * (G * C) * kUpdRows;
+            if (half == 1) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int c = 0; c < C; ++c)
+                        if (EXACT || c < ncol) red[(size_t)(q * C + c) * kUpdRows + rbase + r] = acc[r][c];
+            }
+            asm volatile("bar.sync %0, 64;\n" ::"r"(bar));   // partials visible
+            if (half == 1) continue;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if (EXACT || c < ncol) acc[r][c] = cadd(acc[r][c], red[(size_t)(q * C + c) * kUpdRows + rbase + r]);
         }
         const double2 sig = u.shifts[l];
         double2* zo = Zout + ((int64_t)l * m + cb) * u.LDZ;
