@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(256)
 
     const int unit = warp / u.ksplit, half = warp - unit * u.ksplit;
     const int s_w = unit / u.nws, blk = unit - s_w * u.nws;  // this warp's (shift, column block)
-    const int rg = lane / G, q = lane - rg * G;
+    // half-warps take the column groups (q = lane / RG): a P broadcast then
+    // serves two contiguous 16-lane groups; rows repeat across half-warps
+    const int q = lane / RG, rg = lane - q * RG;
     const int cb = blk * (G * C) + q * C;                     // first output column of this lane
     const int ncol = EXACT ? C : max(0, min(C, m - cb));
     const int rbase = rg * R;                                 // first tile row of this lane

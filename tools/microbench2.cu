@@ -24,6 +24,9 @@ __global__ void tp_lds(int iters, double* out) {
             if (MODE == 2) { double v = b64[base + u * 32 + lane]; acc0 += v; }
             if (MODE == 3) { double v = b64[base + u]; acc0 += v; }
             if (MODE == 4) { double2 v = buf[base + u * 2 + (lane >> 4)]; acc0 += v.x; acc1 += v.y; }
+            if (MODE == 5) { double2 v = buf[base + u * 2 + (lane & 1)]; acc0 += v.x; acc1 += v.y; }
+            if (MODE == 6) { double2 v = buf[base + u * 32 + (lane & 15)]; acc0 += v.x; acc1 += v.y; }
+            if (MODE == 7) { double2 v = buf[base + u * 32 + (lane >> 1)]; acc0 += v.x; acc1 += v.y; }
         }
     }
     if (acc0 + acc1 + acc2 + acc3 == 1234.5) out[0] = acc0;
@@ -77,6 +80,9 @@ int main() {
     TP(1, "LDS.128 per-lane");
     TP(2, "LDS.64 per-lane");
     TP(3, "LDS.64 broadcast");
-    TP(4, "LDS.128 two addresses");
+    TP(4, "LDS.128 two addresses (half-warps)");
+    TP(5, "LDS.128 two addresses (odd/even)");
+    TP(6, "LDS.128 16 distinct (lane&15)");
+    TP(7, "LDS.128 16 distinct (lane>>1)");
     return 0;
 }
