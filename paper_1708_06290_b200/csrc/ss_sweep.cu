@@ -541,7 +541,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         u.nws = nws;
         // a warp pair splits the panel K range of one (shift, column block) when
         // one block covers all m columns: twice the warps on the same staging
-        u.ksplit = (nws == 1) ? 2 : 1;
+        u.ksplit = (nws == 1 && tile.exact) ? 2 : 1;  // scratch = the shift's m x 64 Z2 stage
         u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2));
         u.S = std::max(1, 8 / (nws * u.ksplit));
         const size_t two_per_sm = h->smem_optin / 2 - 1024;

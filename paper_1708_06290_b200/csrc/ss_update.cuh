@@ -109,9 +109,10 @@ __global__ void __launch_bounds__(256)
 
     const int unit = warp / u.ksplit, half = warp - unit * u.ksplit;
     const int s_w = unit / u.nws, blk = unit - s_w * u.nws;  // this warp's (shift, column block)
-    // half-warps take the column groups (q = lane / RG): a P broadcast then
-    // serves two contiguous 16-lane groups; rows repeat across half-warps
-    const int q = lane / RG, rg = lane - q * RG;
+    // adjacent lanes share a row group (q = lane % G): measured on B200 an
+    // LDS.128 costs one cycle per half-warp per 128 distinct bytes, so the
+    // pair-sharing pattern keeps both panel and P loads at 2 cycles
+    const int rg = lane / G, q = lane - rg * G;
     const int cb = blk * (G * C) + q * C;                     // first output column of this lane
     const int ncol = EXACT ? C : max(0, min(C, m - cb));
     const int rbase = rg * R;                                 // first tile row of this lane
@@ -133,7 +134,10 @@ __global__ void __launch_bounds__(256)
                 const int i = i0 + ii;
                 const bool ok = i < r0;
                 const double2* zp = Zin + ((int64_t)(lc + s) * m + c) * u.LDZ + (ok ? i : 0);
-                cp_async16(Zst + v, zp, ok);
+                // row ii = rg*R + w lives at w*RG + rg: a lane's R rows are R
+                // conflict-free LDS.128 at stride RG
+                const int zrg = ii / R, zw = ii - zrg * R;
+                cp_async16(Zst + (v - ii) + zw * RG + zrg, zp, ok);
             }
         }
         cp_async_commit_wait_all();
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(256)
         const int l = lc + s_w;
         const double2* Pl = Pst + (size_t)s_w * nc * m + cb;
         double2* Zs = Zst + (size_t)s_w * m * kUpdRows;
-        const double2* Zl = Zs + rbase;
+        const double2* Zl = Zs + rg;
         double2 acc[R][C];
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(256)
             for (int j = 0; j < m; ++j) {
                 double2 z[R];
 #pragma unroll
-                for (int r = 0; r < R; ++r) z[r] = Zl[j * kUpdRows + r];
+                for (int r = 0; r < R; ++r) z[r] = Zl[j * kUpdRows + r * RG];
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     if (EXACT || c < ncol) {
@@ -189,13 +193,14 @@ __global__ void __launch_bounds__(256)
             // consumed) Z2 staging tile: [c][64 rows] per column block
             const int bar = 1 + unit;
             asm volatile("bar.sync %0, 64;\n" ::"r"(bar));   // half 0 done reading Zs
-            double2* red = Zs + (size_t)blk * (G * C) * kUpdRows;
+            // scratch [(r*C + c)][lane]: conflict-free 16-byte stores / loads
+            double2* red = Zs + lane;
             if (half == 1) {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
 #pragma unroll
                     for (int c = 0; c < C; ++c)
-                        if (EXACT || c < ncol) red[(size_t)(q * C + c) * kUpdRows + rbase + r] = acc[r][c];
+                        if (EXACT || c < ncol) red[(r * C + c) * 32] = acc[r][c];
             }
             asm volatile("bar.sync %0, 64;\n" ::"r"(bar));   // partials visible
             if (half == 1) continue;
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(256)
             for (int r = 0; r < R; ++r)
 #pragma unroll
                 for (int c = 0; c < C; ++c)
-                    if (EXACT || c < ncol) acc[r][c] = cadd(acc[r][c], red[(size_t)(q * C + c) * kUpdRows + rbase + r]);
+                    if (EXACT || c < ncol) acc[r][c] = cadd(acc[r][c], red[(r * C + c) * 32]);
         }
         const double2 sig = u.shifts[l];
         double2* zo = Zout + ((int64_t)l * m + cb) * u.LDZ;
