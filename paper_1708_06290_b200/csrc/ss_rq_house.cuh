@@ -41,66 +41,66 @@ struct RqDims {
     int64_t LDZ;
 };
 
+// shared memory of one k_rq_house block (one shift)
 __host__ __device__ inline size_t rqh_warp_smem(int nb, int m) {
     const int L = m + 1;
     return (size_t)L * nb * 16 + (size_t)nb * L * 16 + (size_t)nb * 16;
 }
 
-// LMAX >= m+1, <= 32.  LFIX > 0 fixes L = m+1 at compile time (exact,
-// predicate-free unrolling for the common m); LFIX = 0 reads it at run time.
+// Two warps per shift block: lane i of warp w owns block row 32w + i (nb <=
+// 64).  Each warp rebuilds the reflector of row t from broadcast loads (no
+// shuffles, no hand-off), updates its own row, and one CTA barrier per step
+// publishes row t-1 for the next reflector.  The panel column entering the
+// window is prefetched one step ahead from global memory.  The reverse
+// accumulation (lanes = columns of W, registers) runs on warp 0.
+// LMAX >= m+1, <= 32; LFIX > 0 fixes L = m+1 at compile time.
 template <int LMAX, int LFIX = 0>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(64)
     k_rq_house(RqDims d, const double2* __restrict__ Z2, double2* __restrict__ Pbuf) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int l = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (l >= d.sb) return;
+    const int l = blockIdx.x;
     const int nb = d.nb;
     const int L = LFIX > 0 ? LFIX : d.m + 1;
     const int m = L - 1;
-    double2* Win = (double2*)(smem + (size_t)warp * rqh_warp_smem(nb, m));  // [L slots][nb rows]
-    double2* U = Win + (size_t)L * nb;                                       // [nb][L]
-    double2* Tau = U + (size_t)nb * L;                                       // [nb]
+    double2* Win = (double2*)smem;           // [L slots][nb rows]
+    double2* U = Win + (size_t)L * nb;       // [nb][L]
+    double2* Tau = U + (size_t)nb * L;       // [nb]
     const double2 sig = d.shifts[l];
     const int arow0 = d.k - nb;  // A row of block row 0
+    const int i = 32 * warp + lane;  // this thread's block row
 
     // initial window: columns nb-1 .. nb-1+m  (Z1 column nb-1 and the m Z2 columns)
-    {
-        double2* dst = Win + (size_t)((nb - 1) % L) * nb;
+    if (i < nb) {
         const double* src = d.A + arow0 + (int64_t)(d.c0 + nb - 1) * d.lda;
-        for (int i = lane; i < nb; i += 32) {
-            double2 v = make_double2(src[i], 0.0);
-            if (i + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
-            dst[i] = v;
+        double2 v = make_double2(src[i], 0.0);
+        if (i + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
+        Win[(size_t)((nb - 1) % L) * nb + i] = v;
+        for (int c = 0; c < m; ++c) {
+            const int j = nb + c;
+            Win[(size_t)(j % L) * nb + i] = Z2[((int64_t)l * m + c) * d.LDZ + d.r0 + i];
         }
     }
-    for (int c = 0; c < m; ++c) {
-        const int j = nb + c;
-        double2* dst = Win + (size_t)(j % L) * nb;
-        const double2* src = Z2 + ((int64_t)l * m + c) * d.LDZ + d.r0;
-        for (int i = lane; i < nb; i += 32) dst[i] = src[i];
-    }
-    // prefetch of the panel column entering next (rows lane, lane+32)
-    double pf0 = 0.0, pf1 = 0.0;
-    auto prefetch = [&](int j) {  // column j, rows 0..j
-        const double* src = d.A + arow0 + (int64_t)(d.c0 + j) * d.lda;
-        pf0 = (lane <= j) ? src[lane] : 0.0;
-        pf1 = (lane + 32 <= j) ? src[lane + 32] : 0.0;
-    };
-    if (nb >= 2) prefetch(nb - 2);
-    __syncwarp();
+    double pf = 0.0;  // prefetched entry (row i) of the panel column entering next
+    if (nb >= 2 && i <= nb - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + nb - 2) * d.lda];
+    __syncthreads();
 
+    int base = (nb - 1) % L;  // slot of column t
     for (int t = nb - 1; t >= 0; --t) {
-        const int base = t % L;  // slot of column t; column t+j sits in slot (base+j) mod L
-        // ---- every lane builds the reflector of row t from broadcast loads ----
+        double2* col[LMAX];  // slot pointers of columns t .. t+m
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) {
+            int sj = base + j;
+            if (sj >= L) sj -= L;
+            col[j] = Win + (size_t)sj * nb;
+        }
+        // ---- reflector of row t (every lane, from broadcast loads) ----
         double2 y[LMAX];
         double s2a = 0.0, s2b = 0.0;
 #pragma unroll
         for (int j = 0; j < LMAX; ++j) {
             if (j < L) {
-                int sj = base + j;
-                if (sj >= L) sj -= L;
-                const double2 x = Win[(size_t)sj * nb + t];
+                const double2 x = col[j][t];
                 y[j] = make_double2(x.x, -x.y);  // conj(row t)
                 if (j < L - 1) {
                     if (j & 1) s2b = fma(y[j].x, y[j].x, fma(y[j].y, y[j].y, s2b));
@@ -128,63 +128,54 @@ __global__ void __launch_bounds__(128)
         }
         double2 uu[LMAX];
 #pragma unroll
-        for (int j = 0; j < LMAX; ++j) uu[j] = (j < L - 1) ? cmul(y[j], scale) : (j == L - 1 ? make_double2(1.0, 0.0) : cz());
-        if (lane < L) {
+        for (int j = 0; j < LMAX; ++j)
+            uu[j] = (j < L - 1) ? cmul(y[j], scale) : (j == L - 1 ? make_double2(1.0, 0.0) : cz());
+        if (warp == 0) {
+            if (lane < L) {
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j)
-                if (j == lane) U[(size_t)t * L + j] = uu[j];
+                for (int j = 0; j < LMAX; ++j)
+                    if (j == lane) U[(size_t)t * L + j] = uu[j];
+            }
+            if (lane == 0) Tau[t] = tau;
         }
-        if (lane == 0) Tau[t] = tau;
-        // ---- rows 0..t-1 (lanes own rows lane, lane+32): z <- z - tau (z u) u^H ----
-        const bool act = t > 0 && (tau.x != 0.0 || tau.y != 0.0);
-        if (act) {
+        // ---- own row i < t: z <- z - tau (z u) u^H ----
+        if (i < t && (tau.x != 0.0 || tau.y != 0.0)) {
+            double2 z[LMAX];
+            double2 w0 = cz(), w1 = cz();
 #pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int i = lane + 32 * rr;
-                if (rr == 1 && nb <= 32) break;
-                if (i < t) {
-                    double2 z[LMAX];
-                    double2 w0 = cz(), w1 = cz();
+            for (int j = 0; j < LMAX; ++j) {
+                if (j < L) {
+                    z[j] = col[j][i];
+                    if (j & 1) w1 = cfma(z[j], uu[j], w1);
+                    else w0 = cfma(z[j], uu[j], w0);
+                }
+            }
+            const double2 tw = cmul(tau, cadd(w0, w1));
 #pragma unroll
-                    for (int j = 0; j < LMAX; ++j) {
-                        if (j < L) {
-                            int sj = base + j;
-                            if (sj >= L) sj -= L;
-                            z[j] = Win[(size_t)sj * nb + i];
-                            if (j & 1) w1 = cfma(z[j], uu[j], w1);
-                            else w0 = cfma(z[j], uu[j], w0);
-                        }
-                    }
-                    const double2 tw = cmul(tau, cadd(w0, w1));
-#pragma unroll
-                    for (int j = 0; j < LMAX; ++j) {
-                        if (j < L) {
-                            // z_j -= tau w conj(u_j)
-                            const double2 cu = make_double2(uu[j].x, -uu[j].y);
-                            int sj = base + j;
-                            if (sj >= L) sj -= L;
-                            Win[(size_t)sj * nb + i] = csub(z[j], cmul(tw, cu));
-                        }
-                    }
+            for (int j = 0; j < LMAX; ++j) {
+                if (j < L) {
+                    const double2 cu = make_double2(uu[j].x, -uu[j].y);  // z_j -= tau w conj(u_j)
+                    col[j][i] = csub(z[j], cmul(tw, cu));
                 }
             }
         }
-        // ---- slide: column t+m retires, panel column t-1 enters its slot ----
+        // ---- slide: column t+m retires, panel column t-1 enters slot (base-1) ----
         if (t > 0) {
-            const int sl = base == 0 ? L - 1 : base - 1;  // slot of column t-1
-            double2* dst = Win + (size_t)sl * nb;
+            const int sl = base == 0 ? L - 1 : base - 1;
             const int j = t - 1;
-            double2 v0 = make_double2(pf0, 0.0), v1 = make_double2(pf1, 0.0);
-            if (lane + m == j) v0 = csub(v0, sig);
-            if (lane + 32 + m == j) v1 = csub(v1, sig);
-            if (lane <= j) dst[lane] = v0;
-            if (lane + 32 <= j) dst[lane + 32] = v1;
-            if (t >= 2) prefetch(t - 2);
+            if (i <= j) {
+                double2 v = make_double2(pf, 0.0);
+                if (i + m == j) v = csub(v, sig);
+                Win[(size_t)sl * nb + i] = v;
+            }
+            if (t >= 2 && i <= t - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + t - 2) * d.lda];
+            base = sl;
         }
-        __syncwarp();
+        __syncthreads();
     }
 
-    // ---- reverse accumulation in registers: lane cc owns column cc of W ----
+    // ---- reverse accumulation in registers (warp 0): lane cc owns column cc ----
+    if (warp != 0) return;
     double2* dstP = Pbuf + (int64_t)l * d.nc * m;  // j-major: P[j*m + cc]
     for (int cc0 = 0; cc0 < m; cc0 += 32) {
         const int cc = cc0 + lane;
@@ -212,7 +203,6 @@ __global__ void __launch_bounds__(128)
             for (int j = 0; j < LMAX - 1; ++j) w[j] = w[j + 1];
             w[LMAX - 1] = cz();
         }
-        // rows nb .. nb+m-1 remain in the window
         if (cc < m) {
 #pragma unroll
             for (int j = 0; j < LMAX; ++j)

@@ -490,15 +490,15 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             rd.shifts = d.shifts;
             rd.LDZ = LDZ;
             const size_t sm = rqh_warp_smem(s.nb, m);
-            if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 5) k_rq_house<6, 6><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 10) k_rq_house<11, 11><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 20) k_rq_house<21, 21><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            if (m == 1) k_rq_house<2, 2><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 5) k_rq_house<6, 6><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 10) k_rq_house<11, 11><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 20) k_rq_house<21, 21><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 2) k_rq_house<2><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 4) k_rq_house<4><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 8) k_rq_house<8><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 16) k_rq_house<16><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            else k_rq_house<32><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
         } else {
             // the reference's scheduled Givens batch: one warp per concurrent
             // rotation (<= 16 warps), rotation parameters in registers
@@ -597,7 +597,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     if (a.s == 0) return SS_OK;
     SS_CUDA_TRY(h, cudaSetDevice(h->device));
     const double rtol = a.rtol > 0.0 ? a.rtol : 1e3 * n * 2.220446049250313e-16;
-    const int nb0 = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
+    const int nb0_req = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
     const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
 
     static bool attrs = false;
@@ -623,6 +623,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const char* rqenv = getenv("SS_BLOCK_RQ");
     const bool use_house = (m + 1 <= 32) && !(rqenv && strcmp(rqenv, "givens") == 0);
     const UpdTile tile = pick_tile(m);
+    // the Householder block RQ maps one block row to one thread of two warps
+    const int nb0 = use_house ? std::min(nb0_req, 64) : nb0_req;
 
     // fro2 / trace for the per-shift singularity thresholds
     {
