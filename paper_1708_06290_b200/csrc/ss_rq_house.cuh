@@ -41,18 +41,21 @@ struct RqDims {
     int64_t LDZ;
 };
 
-// shared memory of one k_rq_house block (one shift)
+// shared memory of one k_rq_house block (one shift): pivot buffers, U, tau
 __host__ __device__ inline size_t rqh_warp_smem(int nb, int m) {
     const int L = m + 1;
-    return (size_t)L * nb * 16 + (size_t)nb * L * 16 + (size_t)nb * 16;
+    return (size_t)2 * 32 * 16 + (size_t)nb * L * 16 + (size_t)nb * 16;
 }
 
-// Two warps per shift block: lane i of warp w owns block row 32w + i (nb <=
-// 64).  Each warp rebuilds the reflector of row t from broadcast loads (no
-// shuffles, no hand-off), updates its own row, and one CTA barrier per step
-// publishes row t-1 for the next reflector.  The panel column entering the
-// window is prefetched one step ahead from global memory.  The reverse
-// accumulation (lanes = columns of W, registers) runs on warp 0.
+// Two warps per shift block, thread i owns block row i (nb <= 64) and keeps
+// that row's active window r[j] = Z(i, t + j), j = 0..m, in REGISTERS: the
+// window slides by one column per step (column t+m retires, panel column
+// t-1 -- prefetched from global one step ahead -- enters), so the only
+// shared-memory traffic per step is the pivot row t, published by its
+// owner (double-buffered: one barrier per step).  Every thread rebuilds the
+// reflector of row t from the broadcast (no shuffles), updates its own row
+// (z <- z - tau (z u) u^H) and shifts its window.  The reverse accumulation
+// (lanes = columns of W, registers) runs on warp 0.
 // LMAX >= m+1, <= 32; LFIX > 0 fixes L = m+1 at compile time.
 template <int LMAX, int LFIX = 0>
 __global__ void __launch_bounds__(64)
@@ -63,56 +66,61 @@ __global__ void __launch_bounds__(64)
     const int nb = d.nb;
     const int L = LFIX > 0 ? LFIX : d.m + 1;
     const int m = L - 1;
-    double2* Win = (double2*)smem;           // [L slots][nb rows]
-    double2* U = Win + (size_t)L * nb;       // [nb][L]
+    double2* Piv = (double2*)smem;           // [2][LMAX] pivot row broadcast
+    double2* U = Piv + 2 * LMAX;             // [nb][L]
     double2* Tau = U + (size_t)nb * L;       // [nb]
     const double2 sig = d.shifts[l];
     const int arow0 = d.k - nb;  // A row of block row 0
     const int i = 32 * warp + lane;  // this thread's block row
+    const bool live = i < nb;
 
-    // initial window: columns nb-1 .. nb-1+m  (Z1 column nb-1 and the m Z2 columns)
-    if (i < nb) {
-        const double* src = d.A + arow0 + (int64_t)(d.c0 + nb - 1) * d.lda;
-        double2 v = make_double2(src[i], 0.0);
-        if (i + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
-        Win[(size_t)((nb - 1) % L) * nb + i] = v;
-        for (int c = 0; c < m; ++c) {
-            const int j = nb + c;
-            Win[(size_t)(j % L) * nb + i] = Z2[((int64_t)l * m + c) * d.LDZ + d.r0 + i];
-        }
-    }
-    double pf = 0.0;  // prefetched entry (row i) of the panel column entering next
-    if (nb >= 2 && i <= nb - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + nb - 2) * d.lda];
-    __syncthreads();
-
-    int base = (nb - 1) % L;  // slot of column t
-    for (int t = nb - 1; t >= 0; --t) {
-        double2* col[LMAX];  // slot pointers of columns t .. t+m
+    // initial window of row i: columns nb-1 .. nb-1+m
+    double2 r[LMAX];
 #pragma unroll
-        for (int j = 0; j < LMAX; ++j) {
-            int sj = base + j;
-            if (sj >= L) sj -= L;
-            col[j] = Win + (size_t)sj * nb;
+    for (int j = 0; j < LMAX; ++j) r[j] = cz();
+    if (live) {
+        double2 v = make_double2(d.A[arow0 + i + (int64_t)(d.c0 + nb - 1) * d.lda], 0.0);
+        if (i + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
+        r[0] = v;
+        const double2* z2 = Z2 + (int64_t)l * m * d.LDZ + d.r0 + i;
+#pragma unroll
+        for (int j = 1; j < LMAX; ++j)
+            if (j < L) r[j] = z2[(int64_t)(j - 1) * d.LDZ];
+    }
+    double pf = 0.0;  // row i of the panel column entering next
+    if (nb >= 2 && i <= nb - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + nb - 2) * d.lda];
+
+    for (int t = nb - 1; t >= 0; --t) {
+        double2* piv = Piv + (t & 1) * LMAX;
+        if (i == t) {
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j < L) piv[j] = r[j];
         }
-        // ---- reflector of row t (every lane, from broadcast loads) ----
+        __syncthreads();
+        // ---- reflector of row t (every thread, from the broadcast) ----
         double2 y[LMAX];
-        double s2a = 0.0, s2b = 0.0;
 #pragma unroll
         for (int j = 0; j < LMAX; ++j) {
             if (j < L) {
-                const double2 x = col[j][t];
+                const double2 x = piv[j];
                 y[j] = make_double2(x.x, -x.y);  // conj(row t)
-                if (j < L - 1) {
-                    if (j & 1) s2b = fma(y[j].x, y[j].x, fma(y[j].y, y[j].y, s2b));
-                    else s2a = fma(y[j].x, y[j].x, fma(y[j].y, y[j].y, s2a));
-                }
+            } else {
+                y[j] = cz();
             }
         }
+        double sq[LMAX];
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) sq[j] = (j < L - 1) ? fma(y[j].x, y[j].x, y[j].y * y[j].y) : 0.0;
+#pragma unroll
+        for (int w = 1; w < LMAX; w <<= 1)  // tree sum
+#pragma unroll
+            for (int j = 0; j + w < LMAX; j += 2 * w) sq[j] += sq[j + w];
+        const double s2 = sq[0];
         double2 alpha = cz();
 #pragma unroll
         for (int j = 0; j < LMAX; ++j)
             if (j == L - 1) alpha = y[j];
-        const double s2 = s2a + s2b;
         double2 tau = cz(), scale = cz();
         if (!(s2 == 0.0 && alpha.y == 0.0)) {
             const double nrm2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
@@ -131,48 +139,36 @@ __global__ void __launch_bounds__(64)
         for (int j = 0; j < LMAX; ++j)
             uu[j] = (j < L - 1) ? cmul(y[j], scale) : (j == L - 1 ? make_double2(1.0, 0.0) : cz());
         if (warp == 0) {
-            if (lane < L) {
 #pragma unroll
-                for (int j = 0; j < LMAX; ++j)
-                    if (j == lane) U[(size_t)t * L + j] = uu[j];
-            }
+            for (int j = 0; j < LMAX; ++j)
+                if (j < L && j == lane) U[(size_t)t * L + j] = uu[j];
             if (lane == 0) Tau[t] = tau;
         }
-        // ---- own row i < t: z <- z - tau (z u) u^H ----
-        if (i < t && (tau.x != 0.0 || tau.y != 0.0)) {
-            double2 z[LMAX];
-            double2 w0 = cz(), w1 = cz();
+        // ---- own row (i < t): r <- r - tau (r u) u^H ----
+        if (i < t) {
+            double2 wp[LMAX];
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j) {
-                if (j < L) {
-                    z[j] = col[j][i];
-                    if (j & 1) w1 = cfma(z[j], uu[j], w1);
-                    else w0 = cfma(z[j], uu[j], w0);
-                }
-            }
-            const double2 tw = cmul(tau, cadd(w0, w1));
+            for (int j = 0; j < LMAX; ++j) wp[j] = (j < L) ? cmul(r[j], uu[j]) : cz();
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j) {
-                if (j < L) {
-                    const double2 cu = make_double2(uu[j].x, -uu[j].y);  // z_j -= tau w conj(u_j)
-                    col[j][i] = csub(z[j], cmul(tw, cu));
-                }
-            }
+            for (int w = 1; w < LMAX; w <<= 1)  // tree sum
+#pragma unroll
+                for (int j = 0; j + w < LMAX; j += 2 * w) wp[j] = cadd(wp[j], wp[j + w]);
+            const double2 tw = cmul(tau, wp[0]);
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j < L) r[j] = csub(r[j], cmul(tw, make_double2(uu[j].x, -uu[j].y)));
         }
-        // ---- slide: column t+m retires, panel column t-1 enters slot (base-1) ----
+        // ---- slide: column t+m retires, panel column t-1 enters r[0] ----
+#pragma unroll
+        for (int j = LMAX - 1; j > 0; --j) r[j] = r[j - 1];
         if (t > 0) {
-            const int sl = base == 0 ? L - 1 : base - 1;
-            const int j = t - 1;
-            if (i <= j) {
-                double2 v = make_double2(pf, 0.0);
-                if (i + m == j) v = csub(v, sig);
-                Win[(size_t)sl * nb + i] = v;
-            }
+            double2 v = make_double2(pf, 0.0);
+            if (i + m == t - 1) v = csub(v, sig);
+            r[0] = v;
             if (t >= 2 && i <= t - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + t - 2) * d.lda];
-            base = sl;
         }
-        __syncthreads();
     }
+    __syncthreads();  // U / Tau complete
 
     // ---- reverse accumulation in registers (warp 0): lane cc owns column cc ----
     if (warp != 0) return;
@@ -184,17 +180,21 @@ __global__ void __launch_bounds__(64)
         for (int j = 0; j < LMAX; ++j) w[j] = make_double2((j == cc) ? 1.0 : 0.0, 0.0);
         for (int t = 0; t < nb; ++t) {
             const double2 tau = Tau[t];
-            double2 dd0 = cz(), dd1 = cz();
+            double2 dp[LMAX];
 #pragma unroll
             for (int j = 0; j < LMAX; ++j) {
                 if (j < L) {
                     const double2 uj = U[(size_t)t * L + j];
-                    const double2 cu = make_double2(uj.x, -uj.y);
-                    if (j & 1) dd1 = cfma(cu, w[j], dd1);
-                    else dd0 = cfma(cu, w[j], dd0);
+                    dp[j] = cmul(make_double2(uj.x, -uj.y), w[j]);
+                } else {
+                    dp[j] = cz();
                 }
             }
-            const double2 td = cmul(tau, cadd(dd0, dd1));
+#pragma unroll
+            for (int s = 1; s < LMAX; s <<= 1)
+#pragma unroll
+                for (int j = 0; j + s < LMAX; j += 2 * s) dp[j] = cadd(dp[j], dp[j + s]);
+            const double2 td = cmul(tau, dp[0]);
 #pragma unroll
             for (int j = 0; j < LMAX; ++j)
                 if (j < L) w[j] = csub(w[j], cmul(U[(size_t)t * L + j], td));
