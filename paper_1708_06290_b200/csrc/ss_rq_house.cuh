@@ -139,9 +139,12 @@ __global__ void __launch_bounds__(64)
         for (int j = 0; j < LMAX; ++j)
             uu[j] = (j < L - 1) ? cmul(y[j], scale) : (j == L - 1 ? make_double2(1.0, 0.0) : cz());
         if (warp == 0) {
+            // select (not branch) this lane's entry: a per-lane branch here
+            // compiles to an 11-way divergent switch
+            double2 mine = cz();
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j)
-                if (j < L && j == lane) U[(size_t)t * L + j] = uu[j];
+            for (int j = 0; j < LMAX; ++j) mine = (j == lane) ? uu[j] : mine;
+            if (lane < L) U[(size_t)t * L + lane] = mine;
             if (lane == 0) Tau[t] = tau;
         }
         // ---- own row (i < t): r <- r - tau (r u) u^H ----
