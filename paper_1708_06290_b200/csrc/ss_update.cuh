@@ -142,6 +142,25 @@ __global__ void __launch_bounds__(256)
         }
         cp_async_commit_wait_all();
         __syncthreads();
+        {
+            // pull the next chunk's P and Z2 tiles into L2 while this chunk
+            // computes, so its cp.async staging hits L2 instead of HBM
+            const int lnx = lc + u.S;
+            if (lnx < lend) {
+                const int nnx = min(u.S, lend - lnx);
+                const char* pb = reinterpret_cast<const char*>(Pbuf + (int64_t)lnx * nc * m);
+                const int plines = (nnx * nc * m * 16 + 127) >> 7;
+                for (int v = tid; v < plines; v += blockDim.x)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + (size_t)v * 128));
+                const int zcols = nnx * m;  // one 64-row tile = 1 KB = 8 lines per column
+                for (int v = tid; v < zcols * 8; v += blockDim.x) {
+                    const int sc = v >> 3, ln = v & 7;
+                    const int s = sc / m, c = sc - s * m;
+                    const double2* zp = Zin + ((int64_t)(lnx + s) * m + c) * u.LDZ + i0 + ln * 8;
+                    if (i0 + ln * 8 < r0) asm volatile("prefetch.global.L2 [%0];" ::"l"(zp));
+                }
+            }
+        }
         if (s_w >= nsc) continue;
         const int l = lc + s_w;
         const double2* Pl = Pst + (size_t)s_w * nc * m + cb;
