@@ -34,6 +34,7 @@
 #include "ss_internal.h"
 #include "ss_rq_house.cuh"
 #include "ss_update.cuh"
+#include "ss_update_ws.cuh"
 
 using namespace ssd;
 
@@ -375,6 +376,37 @@ int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStrea
     return SS_OK;
 }
 
+template <int G, int C>
+int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const UpdDims& u,
+                       const double2* zin, double2* zout, const double2* pbuf) {
+    static bool configured = false;
+    if (!configured) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update_ws<G, C>));
+        configured = true;
+    }
+    k_update_ws<G, C><<<grid, kWsThreads, smem, st>>>(u, zin, zout, pbuf);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+// Warp-specialised TMA/mbarrier update for tiles where one warp pair covers
+// all m columns (G*C == m); returns SS_EARG when the tile is not covered.
+int launch_update_ws(ss_handle* h, const UpdTile& t, dim3 grid, size_t smem, cudaStream_t st,
+                     const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
+    if (t.G == 2 && t.C == 5) return launch_update_ws_t<2, 5>(h, grid, smem, st, u, zin, zout, pbuf);
+    if (t.G == 2 && t.C == 4) return launch_update_ws_t<2, 4>(h, grid, smem, st, u, zin, zout, pbuf);
+    if (t.G == 1) {
+        switch (t.C) {
+#define SS_CASE(K) \
+    case K: return launch_update_ws_t<1, K>(h, grid, smem, st, u, zin, zout, pbuf);
+            SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
+#undef SS_CASE
+            default: break;
+        }
+    }
+    return SS_EARG;
+}
+
 int launch_update(ss_handle* h, const UpdTile& t, dim3 grid, int threads, size_t smem,
                   cudaStream_t st, const UpdDims& u, const double2* zin, double2* zout,
                   const double2* pbuf) {
@@ -564,8 +596,19 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             (a.mode == 0 ? (double)a.p * s.nb : (double)s.nb) + (double)(k - s.nb) * s.nb;
         const double fl_alg = 4.0 * m * nnz * sb;
         ev = ss::timing_begin(h, st);
-        int rc = launch_update(h, tile, g, 32 * u.S * nws * u.ksplit, smem_u, st, u, B.Z[cur],
+        int rc;
+        const bool ws = nws == 1 && tile.exact && tile.G * tile.C == m && !getenv("SS_UPDATE_CLASSIC") &&
+                        ws_smem_bytes(s.nb, m) + 1024 <= h->smem_optin;
+        if (ws) {
+            // warp-specialised pipeline: 1 producer + 4 consumer pairs, SG shifts per CTA
+            u.SG = 32;
+            dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
+            rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z[cur], B.Z[cur ^ 1],
+                                  B.P);
+        } else {
+            rc = launch_update(h, tile, g, 32 * u.S * nws * u.ksplit, smem_u, st, u, B.Z[cur],
                                B.Z[cur ^ 1], B.P);
+        }
         if (rc) return rc;
         ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
         cur ^= 1;
