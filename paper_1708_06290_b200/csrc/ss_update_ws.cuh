@@ -55,6 +55,17 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
         : "memory");
 }
 
+// Row map of the warp-specialised kernel: lane row group rg owns tile rows
+// rg + RG*w (w = 0..R-1), so for fixed w the lanes of a half-warp touch
+// consecutive rows (conflict-free Z-tile LDS.128, coalesced stores).  The
+// panel keeps rows (rg + RG*2p, rg + RG*(2p+1)) adjacent for 16-byte loads.
+template <int G>
+__device__ __forceinline__ int pan_index_ws(int row) {
+    constexpr int RG = 32 / G;
+    const int rg = row % RG, w = row / RG, p = w >> 1, e = w & 1;
+    return p * (2 * RG) + rg * 2 + e;
+}
+
 constexpr int kWsStages = 6;
 constexpr int kWsPairs = 4;
 constexpr int kWsThreads = 32 * (1 + 2 * kWsPairs);
@@ -69,9 +80,10 @@ template <int G, int C>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_update_ws(UpdDims u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
                 const double2* __restrict__ Pbuf) {
-    constexpr int R = 2 * G, RG = 32 / G;
+    constexpr int R = 2 * G, RG = 32 / G, M = G * C;  // one warp pair covers all m = M columns
     extern __shared__ __align__(128) unsigned char smem[];
-    const int nb = u.nb, m = u.m, nc = u.nc, r0 = u.r0;
+    const int nb = u.nb, nc = u.nc, r0 = u.r0;
+    constexpr int m = M;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [kWsStages]
     uint64_t* empty = full + kWsStages;                         // [kWsStages]
     double* Pan = reinterpret_cast<double*>(smem + 128);        // [nb][64] pair-interleaved
@@ -94,7 +106,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int v = tid; v < nb * kUpdRows; v += blockDim.x) {
         const int j = v >> 6, rr = v & 63;
         const int i = i0 + rr, col = u.c0 + j;
-        double* dst = Pan + j * kUpdRows + pan_index<G>(rr);
+        double* dst = Pan + j * kUpdRows + pan_index_ws<G>(rr);
         if (i >= r0) {
             *dst = 0.0;
         } else if (i >= u.ptop) {
@@ -133,8 +145,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int cw = warp - 1, pair = cw >> 1, half = cw & 1;
     const int rg = lane / G, q = lane - rg * G;
     const int cb = q * C;
-    const int rbase = rg * R;
     const int dlo = r0 - m;
+    // interior tiles need neither the r0 row guard nor the lazy-shift rows
+    const bool interior = i0 + kUpdRows <= dlo;
     const int jlo = half == 0 ? 0 : u.jh;
     const int jhi = half == 1 ? nb : u.jh;
     const double* pan_l = Pan + rg * 2;
@@ -169,7 +182,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             for (int j = 0; j < m; ++j) {
                 double2 z[R];
 #pragma unroll
-                for (int r = 0; r < R; ++r) z[r] = Zs[j * kUpdRows + rbase + r];
+                for (int r = 0; r < R; ++r) z[r] = Zs[j * kUpdRows + rg + RG * r];
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const double2 pv = Pl[(nb + j) * m + c];
@@ -196,18 +209,25 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 for (int c = 0; c < C; ++c) acc[r][c] = cadd(acc[r][c], red[(r * C + c) * 32]);
             const int l = l0 + k;
             const double2 sig = u.shifts[l];
-            double2* zo = Zout + ((int64_t)l * m + cb) * u.LDZ;
+            double2* zo = Zout + ((int64_t)l * m + cb) * u.LDZ + i0 + rg;
+            if (interior) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int row = i0 + rbase + r;
-                if (row >= r0) continue;
-                const int dd = row - dlo;
-                const bool corr = dd >= 0 && dd < u.mnb;
+                for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    double2 v = acc[r][c];
-                    if (corr) v = csub(v, cmul(sig, Pl[dd * m + c]));
-                    zo[(int64_t)c * u.LDZ + row] = v;
+                    for (int c = 0; c < C; ++c) zo[(int64_t)c * u.LDZ + RG * r] = acc[r][c];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int row = i0 + rg + RG * r;
+                    if (row >= r0) continue;
+                    const int dd = row - dlo;
+                    const bool corr = dd >= 0 && dd < u.mnb;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        double2 v = acc[r][c];
+                        if (corr) v = csub(v, cmul(sig, Pl[dd * m + c]));
+                        zo[(int64_t)c * u.LDZ + RG * r] = v;
+                    }
                 }
             }
         }
