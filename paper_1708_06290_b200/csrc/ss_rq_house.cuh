@@ -47,21 +47,41 @@ __host__ __device__ inline size_t rqh_warp_smem(int nb, int m) {
     return (size_t)2 * 32 * 16 + (size_t)nb * L * 16 + (size_t)nb * 16;
 }
 
-// Two warps per shift block, thread i owns block row i (nb <= 64) and keeps
-// that row's active window r[j] = Z(i, t + j), j = 0..m, in REGISTERS: the
-// window slides by one column per step (column t+m retires, panel column
-// t-1 -- prefetched from global one step ahead -- enters), so the only
-// shared-memory traffic per step is the pivot row t, published by its
-// owner (double-buffered: one barrier per step).  Every thread rebuilds the
-// reflector of row t from the broadcast (no shuffles), updates its own row
-// (z <- z - tau (z u) u^H) and shifts its window.  The reverse accumulation
-// (lanes = columns of W, registers) runs on warp 0.
+// One warp per shift block: lane owns block rows lane and lane+32 (nb <= 64)
+// and keeps each row's active window r[j] = Z(i, t + j), j = 0..m, in
+// REGISTERS; the window slides by one column per step (column t+m retires,
+// panel column t-1 -- prefetched from global one step ahead -- enters).
+// Per step the owner lane publishes the pivot row t in shared memory
+// (double-buffered, __syncwarp only), every lane rebuilds the reflector of
+// row t from the broadcast (computed once per block, no shuffles), updates
+// its rows (z <- z - tau (z u) u^H) and shifts its windows.  The reverse
+// accumulation (lanes = columns of W, registers) follows on the same warp.
 // LMAX >= m+1, <= 32; LFIX > 0 fixes L = m+1 at compile time.
+template <int LMAX>
+__device__ __forceinline__ void rq_row_update(double2 (&r)[LMAX], const double2 (&uu)[LMAX],
+                                              double2 tau, int L) {
+    double2 wp[LMAX];
+#pragma unroll
+    for (int j = 0; j < LMAX; ++j) wp[j] = (j < L) ? cmul(r[j], uu[j]) : cz();
+#pragma unroll
+    for (int w = 1; w < LMAX; w <<= 1)  // tree sum
+#pragma unroll
+        for (int j = 0; j + w < LMAX; j += 2 * w) wp[j] = cadd(wp[j], wp[j + w]);
+    const double2 tw = cmul(tau, wp[0]);
+#pragma unroll
+    for (int j = 0; j < LMAX; ++j)
+        if (j < L) {
+            // r_j -= tw conj(u_j)
+            r[j].x = fma(-tw.x, uu[j].x, fma(-tw.y, uu[j].y, r[j].x));
+            r[j].y = fma(-tw.y, uu[j].x, fma(tw.x, uu[j].y, r[j].y));
+        }
+}
+
 template <int LMAX, int LFIX = 0>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(32)
     k_rq_house(RqDims d, const double2* __restrict__ Z2, double2* __restrict__ Pbuf) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     const int l = blockIdx.x;
     const int nb = d.nb;
     const int L = LFIX > 0 ? LFIX : d.m + 1;
@@ -71,34 +91,53 @@ __global__ void __launch_bounds__(64)
     double2* Tau = U + (size_t)nb * L;       // [nb]
     const double2 sig = d.shifts[l];
     const int arow0 = d.k - nb;  // A row of block row 0
-    const int i = 32 * warp + lane;  // this thread's block row
-    const bool live = i < nb;
+    const int i0 = lane, i1 = lane + 32;
 
-    // initial window of row i: columns nb-1 .. nb-1+m
-    double2 r[LMAX];
+    // initial windows: columns nb-1 .. nb-1+m
+    double2 ra[LMAX], rb[LMAX];
 #pragma unroll
-    for (int j = 0; j < LMAX; ++j) r[j] = cz();
-    if (live) {
-        double2 v = make_double2(d.A[arow0 + i + (int64_t)(d.c0 + nb - 1) * d.lda], 0.0);
-        if (i + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
-        r[0] = v;
-        const double2* z2 = Z2 + (int64_t)l * m * d.LDZ + d.r0 + i;
+    for (int j = 0; j < LMAX; ++j) ra[j] = rb[j] = cz();
+    {
+        const double* a0 = d.A + arow0 + (int64_t)(d.c0 + nb - 1) * d.lda;
+        const double2* z2 = Z2 + (int64_t)l * m * d.LDZ + d.r0;
+        if (i0 < nb) {
+            double2 v = make_double2(a0[i0], 0.0);
+            if (i0 + m == nb - 1) v = csub(v, sig);  // lazy -sigma on Ahat's diagonal
+            ra[0] = v;
 #pragma unroll
-        for (int j = 1; j < LMAX; ++j)
-            if (j < L) r[j] = z2[(int64_t)(j - 1) * d.LDZ];
+            for (int j = 1; j < LMAX; ++j)
+                if (j < L) ra[j] = z2[(int64_t)(j - 1) * d.LDZ + i0];
+        }
+        if (i1 < nb) {
+            double2 v = make_double2(a0[i1], 0.0);
+            if (i1 + m == nb - 1) v = csub(v, sig);
+            rb[0] = v;
+#pragma unroll
+            for (int j = 1; j < LMAX; ++j)
+                if (j < L) rb[j] = z2[(int64_t)(j - 1) * d.LDZ + i1];
+        }
     }
-    double pf = 0.0;  // row i of the panel column entering next
-    if (nb >= 2 && i <= nb - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + nb - 2) * d.lda];
+    double pfa = 0.0, pfb = 0.0;  // rows i0, i1 of the panel column entering next
+    if (nb >= 2) {
+        const double* an = d.A + arow0 + (int64_t)(d.c0 + nb - 2) * d.lda;
+        if (i0 <= nb - 2) pfa = an[i0];
+        if (i1 <= nb - 2) pfb = an[i1];
+    }
 
     for (int t = nb - 1; t >= 0; --t) {
         double2* piv = Piv + (t & 1) * LMAX;
-        if (i == t) {
+        if (i0 == t) {
 #pragma unroll
             for (int j = 0; j < LMAX; ++j)
-                if (j < L) piv[j] = r[j];
+                if (j < L) piv[j] = ra[j];
         }
-        __syncthreads();
-        // ---- reflector of row t (every thread, from the broadcast) ----
+        if (i1 == t) {
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j < L) piv[j] = rb[j];
+        }
+        __syncwarp();
+        // ---- reflector of row t (every lane, from the broadcast) ----
         double2 y[LMAX];
 #pragma unroll
         for (int j = 0; j < LMAX; ++j) {
@@ -138,43 +177,40 @@ __global__ void __launch_bounds__(64)
 #pragma unroll
         for (int j = 0; j < LMAX; ++j)
             uu[j] = (j < L - 1) ? cmul(y[j], scale) : (j == L - 1 ? make_double2(1.0, 0.0) : cz());
-        if (warp == 0) {
+        {
             // select (not branch) this lane's entry: a per-lane branch here
-            // compiles to an 11-way divergent switch
+            // compiles to an L-way divergent switch
             double2 mine = cz();
 #pragma unroll
             for (int j = 0; j < LMAX; ++j) mine = (j == lane) ? uu[j] : mine;
             if (lane < L) U[(size_t)t * L + lane] = mine;
             if (lane == 0) Tau[t] = tau;
         }
-        // ---- own row (i < t): r <- r - tau (r u) u^H ----
-        if (i < t) {
-            double2 wp[LMAX];
-#pragma unroll
-            for (int j = 0; j < LMAX; ++j) wp[j] = (j < L) ? cmul(r[j], uu[j]) : cz();
-#pragma unroll
-            for (int w = 1; w < LMAX; w <<= 1)  // tree sum
-#pragma unroll
-                for (int j = 0; j + w < LMAX; j += 2 * w) wp[j] = cadd(wp[j], wp[j + w]);
-            const double2 tw = cmul(tau, wp[0]);
-#pragma unroll
-            for (int j = 0; j < LMAX; ++j)
-                if (j < L) r[j] = csub(r[j], cmul(tw, make_double2(uu[j].x, -uu[j].y)));
-        }
+        // ---- own rows below the pivot's column range: i < t ----
+        if (i0 < t) rq_row_update<LMAX>(ra, uu, tau, L);
+        if (t > 32 && i1 < t) rq_row_update<LMAX>(rb, uu, tau, L);
         // ---- slide: column t+m retires, panel column t-1 enters r[0] ----
 #pragma unroll
-        for (int j = LMAX - 1; j > 0; --j) r[j] = r[j - 1];
+        for (int j = LMAX - 1; j > 0; --j) {
+            ra[j] = ra[j - 1];
+            rb[j] = rb[j - 1];
+        }
         if (t > 0) {
-            double2 v = make_double2(pf, 0.0);
-            if (i + m == t - 1) v = csub(v, sig);
-            r[0] = v;
-            if (t >= 2 && i <= t - 2) pf = d.A[arow0 + i + (int64_t)(d.c0 + t - 2) * d.lda];
+            double2 va = make_double2(pfa, 0.0), vb = make_double2(pfb, 0.0);
+            if (i0 + m == t - 1) va = csub(va, sig);
+            if (i1 + m == t - 1) vb = csub(vb, sig);
+            ra[0] = va;
+            rb[0] = vb;
+            if (t >= 2) {
+                const double* an = d.A + arow0 + (int64_t)(d.c0 + t - 2) * d.lda;
+                if (i0 <= t - 2) pfa = an[i0];
+                if (i1 <= t - 2) pfb = an[i1];
+            }
         }
     }
-    __syncthreads();  // U / Tau complete
+    __syncwarp();  // U / Tau complete
 
-    // ---- reverse accumulation in registers (warp 0): lane cc owns column cc ----
-    if (warp != 0) return;
+    // ---- reverse accumulation in registers: lane cc owns column cc ----
     double2* dstP = Pbuf + (int64_t)l * d.nc * m;  // j-major: P[j*m + cc]
     for (int cc0 = 0; cc0 < m; cc0 += 32) {
         const int cc = cc0 + lane;

@@ -522,15 +522,15 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             rd.shifts = d.shifts;
             rd.LDZ = LDZ;
             const size_t sm = rqh_warp_smem(s.nb, m);
-            if (m == 1) k_rq_house<2, 2><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 5) k_rq_house<6, 6><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 10) k_rq_house<11, 11><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 20) k_rq_house<21, 21><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 2) k_rq_house<2><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 4) k_rq_house<4><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 8) k_rq_house<8><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 16) k_rq_house<16><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
-            else k_rq_house<32><<<sb, 64, sm, st>>>(rd, B.Z[cur], B.P);
+            if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 5) k_rq_house<6, 6><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 10) k_rq_house<11, 11><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m == 20) k_rq_house<21, 21><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
         } else {
             // the reference's scheduled Givens batch: one warp per concurrent
             // rotation (<= 16 warps), rotation parameters in registers
