@@ -602,6 +602,9 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         if (ws) {
             // warp-specialised pipeline: 1 producer + 4 consumer pairs, SG shifts per CTA
             u.SG = 32;
+            // half 0 also carries the Z2 x P22 part (2 panel columns' worth of
+            // DFMA per column of m) and the epilogue: give it fewer panel columns
+            u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2 - 1));
             dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
             rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z[cur], B.Z[cur ^ 1],
                                   B.P);
@@ -705,7 +708,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // Independent halves of a batch on two streams: the latency-bound block
     // RQ of one half overlaps the FP64-bound window update of the other.
     const char* sv = getenv("SS_STREAMS");
-    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : 1;
+    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : 2;
     if (sb_max < 64) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {

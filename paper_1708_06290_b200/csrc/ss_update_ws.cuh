@@ -66,7 +66,7 @@ __device__ __forceinline__ int pan_index_ws(int row) {
     return p * (2 * RG) + rg * 2 + e;
 }
 
-constexpr int kWsStages = 6;
+constexpr int kWsStages = 8;
 constexpr int kWsPairs = 4;
 constexpr int kWsThreads = 32 * (1 + 2 * kWsPairs);
 
