@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshiftsolve_b200.so")
+LIB_PATH = os.environ.get("SS_LIB_PATH") or os.path.join(_HERE, "libshiftsolve_b200.so")
 
 SS_OK, SS_EDIM, SS_EARG, SS_ECUDA, SS_ENOMEM = 0, 1, 2, 3, 4
 

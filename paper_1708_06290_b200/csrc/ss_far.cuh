@@ -1,0 +1,232 @@
+// Persistent warp-specialised far-row update of the two-level sweep.
+//
+// Same math as k_update_ws (ss_update_ws.cuh) -- per shift l and far row i
+//   Zout_l[i, :] = Zin_l[i, :] P22_l + Pan[i, :] P12_l - sigma_l P12_l[i - (r0 - m), :]
+// (reference solvers.py:186-199 with the outer block's composite W in place
+// of one window's P) -- restructured after ncu showed ~19% of the consumer
+// warps' time waiting in k_update_ws:
+//  * persistent: one CTA per SM walks a contiguous range of (64-row tile,
+//    shift) units in tile-major order, so the stage ring never drains between
+//    CTAs and the 64 x nb panel tile is restaged only when the range crosses
+//    a tile boundary (consumer-only named barrier; the producer keeps
+//    prefetching across it);
+//  * asynchronous pair hand-off: in a consumer pair, half 0 does the Z2 part
+//    FIRST and signals "Z tile consumed" (mbarrier), then its panel columns;
+//    half 1 does its panel columns, waits for that signal, writes its partial
+//    sums over the Z tile and signals "partials ready"; only half 0 waits for
+//    the partials, after its own work -- no pair-wide bar.sync;
+//  * the producer parks on the empty barriers with a suspend-time hint.
+#pragma once
+
+#include "ss_update_ws.cuh"
+
+namespace ssd {
+
+constexpr int kFarStages = 8;
+constexpr int kFarPairs = 4;
+constexpr int kFarThreads = 32 * (1 + 2 * kFarPairs);
+
+__host__ __device__ inline size_t far_smem_bytes(int nb, int m) {
+    const int nc = nb + m;
+    const size_t stage = ((size_t)nc * m + (size_t)m * kUpdRows) * 16;
+    return 256 + (size_t)nb * kUpdRows * 8 + kFarStages * stage;
+}
+
+template <int G, int C, bool ZID>
+__global__ void __launch_bounds__(kFarThreads, 1)
+    k_far(UpdDims u, double2* Z, const double2* __restrict__ Pbuf) {
+    constexpr int R = 2 * G, RG = 32 / G, M = G * C;
+    constexpr int m = M;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nb = u.nb, nc = u.nc, r0 = u.r0, sb = u.sb;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [kFarStages]
+    uint64_t* empty = full + kFarStages;                   // [kFarStages]
+    uint64_t* zfree = empty + kFarStages;                  // [kFarPairs]
+    uint64_t* partr = zfree + kFarPairs;                   // [kFarPairs]
+    double* Pan = reinterpret_cast<double*>(smem + 256);   // [nb][64] pair-interleaved
+    double2* Stg = reinterpret_cast<double2*>(smem + 256 + (size_t)nb * kUpdRows * 8);
+    const size_t stage_el = (size_t)nc * m + (size_t)m * kUpdRows;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntiles = (r0 - u.rlo + kUpdRows - 1) / kUpdRows;
+    const int64_t units = (int64_t)ntiles * sb;
+    const int64_t ua = units * blockIdx.x / gridDim.x, ub = units * (blockIdx.x + 1) / gridDim.x;
+    const int nun = (int)(ub - ua);
+
+    if (tid == 0) {
+        for (int s = 0; s < kFarStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 2);
+        }
+        for (int p = 0; p < kFarPairs; ++p) {
+            mbar_init(zfree + p, 1);
+            mbar_init(partr + p, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (nun <= 0) return;
+
+    if (warp == 0) {
+        // ---------------- producer: stages in unit order ----------------
+        if (lane == 0) {
+            const unsigned p12bytes = (unsigned)(nb * m * 16);
+            const unsigned p22bytes = ZID ? 0u : (unsigned)(m * m * 16);
+            for (int k = 0; k < nun; ++k) {
+                const int s = k % kFarStages, use = k / kFarStages;
+                if (use > 0) mbar_wait_sleep(empty + s, (use - 1) & 1);
+                const int64_t unit = ua + k;
+                const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
+                const int i0 = u.rlo + tile * kUpdRows;
+                const unsigned zbytes = (unsigned)(min(kUpdRows, r0 - i0) * 16);
+                double2* st = Stg + (size_t)s * stage_el;
+                const double2* pl = Pbuf + (int64_t)l * u.pstride;
+                mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
+                tma_bulk_g2s(st, pl + u.p12off, p12bytes, full + s);
+                if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
+                double2* zt = st + (size_t)nc * m;
+                for (int c = 0; c < m; ++c)
+                    tma_bulk_g2s(zt + c * kUpdRows, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
+                                 full + s);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const int cw = warp - 1, pair = cw >> 1, half = cw & 1;
+    const int rg = lane / G, q = lane - rg * G;
+    const int cb = q * C;
+    const int dlo = r0 - m;
+    const int jlo = half == 0 ? 0 : u.jh;
+    const int jhi = half == 1 ? nb : u.jh;
+    const double* pan_l = Pan + rg * 2;
+    int npair = 0;  // units this pair has processed (mbarrier phase of zfree / partr)
+    const int tfirst = (int)(ua / sb), tlast = (int)((ub - 1) / sb);
+    for (int tile = tfirst; tile <= tlast; ++tile) {
+        // (re)stage the panel tile: every consumer is done with the old one
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * kFarPairs) : "memory");
+        {
+            const int i0n = u.rlo + tile * kUpdRows;
+            for (int v = tid - 32; v < nb * kUpdRows; v += 32 * 2 * kFarPairs) {
+                const int j = v >> 6, rr = v & 63;
+                const int i = i0n + rr, col = u.c0 + j;
+                double* dst = Pan + j * kUpdRows + pan_index_ws<G>(rr);
+                if (i >= r0) {
+                    *dst = 0.0;
+                } else if (i >= u.ptop) {
+                    cp_async8(dst, u.A + (i - u.ptop) + (int64_t)col * u.lda, true);
+                } else if (u.ident_top) {
+                    *dst = (i == col) ? 1.0 : 0.0;
+                } else {
+                    cp_async8(dst, u.T + i + (int64_t)col * u.ldt, true);
+                }
+            }
+            cp_async_commit_wait_all();
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * kFarPairs) : "memory");
+        // this tile's units of the CTA range: k in [ka, kb); pair p takes k = p mod 4
+        const int ka = (int)(max(ua, (int64_t)tile * sb) - ua);
+        const int kb = (int)(min(ub, (int64_t)(tile + 1) * sb) - ua);
+        const int l0t = (int)(ua + ka - (int64_t)tile * sb) - ka;  // l = l0t + k
+        for (int k = ka + ((pair - ka) & (kFarPairs - 1)); k < kb; k += kFarPairs) {
+        const int l = l0t + k;
+        const int i0 = u.rlo + tile * kUpdRows;
+        const bool interior = i0 + kUpdRows <= (u.mnb > 0 ? dlo : r0);
+        const int s = k % kFarStages, use = k / kFarStages;
+        mbar_wait(full + s, use & 1);
+        double2* st = Stg + (size_t)s * stage_el;
+        const double2* Pl = st + cb;
+        double2* Zs = st + (size_t)nc * m;
+        double2 acc[R][C];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[r][c] = cz();
+        if (half == 0) {
+            // Z2 part first, then release the Z tile to the partner
+            if (ZID) {
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r][c] = Zs[(cb + c) * kUpdRows + rg + RG * r];
+            } else {
+                for (int j = 0; j < m; ++j) {
+                    double2 z[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) z[r] = Zs[j * kUpdRows + rg + RG * r];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const double2 pv = Pl[(nb + j) * m + c];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(zfree + pair);
+        }
+#pragma unroll 2
+        for (int j = jlo; j < jhi; ++j) {
+            double a[R];
+#pragma unroll
+            for (int p = 0; p < R / 2; ++p) {
+                const double2 v = *reinterpret_cast<const double2*>(pan_l + j * kUpdRows + p * (2 * RG));
+                a[2 * p] = v.x;
+                a[2 * p + 1] = v.y;
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const double2 pv = Pl[j * m + c];
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
+            }
+        }
+        double2* red = Zs + lane;  // [(r*C + c)][lane] over the consumed Z tile
+        if (half == 1) {
+            mbar_wait(zfree + pair, npair & 1);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < C; ++c) red[(r * C + c) * 32] = acc[r][c];
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(partr + pair);
+                mbar_arrive(empty + s);
+            }
+        } else {
+            mbar_wait(partr + pair, npair & 1);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < C; ++c) acc[r][c] = cadd(acc[r][c], red[(r * C + c) * 32]);
+            const double2 sig = u.shifts[l];
+            double2* zo = Z + ((int64_t)l * m + cb) * u.LDZ + i0 + rg;
+            if (interior) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) zo[(int64_t)c * u.LDZ + RG * r] = acc[r][c];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int row = i0 + rg + RG * r;
+                    if (row >= r0) continue;
+                    const int dd = row - dlo;
+                    const bool corr = dd >= 0 && dd < u.mnb;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        double2 v = acc[r][c];
+                        if (corr) v = csub(v, cmul(sig, Pl[dd * m + c]));
+                        zo[(int64_t)c * u.LDZ + RG * r] = v;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        ++npair;
+        }
+    }
+}
+
+}  // namespace ssd

@@ -35,6 +35,8 @@
 #include "ss_rq_house.cuh"
 #include "ss_update.cuh"
 #include "ss_update_ws.cuh"
+#include "ss_block.cuh"
+#include "ss_far.cuh"
 
 using namespace ssd;
 
@@ -103,10 +105,9 @@ __global__ void k_fro2_trace_final(int nparts, const double* __restrict__ part,
 
 // ---------------------------------------------------------------------------
 // seed (solvers.py:157-163): Z2_l = last m columns of [top; A], -sigma_l on
-// A's diagonal.  Both ping-pong buffers are seeded so rows a step does not
-// rewrite (the still-zero identity rows of the reduced solve) stay valid.
+// A's diagonal.  The window state is updated in place afterwards.
 // ---------------------------------------------------------------------------
-__global__ void k_seed(Dims d, double2* __restrict__ Za, double2* __restrict__ Zb) {
+__global__ void k_seed(Dims d, double2* __restrict__ Za) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int l = blockIdx.y;
     if (i >= d.LDZ) return;
@@ -123,7 +124,6 @@ __global__ void k_seed(Dims d, double2* __restrict__ Za, double2* __restrict__ Z
         }
         const int64_t idx = ((int64_t)l * d.m + c) * d.LDZ + i;
         Za[idx] = v;
-        Zb[idx] = v;
     }
 }
 
@@ -376,17 +376,50 @@ int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStrea
     return SS_OK;
 }
 
-template <int G, int C>
-int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const UpdDims& u,
+template <int G, int C, bool ZID>
+int launch_update_ws_z(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const UpdDims& u,
                        const double2* zin, double2* zout, const double2* pbuf) {
     static bool configured = false;
     if (!configured) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_update_ws<G, C>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update_ws<G, C, ZID>));
         configured = true;
     }
-    k_update_ws<G, C><<<grid, kWsThreads, smem, st>>>(u, zin, zout, pbuf);
+    k_update_ws<G, C, ZID><<<grid, kWsThreads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
+}
+
+template <int G, int C>
+int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const UpdDims& u,
+                       const double2* zin, double2* zout, const double2* pbuf) {
+    if (u.zid) return launch_update_ws_z<G, C, true>(h, grid, smem, st, u, zin, zout, pbuf);
+    return launch_update_ws_z<G, C, false>(h, grid, smem, st, u, zin, zout, pbuf);
+}
+
+template <int G, int C, bool ZID>
+int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
+                 const double2* pbuf) {
+    static bool configured = false;
+    if (!configured) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, ZID>));
+        configured = true;
+    }
+    k_far<G, C, ZID><<<grid, kFarThreads, smem, st>>>(u, z, pbuf);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+// Persistent far-row update (ss_far.cuh): one CTA per SM over (tile, shift) units.
+int launch_far(ss_handle* h, const UpdTile& t, int grid, size_t smem, cudaStream_t st,
+               const UpdDims& u, double2* z, const double2* pbuf) {
+#define SS_FAR(GG, CC)                                                                  \
+    if (t.G == GG && t.C == CC)                                                         \
+        return u.zid ? launch_far_z<GG, CC, true>(h, grid, smem, st, u, z, pbuf)        \
+                     : launch_far_z<GG, CC, false>(h, grid, smem, st, u, z, pbuf);
+    SS_FAR(2, 5) SS_FAR(2, 4) SS_FAR(1, 1) SS_FAR(1, 2) SS_FAR(1, 3) SS_FAR(1, 4) SS_FAR(1, 5)
+    SS_FAR(1, 6) SS_FAR(1, 7) SS_FAR(1, 8)
+#undef SS_FAR
+    return SS_EARG;
 }
 
 // Warp-specialised TMA/mbarrier update for tiles where one warp pair covers
@@ -459,14 +492,57 @@ struct SweepArgs {
 
 // Per-part device buffers: Z2 ping-pong + P for the part's shifts.
 struct PartBufs {
-    double2* Z[2];
+    double2* Z;  // window state, updated in place
     double2* P;
 };
 
 // Enqueue the whole sweep (seed, window steps, head) for shifts
 // [lo, lo + sb) of the call on stream `st`.
+int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, const BlkDims& bd,
+                 const double2* Z, double2* W) {
+    switch (m) {
+#define SS_CASE(K)                                                        \
+    case K: {                                                             \
+        static bool configured = false;                                   \
+        if (!configured) {                                                \
+            SS_CUDA_TRY(h, allow_max_smem(h, k_block<K>));                \
+            configured = true;                                            \
+        }                                                                 \
+        k_block<K><<<sb, kBlkNB, smem, st>>>(bd, Z, W);                   \
+        break;                                                            \
+    }
+        SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
+        SS_CASE(10)
+#undef SS_CASE
+        default: return ss::set_err(h, SS_EARG, "two-level sweep: unsupported m");
+    }
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+bool block_supported(int m) { return (m >= 1 && m <= 8) || m == 10; }
+
+// Reference phase flops of the window sweep at block size nb0 (shape only:
+// batched.py:58-61, solvers.py:186-199), independent of how the device
+// schedules the work.
+void account_ref_flops(ss_handle* h, int sb, int n, int m, int ptop, int nb0) {
+    for (int k = n; k >= m + 1;) {
+        const int nb = std::min(nb0, k - m), nc = nb + m, mnb = std::min(m, nb);
+        const int r0 = ptop + k - nb;
+        const ss::Sched* sc = ss::get_sched(h, nb, nc);
+        double rq_fl = 0.0;
+        if (sc)
+            for (int qq = 0; qq < sc->rots; ++qq) rq_fl += 20.0 * ((sc->rot[qq] & 0xffu) + nc) + 16.0;
+        h->flops[ss::PH_RQ] += rq_fl * sb;
+        h->flops[ss::PH_BATCHED_GEMM] += (double)sb * (8.0 * r0 * m * m + 8.0 * mnb * m);
+        h->flops[ss::PH_OUTER_GEMM] += 8.0 * r0 * ((double)sb * m) * nb;
+        k -= nb;
+    }
+}
+
 int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs B, int nb0,
-                 int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, cudaStream_t st) {
+                 int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, bool two_level,
+                 cudaStream_t st) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : n;
     const int nws = (m + tile.G * tile.C - 1) / (tile.G * tile.C);  // warps per shift
@@ -484,11 +560,86 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     d.LDZ = LDZ;
     {
         dim3 g((unsigned)((LDZ + 255) / 256), (unsigned)sb);
-        k_seed<<<g, 256, 0, st>>>(d, B.Z[0], B.Z[1]);
+        k_seed<<<g, 256, 0, st>>>(d, B.Z);
         SS_LAUNCH_CHECK(h);
     }
-    int cur = 0;
-    int k = n;
+    int k = two_level ? 0 : n;
+    if (two_level) {
+        // ---- two-level sweep: k_block per outer block, far rows from W ----
+        account_ref_flops(h, sb, n, m, ptop, nb0);
+        const int64_t wstride = (int64_t)(kBlkNB + m) * m;
+        for (int ko = n; ko >= m + 1;) {
+            const int NBo = std::min(kBlkNB, ko - m);
+            BlkDims bd;
+            bd.m = m;
+            bd.ptop = ptop;
+            bd.k = ko;
+            bd.NBo = NBo;
+            bd.c0 = ko - m - NBo;
+            bd.r0 = ptop + ko - NBo;
+            bd.A = a.A;
+            bd.lda = a.lda;
+            bd.shifts = d.shifts;
+            bd.LDZ = LDZ;
+            bd.wstride = wstride;
+            cudaEvent_t ev = ss::timing_begin(h, st);
+            int rc = launch_block(h, m, sb, blk_smem_bytes(m), st, bd, B.Z, B.P);
+            if (rc) return rc;
+            ss::timing_end(h, st, ev, ss::PH_RQ);
+            const int rlo = a.mode == 1 ? bd.c0 : 0;
+            const int rows = bd.r0 - rlo;
+            for (int jb = 0; rows > 0 && jb < NBo; jb += 64) {
+                const int nbp = std::min(64, NBo - jb);
+                UpdDims u;
+                u.n = n;
+                u.m = m;
+                u.ptop = ptop;
+                u.ident_top = d.ident_top;
+                u.A = a.A;
+                u.lda = a.lda;
+                u.T = a.C;
+                u.ldt = a.ldc;
+                u.shifts = d.shifts;
+                u.sb = sb;
+                u.LDZ = LDZ;
+                u.nb = nbp;
+                u.mnb = jb == 0 ? std::min(m, NBo) : 0;
+                u.r0 = bd.r0;
+                u.c0 = bd.c0 + jb;
+                u.nc = nbp + m;
+                u.rlo = rlo;
+                u.nws = 1;
+                u.ksplit = 2;
+                u.pstride = wstride;
+                u.p12off = (int64_t)jb * m;
+                u.p22off = (int64_t)NBo * m;
+                u.zid = jb == 0 ? 0 : 1;
+                u.S = 1;
+                u.SG = 32;
+                // half 0 also carries the Z2 part (two panel columns' worth of
+                // DFMA per column of m unless it is the identity) and the epilogue
+                u.jh = u.zid ? nbp / 2 : std::max(0, std::min(nbp, (nbp - 2 * m) / 2 - 1));
+                // algorithmic flops: every far panel row is structurally nonzero
+                const double nnz = ((a.mode == 0 ? (double)a.p : 0.0) + (double)(ko - NBo)) * nbp +
+                                   (a.mode == 1 ? (double)nbp : 0.0);
+                const double fl_alg = 4.0 * m * nnz * sb;
+                dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
+                ev = ss::timing_begin(h, st);
+                if (getenv("SS_FAR_CLASSIC")) {
+                    rc = launch_update_ws(h, tile, gw, ws_smem_bytes(nbp, m), st, u, B.Z, B.Z, B.P);
+                } else {
+                    const int64_t units = (int64_t)gw.x * sb;
+                    const int grid = (int)std::min<int64_t>(units, h->num_sms);
+                    rc = launch_far(h, tile, grid, far_smem_bytes(nbp, m), st, u, B.Z, B.P);
+                }
+                if (rc) return ss::set_err(h, rc, "two-level far update: unsupported tile");
+                // reference-phase split of the measured time by the far update's shares
+                ss::timing_end(h, st, ev, ss::PH_UPDATE, u.zid ? 0.0 : 8.0 * rows * m * m * (double)sb,
+                               8.0 * rows * (double)sb * m * nbp, fl_alg);
+            }
+            ko -= NBo;
+        }
+    }
     while (k >= m + 1) {
         Step s;
         s.k = k;
@@ -522,15 +673,15 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             rd.shifts = d.shifts;
             rd.LDZ = LDZ;
             const size_t sm = rqh_warp_smem(s.nb, m);
-            if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 5) k_rq_house<6, 6><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 10) k_rq_house<11, 11><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m == 20) k_rq_house<21, 21><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
-            else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z[cur], B.P);
+            if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m == 5) k_rq_house<6, 6><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m == 10) k_rq_house<11, 11><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m == 20) k_rq_house<21, 21><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m + 1 <= 2) k_rq_house<2><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m + 1 <= 4) k_rq_house<4><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
         } else {
             // the reference's scheduled Givens batch: one warp per concurrent
             // rotation (<= 16 warps), rotation parameters in registers
@@ -542,10 +693,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 per_warp += (J + nw - 1) / nw;
             }
             const int slots = (per_warp + 31) / 32;
-            if (slots <= 1) k_rq<1><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
-            else if (slots <= 2) k_rq<2><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
-            else if (slots <= 4) k_rq<4><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
-            else if (slots <= 8) k_rq<8><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z[cur], B.P);
+            if (slots <= 1) k_rq<1><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z, B.P);
+            else if (slots <= 2) k_rq<2><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z, B.P);
+            else if (slots <= 4) k_rq<4><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z, B.P);
+            else if (slots <= 8) k_rq<8><<<sb, 32 * nw, smem_rq, st>>>(d, s, B.Z, B.P);
             else return ss::set_err(h, SS_EARG, "window block too large for the register rotation store");
         }
         SS_LAUNCH_CHECK(h);
@@ -570,6 +721,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         u.c0 = s.c0;
         u.nc = s.nc;
         u.rlo = a.mode == 1 ? s.c0 : 0;
+        u.pstride = (int64_t)s.nc * m;
+        u.p12off = 0;
+        u.p22off = (int64_t)s.nb * m;
+        u.zid = 0;
         u.nws = nws;
         // a warp pair splits the panel K range of one (shift, column block) when
         // one block covers all m columns: twice the warps on the same staging
@@ -606,15 +761,14 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             // DFMA per column of m) and the epilogue: give it fewer panel columns
             u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2 - 1));
             dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
-            rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z[cur], B.Z[cur ^ 1],
+            rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z, B.Z,
                                   B.P);
         } else {
-            rc = launch_update(h, tile, g, 32 * u.S * nws * u.ksplit, smem_u, st, u, B.Z[cur],
-                               B.Z[cur ^ 1], B.P);
+            rc = launch_update(h, tile, g, 32 * u.S * nws * u.ksplit, smem_u, st, u, B.Z,
+                               B.Z, B.P);
         }
         if (rc) return rc;
         ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, fl_alg);
-        cur ^= 1;
         k -= s.nb;
     }
     HeadOut ho;
@@ -630,7 +784,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     ho.fail = a.fail + lo;
     cudaEvent_t evh = ss::timing_begin(h, st);
     const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
-    k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z[cur]);
+    k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z);
     SS_LAUNCH_CHECK(h);
     ss::timing_end(h, st, evh, ss::PH_TAIL);
     h->flops[ss::PH_TAIL] += a.mode == 0 ? (double)sb * 8.0 * a.p * m * m : (double)sb * 8.0 * n * m;
@@ -685,9 +839,16 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         SS_LAUNCH_CHECK(h);
     }
 
-    // batch size from memory: 2 window buffers + P per shift
+    // two-level sweep (ss_block.cuh) when the fused block kernel and the
+    // warp-specialised far update cover m; SS_ONE_LEVEL=1 forces the
+    // per-window sweep
+    const bool two_level = use_house && block_supported(m) && tile.exact && tile.G * tile.C == m &&
+                           !getenv("SS_ONE_LEVEL") && !getenv("SS_UPDATE_CLASSIC") &&
+                           ws_smem_bytes(64, m) + 1024 <= h->smem_optin;
+    // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
-    const size_t per_shift = 2 * (size_t)LDZ * m * 16 + (size_t)ncmax * m * 16 + 64;
+    const int64_t pst = two_level ? (int64_t)(kBlkNB + m) * m : (int64_t)ncmax * m;
+    const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64;
     int64_t sb_max = a.batch > 0 ? a.batch : a.s;
     {
         size_t fr = 0, tot = 0;
@@ -702,8 +863,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         if (rc) return rc;
     }
     double2* Z0 = (double2*)h->ws;
-    double2* Z1 = Z0 + (size_t)sb_max * m * LDZ;
-    double2* P0 = Z1 + (size_t)sb_max * m * LDZ;
+    double2* P0 = Z0 + (size_t)sb_max * m * LDZ;
 
     // Independent halves of a batch on two streams: the latency-bound block
     // RQ of one half overlaps the FP64-bound window update of the other.
@@ -724,11 +884,10 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         for (int p = 0; p < parts; ++p) {
             const int cnt = sb / parts + (p < sb % parts ? 1 : 0);
             PartBufs B;
-            B.Z[0] = Z0 + (size_t)off * m * LDZ;
-            B.Z[1] = Z1 + (size_t)off * m * LDZ;
-            B.P = P0 + (size_t)off * ncmax * m;
+            B.Z = Z0 + (size_t)off * m * LDZ;
+            B.P = P0 + (size_t)off * pst;
             int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, tile,
-                                  streams[p]);
+                                  two_level, streams[p]);
             if (rc) return rc;
             off += cnt;
         }

@@ -59,6 +59,11 @@ struct UpdDims {
     int nws;     // column blocks per shift
     int ksplit;  // warps per (shift, column block): 1, or 2 = panel K range split
     int jh;      // ksplit == 2: warp half 0 takes panel columns [0, jh) + the Z2 part
+    // P source (warp-specialised kernel): per shift, P12 = pstride*l + p12off
+    // (nb x m, j-major), P22 = pstride*l + p22off (m x m) unless zid (P22 = I:
+    // the far-row passes of the two-level sweep after the first)
+    int64_t pstride, p12off, p22off;
+    int zid;
 };
 
 __host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S) {

@@ -46,6 +46,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// Producer-side wait: the suspend-time hint parks the polling thread in the
+// barrier unit instead of spinning (a spinning producer took ~10% of the
+// kernel's issue slots from the consumers sharing its SMSP).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
                                              uint64_t* bar) {
     asm volatile(
@@ -66,7 +78,10 @@ __device__ __forceinline__ int pan_index_ws(int row) {
     return p * (2 * RG) + rg * 2 + e;
 }
 
-constexpr int kWsStages = 8;
+#ifndef SS_WS_STAGES
+#define SS_WS_STAGES 8
+#endif
+constexpr int kWsStages = SS_WS_STAGES;
 constexpr int kWsPairs = 4;
 constexpr int kWsThreads = 32 * (1 + 2 * kWsPairs);
 
@@ -76,12 +91,14 @@ __host__ __device__ inline size_t ws_smem_bytes(int nb, int m) {
     return 128 + (size_t)nb * kUpdRows * 8 + kWsStages * stage;
 }
 
-template <int G, int C>
+// ZID: the Z2 part is the identity (Zout = Zin + Pan P12): the second and
+// later far-row passes of the two-level sweep.  Zin may alias Zout (in-place:
+// every (row tile, shift) is read and written by one CTA only).
+template <int G, int C, bool ZID>
 __global__ void __launch_bounds__(kWsThreads, 1)
-    k_update_ws(UpdDims u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
-                const double2* __restrict__ Pbuf) {
+    k_update_ws(UpdDims u, const double2* Zin, double2* Zout, const double2* __restrict__ Pbuf) {
     constexpr int R = 2 * G, RG = 32 / G, M = G * C;  // one warp pair covers all m = M columns
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem[];
     const int nb = u.nb, nc = u.nc, r0 = u.r0;
     constexpr int m = M;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [kWsStages]
@@ -123,15 +140,18 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (warp == 0) {
         // ---------------- producer ----------------
         if (lane == 0) {
-            const unsigned pbytes = (unsigned)(nc * m * 16);
+            const unsigned p12bytes = (unsigned)(nb * m * 16);
+            const unsigned p22bytes = ZID ? 0u : (unsigned)(m * m * 16);
             const unsigned zbytes = (unsigned)(rows_valid * 16);
             for (int k = 0; k < nsh; ++k) {
                 const int s = k % kWsStages, use = k / kWsStages;
-                if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+                if (use > 0) mbar_wait_sleep(empty + s, (use - 1) & 1);
                 double2* st = Stg + (size_t)s * stage_el;
                 const int l = l0 + k;
-                mbar_expect_tx(full + s, pbytes + (unsigned)m * zbytes);
-                tma_bulk_g2s(st, Pbuf + (int64_t)l * nc * m, pbytes, full + s);
+                const double2* pl = Pbuf + (int64_t)l * u.pstride;
+                mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
+                tma_bulk_g2s(st, pl + u.p12off, p12bytes, full + s);
+                if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
                 double2* zt = st + (size_t)nc * m;
                 for (int c = 0; c < m; ++c)
                     tma_bulk_g2s(zt + c * kUpdRows, Zin + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
@@ -147,7 +167,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int cb = q * C;
     const int dlo = r0 - m;
     // interior tiles need neither the r0 row guard nor the lazy-shift rows
-    const bool interior = i0 + kUpdRows <= dlo;
+    const bool interior = i0 + kUpdRows <= (u.mnb > 0 ? dlo : r0);
     const int jlo = half == 0 ? 0 : u.jh;
     const int jhi = half == 1 ? nb : u.jh;
     const double* pan_l = Pan + rg * 2;
@@ -179,15 +199,23 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             }
         }
         if (half == 0) {
-            for (int j = 0; j < m; ++j) {
-                double2 z[R];
+            if (ZID) {
 #pragma unroll
-                for (int r = 0; r < R; ++r) z[r] = Zs[j * kUpdRows + rg + RG * r];
+                for (int c = 0; c < C; ++c)
 #pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    const double2 pv = Pl[(nb + j) * m + c];
+                    for (int r = 0; r < R; ++r)
+                        acc[r][c] = cadd(acc[r][c], Zs[(cb + c) * kUpdRows + rg + RG * r]);
+            } else {
+                for (int j = 0; j < m; ++j) {
+                    double2 z[R];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
+                    for (int r = 0; r < R; ++r) z[r] = Zs[j * kUpdRows + rg + RG * r];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const double2 pv = Pl[(nb + j) * m + c];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
+                    }
                 }
             }
         }
