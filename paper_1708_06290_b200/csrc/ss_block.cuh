@@ -51,74 +51,93 @@ struct BlkDims {
 
 __host__ __device__ inline size_t blk_smem_bytes(int m) {
     const int L = m + 1;
-    size_t b = 32 * 8;                      // one mbarrier per reflector of the inner window
+    size_t b = 0;
     b += (size_t)(kBlkInner + m) * m * 16;  // P
     b += (size_t)kBlkInner * L * 16;        // U
     b += (size_t)kBlkInner * 16;            // Tau
     b += (size_t)2 * 32 * 16;               // pivot broadcast
     b += (size_t)m * m * 16;                // W22
-    b += (size_t)kBlkNB * m * 16;           // block state / W rows, column-major [c][128]
     return b;
 }
 
-// P_i rows by forward accumulation: P = Q E with Q = H_{nbi-1} ... H_0, so
-// row r of P is e_r^T run through the same right-applied reflector sequence
-// as a block row (window of L columns sliding one column per reflector; the
-// entering column holds e_r's entry).  Two helper warps do this for the
-// nbi + m rows of P in lockstep with the reflector chain (one mbarrier per
-// reflector), so P is complete one step after the chain -- no serial
-// reverse accumulation.
+// Row update of the chain with FMA-chain dot products (two partial sums, no
+// add tree): z <- z - tau (z u) u^H over the L-column window.
+template <int L>
+__device__ __forceinline__ void blk_row_update(double2 (&z)[L], const double2* __restrict__ u,
+                                               double2 tau) {
+    double2 d0 = cz(), d1 = cz();
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        const double2 uj = u[j];
+        double2& d = (j & 1) ? d1 : d0;
+        d.x = fma(z[j].x, uj.x, d.x);
+        d.x = fma(-z[j].y, uj.y, d.x);
+        d.y = fma(z[j].x, uj.y, d.y);
+        d.y = fma(z[j].y, uj.x, d.y);
+    }
+    const double2 tw = cmul(tau, cadd(d0, d1));
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        const double2 uj = u[j];
+        z[j].x = fma(-tw.x, uj.x, fma(-tw.y, uj.y, z[j].x));
+        z[j].y = fma(-tw.y, uj.x, fma(tw.x, uj.y, z[j].y));
+    }
+}
+
+// One warp per shift.  Block row t of the outer block is handled by lane
+// (t + 128 - NBo) & 31 in pass (t + 128 - NBo) >> 5 in every phase, so the
+// inner window i is pass 3 - i, the state rows above it are passes < 3 - i
+// and the W rows below it passes > 3 - i; a row never changes lanes, so its
+// values can stay in the (L2-resident) window buffer Z / the W output
+// between phases without cross-lane hazards.  With 15 KB of shared memory
+// and one warp per CTA every shift's chain is resident at once: the chain is
+// a serial dependency (latency-bound), so the SM is filled with many chains
+// instead of one chain plus idle warps.
+//
+// After the chain, P_i = H_{nbi-1}(...(H_0 E)) by reverse accumulation:
+// lane pair (2c, 2c+1) owns column c of P, each lane half of the sliding
+// L-window (6 entries), so a step is 6 complex dot terms + one shuffle
+// exchange.
 template <int M>
-__global__ void __launch_bounds__(kBlkNB, SS_BLK_MINB)
-    k_block(BlkDims d, const double2* __restrict__ Z, double2* __restrict__ W) {
+__global__ void __launch_bounds__(32, 8)
+    k_block(BlkDims d, double2* __restrict__ Z, double2* __restrict__ W) {
     constexpr int L = M + 1;
+    constexpr int HW = 6;  // window entries per lane of a column pair (L <= 12)
+    static_assert(L <= 2 * HW, "k_block: m <= 11");
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* mb = reinterpret_cast<uint64_t*>(smem);                 // [32]
-    double2* P = reinterpret_cast<double2*>(smem + 32 * 8);          // [(32 + M) * M] j-major
-    double2* U = P + (kBlkInner + M) * M;                            // [32][L]
-    double2* Tau = U + kBlkInner * L;                                // [32]
-    double2* Piv = Tau + kBlkInner;                                  // [2][32]
-    double2* W22 = Piv + 64;                                         // [M][M]: W22[r * M + c]
-    double2* S = W22 + M * M;  // [M][128]: state row t (later W row t), column c at S[c*128 + tid]
+    double2* P = reinterpret_cast<double2*>(smem);  // [(32 + M) * M] j-major
+    double2* U = P + (kBlkInner + M) * M;           // [32][L]
+    double2* Tau = U + kBlkInner * L;               // [32]
+    double2* Piv = Tau + kBlkInner;                 // [2][32]
+    double2* W22 = Piv + 64;                        // [M][M]: W22[r * M + c]
 
     const int l = blockIdx.x;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int lane = threadIdx.x;
     const int NBo = d.NBo;
-    const int t = tid - (kBlkNB - NBo);  // block row of this thread (< 0: idle)
-    const bool active = t >= 0;
-    const int64_t arow = (int64_t)(d.k - NBo) + t;  // A row of block row t
+    const int off = kBlkNB - NBo;  // rows are numbered from the top of a 128-row frame
     const double2 sig = d.shifts[l];
     const double* Ab = d.A + (int64_t)d.c0 * d.lda;  // panel column 0
+    double2* Zl = Z + (int64_t)l * M * d.LDZ + d.r0;  // block row t, column c: Zl[c*LDZ + t]
+    double2* Wl = W + (int64_t)l * d.wstride;         // W row t, column c: Wl[t*M + c]
 
-    if (tid == 0) {
-        for (int q = 0; q < kBlkInner; ++q) mbar_init(mb + q, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // the block's state rows live in shared memory (column-major, one row per
-    // thread); only the RQ warp holds its rows in registers during its chain
-    {
-        const double2* zr = Z + (int64_t)l * M * d.LDZ + d.r0 + t;
-#pragma unroll
-        for (int c = 0; c < M; ++c) S[c * kBlkNB + tid] = active ? zr[(int64_t)c * d.LDZ] : cz();
-    }
-    for (int u = tid; u < M * M; u += kBlkNB) W22[u] = make_double2((u / M) == (u % M) ? 1.0 : 0.0, 0.0);
-    __syncthreads();
+    for (int u = lane; u < M * M; u += 32) W22[u] = make_double2((u / M) == (u % M) ? 1.0 : 0.0, 0.0);
 
     const int ni = (NBo + kBlkInner - 1) / kBlkInner;
     for (int i = 0; i < ni; ++i) {
         const int top = NBo - kBlkInner * i;  // rows [b, top) = inner block
         const int b = max(0, top - kBlkInner);
         const int nbi = top - b;
-        const int rqw = 3 - i;
-        const int hw = (warp - rqw - 1) & 3;  // helper index 0, 1 (2: idle)
-        if (warp == rqw) {
+        const int pass_rq = 3 - i;
+        {
             // ---------------- reflector chain over the inner block ----------------
+            const int t = pass_rq * 32 + lane - off;  // this lane's block row
             const int rho = t - b;
-            const bool mine = active && rho >= 0;
+            const bool mine = t >= 0 && rho >= 0;
+            const int64_t arow = (int64_t)(d.k - NBo) + t;
             double2 z[L];  // window: z[0] = panel column, z[1..L) = state
-#pragma unroll
-            for (int c = 0; c < M; ++c) z[c + 1] = S[c * kBlkNB + tid];
             z[0] = cz();
+#pragma unroll
+            for (int c = 0; c < M; ++c) z[c + 1] = mine ? Zl[(int64_t)c * d.LDZ + t] : cz();
             if (mine) {
                 z[0] = make_double2(Ab[arow + (int64_t)(b + nbi - 1) * d.lda], 0.0);
                 if (nbi - 1 == rho + M) z[0] = csub(z[0], sig);
@@ -132,7 +151,6 @@ __global__ void __launch_bounds__(kBlkNB, SS_BLK_MINB)
                     for (int j = 0; j < L; ++j) piv[j] = z[j];
                 }
                 __syncwarp();
-                // ||row||^2 without the pivot entry, and the pivot (redundant per lane)
                 double sq[L - 1];
 #pragma unroll
                 for (int j = 0; j < L - 1; ++j) {
@@ -159,7 +177,6 @@ __global__ void __launch_bounds__(kBlkNB, SS_BLK_MINB)
                     const double iz = rz * rz;
                     scale = make_double2(zx * iz, -zy * iz);
                 }
-                // lane j < L publishes u_j (u_{L-1} = 1) and tau
                 if (lane < L) {
                     const double2 x = piv[lane];
                     U[ti * L + lane] =
@@ -167,13 +184,7 @@ __global__ void __launch_bounds__(kBlkNB, SS_BLK_MINB)
                 }
                 if (lane == 0) Tau[ti] = tau;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(mb + ti);  // release U[ti], Tau[ti] to the helpers
-                if (mine && rho < ti) {
-                    double2 uu[L];
-#pragma unroll
-                    for (int j = 0; j < L; ++j) uu[j] = U[ti * L + j];
-                    rq_row_update<L>(z, uu, tau, L);
-                }
+                if (mine && rho < ti) blk_row_update<L>(z, U + ti * L, tau);
 #pragma unroll
                 for (int j = L - 1; j > 0; --j) z[j] = z[j - 1];
                 if (ti > 0) {
@@ -183,106 +194,129 @@ __global__ void __launch_bounds__(kBlkNB, SS_BLK_MINB)
                     if (mine && ti >= 2 && rho <= ti - 2) pf = Ab[arow + (int64_t)(b + ti - 2) * d.lda];
                 }
             }
-        } else if (hw < 2) {
-            // ---------------- P rows, one reflector behind the chain ----------------
-            const int pr = hw * 32 + lane;  // row of P_i
-            const bool prow = pr < nbi + M;
-            double2 w[L];
+            __syncwarp();
+        }
+        // ---------------- reverse accumulation -> P (j-major) ----------------
+        if (lane < 2 * M) {
+            const unsigned pm = 0x000fffffu >> (20 - 2 * M);
+            const int c = lane >> 1, hh = lane & 1, base = hh * HW;
+            double2 w[HW];
 #pragma unroll
-            for (int j = 0; j < L; ++j) w[j] = make_double2(pr == nbi - 1 + j ? 1.0 : 0.0, 0.0);
-            for (int ti = nbi - 1; ti >= 0; --ti) {
-                mbar_wait(mb + ti, i & 1);
-                const double2 ts = Tau[ti];
-                const double2* uu = U + ti * L;
-                double2 dp = cz(), dq = cz();
+            for (int k = 0; k < HW; ++k) w[k] = make_double2(base + k == c ? 1.0 : 0.0, 0.0);
+            for (int s = 0; s < nbi; ++s) {
+                const double2* us = U + s * L + base;
+                double2 dp = cz();
 #pragma unroll
-                for (int j = 0; j < L; j += 2) {
-                    dp = cfma(w[j], uu[j], dp);
-                    if (j + 1 < L) dq = cfma(w[j + 1], uu[j + 1], dq);
+                for (int k = 0; k < HW; ++k) {
+                    if (base + k < L) {
+                        const double2 uk = us[k];  // conj(u) w
+                        dp.x = fma(uk.x, w[k].x, dp.x);
+                        dp.x = fma(uk.y, w[k].y, dp.x);
+                        dp.y = fma(uk.x, w[k].y, dp.y);
+                        dp.y = fma(-uk.y, w[k].x, dp.y);
+                    }
                 }
-                const double2 tw = cmul(ts, cadd(dp, dq));
+                dp.x += __shfl_xor_sync(pm, dp.x, 1);
+                dp.y += __shfl_xor_sync(pm, dp.y, 1);
+                const double2 td = cmul(Tau[s], dp);
 #pragma unroll
-                for (int j = 0; j < L; ++j) {
-                    const double2 uj = uu[j];
-                    w[j].x = fma(-tw.x, uj.x, fma(-tw.y, uj.y, w[j].x));
-                    w[j].y = fma(-tw.y, uj.x, fma(tw.x, uj.y, w[j].y));
+                for (int k = 0; k < HW; ++k) {
+                    if (base + k < L) {
+                        const double2 uk = us[k];
+                        w[k].x = fma(-uk.x, td.x, fma(uk.y, td.y, w[k].x));
+                        w[k].y = fma(-uk.x, td.y, fma(-uk.y, td.x, w[k].y));
+                    }
                 }
-                if (ti > 0) {
+                if (hh == 0) P[s * M + c] = w[0];
+                const double nx = __shfl_xor_sync(pm, w[0].x, 1);
+                const double ny = __shfl_xor_sync(pm, w[0].y, 1);
 #pragma unroll
-                    for (int j = L - 1; j > 0; --j) w[j] = w[j - 1];
-                    w[0] = make_double2(pr == ti - 1 ? 1.0 : 0.0, 0.0);
+                for (int k = 0; k < HW - 1; ++k) w[k] = w[k + 1];
+                w[HW - 1] = hh == 0 ? make_double2(nx, ny) : cz();
+            }
+#pragma unroll
+            for (int k = 0; k < HW; ++k)
+                if (base + k < M) P[(nbi + base + k) * M + c] = w[k];
+        }
+        __syncwarp();
+        // ---------------- apply P_i: W22, then every row pass ----------------
+        {
+            double2 w22n[(M * M + 31) / 32];
+#pragma unroll
+            for (int e = 0; e < (M * M + 31) / 32; ++e) {
+                const int u = lane + 32 * e;
+                w22n[e] = cz();
+                if (u < M * M) {
+                    const int r = u / M, c = u - (u / M) * M;
+#pragma unroll
+                    for (int j = 0; j < M; ++j) w22n[e] = cfma(W22[r * M + j], P[(nbi + j) * M + c], w22n[e]);
                 }
             }
-            if (prow) {
+            __syncwarp();
 #pragma unroll
-                for (int c = 0; c < M; ++c) P[pr * M + c] = w[c];
+            for (int e = 0; e < (M * M + 31) / 32; ++e) {
+                const int u = lane + 32 * e;
+                if (u < M * M) W22[u] = w22n[e];
             }
         }
-        __syncthreads();  // P ready
-        // ---------------- apply P_i to every row of the block ----------------
-        double2 w22n = cz();
-        if (tid < M * M) {  // W22 <- W22 P22 (identity-part rows of W)
-            const int r = tid / M, c = tid - (tid / M) * M;
-#pragma unroll
-            for (int j = 0; j < M; ++j) w22n = cfma(W22[r * M + j], P[(nbi + j) * M + c], w22n);
-        }
-        if (active) {
+        for (int pass = 0; pass < 4; ++pass) {
+            const int t = pass * 32 + lane - off;
+            if (t < 0) continue;
             double2 acc[M];
-            if (t >= b && t < top) {
-                // finished inner-block row: becomes W row t = P12[t - b]
+            if (pass == pass_rq) {
+                // finished inner-block row: W row t = P12[t - b]
 #pragma unroll
-                for (int c = 0; c < M; ++c) acc[c] = P[(t - b) * M + c];
-            } else {
-                // state (t < b) or W row (t >= top): row <- row P22 (+ panel part)
+                for (int c = 0; c < M; ++c) Wl[(int64_t)t * M + c] = P[(t - b) * M + c];
+                continue;
+            }
+            const bool state = pass < pass_rq;  // t < b: state row; else W row
 #pragma unroll
-                for (int c = 0; c < M; ++c) acc[c] = cz();
+            for (int c = 0; c < M; ++c) acc[c] = cz();
 #pragma unroll
-                for (int j = 0; j < M; ++j) {
-                    const double2 zj = S[j * kBlkNB + tid];
+            for (int j = 0; j < M; ++j) {
+                const double2 zj = state ? Zl[(int64_t)j * d.LDZ + t] : Wl[(int64_t)t * M + j];
 #pragma unroll
-                    for (int c = 0; c < M; ++c) acc[c] = cfma(zj, P[(nbi + j) * M + c], acc[c]);
-                }
-                if (t < b) {
-                    const double* ap = Ab + arow + (int64_t)b * d.lda;
-                    int jj = 0;
-                    for (; jj + 4 <= nbi; jj += 4) {
-                        double av[4];
+                for (int c = 0; c < M; ++c) acc[c] = cfma(zj, P[(nbi + j) * M + c], acc[c]);
+            }
+            if (state) {
+                const double* ap = Ab + (int64_t)(d.k - NBo) + t + (int64_t)b * d.lda;
+                double av[8];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) av[e] = ap[(int64_t)(jj + e) * d.lda];
+                for (int e = 0; e < 8; ++e) av[e] = e < nbi ? ap[(int64_t)e * d.lda] : 0.0;
+                for (int jj = 0; jj < nbi; jj += 8) {
+                    double an[8];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e)
+                    for (int e = 0; e < 8; ++e)
+                        an[e] = jj + 8 + e < nbi ? ap[(int64_t)(jj + 8 + e) * d.lda] : 0.0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        if (jj + e < nbi) {
 #pragma unroll
                             for (int c = 0; c < M; ++c) acc[c] = rfma(av[e], P[(jj + e) * M + c], acc[c]);
+                        }
                     }
-                    for (; jj < nbi; ++jj) {
-                        const double av = ap[(int64_t)jj * d.lda];
 #pragma unroll
-                        for (int c = 0; c < M; ++c) acc[c] = rfma(av, P[jj * M + c], acc[c]);
-                    }
-                    // lazy shift: A's diagonal in column b + dd sits in row b - M + dd
-                    const int dd = t - (b - M);
-                    if (dd >= 0 && dd < min(M, nbi)) {
-#pragma unroll
-                        for (int c = 0; c < M; ++c) acc[c] = csub(acc[c], cmul(sig, P[dd * M + c]));
-                    }
+                    for (int e = 0; e < 8; ++e) av[e] = an[e];
                 }
-            }
+                // lazy shift: A's diagonal in column b + dd sits in row b - M + dd
+                const int dd = t - (b - M);
+                if (dd >= 0 && dd < min(M, nbi)) {
 #pragma unroll
-            for (int c = 0; c < M; ++c) S[c * kBlkNB + tid] = acc[c];
+                    for (int c = 0; c < M; ++c) acc[c] = csub(acc[c], cmul(sig, P[dd * M + c]));
+                }
+#pragma unroll
+                for (int c = 0; c < M; ++c) Zl[(int64_t)c * d.LDZ + t] = acc[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < M; ++c) Wl[(int64_t)t * M + c] = acc[c];
+            }
         }
-        __syncthreads();  // everyone done with P / W22 (old)
-        if (tid < M * M) W22[tid] = w22n;
+        __syncwarp();
     }
-    __syncthreads();
-    // ---------------- W out: rows [0, NBo) from registers, W22 from smem ----------------
-    double2* wl = W + (int64_t)l * d.wstride;
-    for (int u = tid; u < NBo * M; u += kBlkNB) {  // coalesced: W is j-major
+    // W22 rows [NBo, NBo + m)
+    for (int u = lane; u < M * M; u += 32) {
         const int r = u / M, c = u - (u / M) * M;
-        wl[u] = S[c * kBlkNB + (kBlkNB - NBo) + r];
-    }
-    for (int u = tid; u < M * M; u += kBlkNB) {
-        const int r = u / M, c = u - (u / M) * M;
-        wl[(int64_t)(NBo + r) * M + c] = W22[r * M + c];
+        Wl[(int64_t)(NBo + r) * M + c] = W22[r * M + c];
     }
 }
 

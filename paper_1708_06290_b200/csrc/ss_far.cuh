@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(kFarThreads, 1)
             const unsigned p22bytes = ZID ? 0u : (unsigned)(m * m * 16);
             for (int k = 0; k < nun; ++k) {
                 const int s = k % kFarStages, use = k / kFarStages;
-                if (use > 0) mbar_wait_sleep(empty + s, (use - 1) & 1);
+                if (use > 0) {
+                    if (u.flags & 1) mbar_wait(empty + s, (use - 1) & 1);
+                    else mbar_wait_sleep(empty + s, (use - 1) & 1);
+                }
                 const int64_t unit = ua + k;
                 const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
                 const int i0 = u.rlo + tile * kUpdRows;

@@ -499,7 +499,7 @@ struct PartBufs {
 // Enqueue the whole sweep (seed, window steps, head) for shifts
 // [lo, lo + sb) of the call on stream `st`.
 int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, const BlkDims& bd,
-                 const double2* Z, double2* W) {
+                 double2* Z, double2* W) {
     switch (m) {
 #define SS_CASE(K)                                                        \
     case K: {                                                             \
@@ -508,7 +508,7 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
             SS_CUDA_TRY(h, allow_max_smem(h, k_block<K>));                \
             configured = true;                                            \
         }                                                                 \
-        k_block<K><<<sb, kBlkNB, smem, st>>>(bd, Z, W);                   \
+        k_block<K><<<sb, 32, smem, st>>>(bd, Z, W);                   \
         break;                                                            \
     }
         SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
@@ -619,6 +619,9 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 // half 0 also carries the Z2 part (two panel columns' worth of
                 // DFMA per column of m unless it is the identity) and the epilogue
                 u.jh = u.zid ? nbp / 2 : std::max(0, std::min(nbp, (nbp - 2 * m) / 2 - 1));
+                u.flags = 0;
+                if (const char* e = getenv("SS_FAR_JH")) u.jh = std::max(0, std::min(nbp, u.jh + atoi(e)));
+                if (getenv("SS_FAR_SPIN")) u.flags |= 1;
                 // algorithmic flops: every far panel row is structurally nonzero
                 const double nnz = ((a.mode == 0 ? (double)a.p : 0.0) + (double)(ko - NBo)) * nbp +
                                    (a.mode == 1 ? (double)nbp : 0.0);
@@ -725,6 +728,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         u.p12off = 0;
         u.p22off = (int64_t)s.nb * m;
         u.zid = 0;
+        u.flags = 0;
         u.nws = nws;
         // a warp pair splits the panel K range of one (shift, column block) when
         // one block covers all m columns: twice the warps on the same staging
@@ -867,8 +871,10 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     // Independent halves of a batch on two streams: the latency-bound block
     // RQ of one half overlaps the FP64-bound window update of the other.
+    // (the two-level sweep's persistent far-row kernel owns every SM, so it
+    // runs on one stream; the one-level sweep overlaps two halves)
     const char* sv = getenv("SS_STREAMS");
-    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : 2;
+    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : (two_level ? 1 : 2);
     if (sb_max < 64) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {

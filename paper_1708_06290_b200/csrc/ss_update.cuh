@@ -64,6 +64,7 @@ struct UpdDims {
     // the far-row passes of the two-level sweep after the first)
     int64_t pstride, p12off, p22off;
     int zid;
+    int flags;  // experiment knobs (bit 0: producer spins instead of parking)
 };
 
 __host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S) {
