@@ -325,7 +325,7 @@ def main():
     f_alg = 2.0 * n * n * m + 4.0 * n * m * (m + p)
     sweep_tflops = f_alg * value / world / 1e12
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r1_update_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r1_far_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")

@@ -22,42 +22,53 @@
 
 namespace ssd {
 
-constexpr int kFarStages = 8;
-constexpr int kFarPairs = 4;
-constexpr int kFarThreads = 32 * (1 + 2 * kFarPairs);
+// Tile shape (template): lane = (row group rg < 32/G, column group q < G),
+// R rows x C columns per lane, tile = (32/G) R rows.  NPAIR consumer pairs,
+// NST ring stages.
+__host__ __device__ constexpr int far_threads(int npair) { return 32 * (1 + 2 * npair); }
 
-__host__ __device__ inline size_t far_smem_bytes(int nb, int m) {
+__host__ __device__ inline size_t far_smem_bytes(int nb, int m, int tile, int nst) {
     const int nc = nb + m;
-    const size_t stage = ((size_t)nc * m + (size_t)m * kUpdRows) * 16;
-    return 256 + (size_t)nb * kUpdRows * 8 + kFarStages * stage;
+    const size_t stage = ((size_t)nc * m + (size_t)m * tile) * 16;
+    return 256 + (size_t)nb * tile * 8 + nst * stage;
 }
 
-template <int G, int C, bool ZID>
-__global__ void __launch_bounds__(kFarThreads, 1)
+// panel position of tile row `row`: lane row group rg owns rows rg + RG*w;
+// rows (rg + RG*2p, rg + RG*(2p+1)) are adjacent so one LDS.128 feeds two
+template <int G>
+__device__ __forceinline__ int far_pan_index(int row) {
+    constexpr int RG = 32 / G;
+    const int rg = row % RG, w = row / RG, p = w >> 1, e = w & 1;
+    return p * (2 * RG) + rg * 2 + e;
+}
+
+template <int G, int C, int R, int NPAIR, int NST, bool ZID>
+__global__ void __launch_bounds__(far_threads(NPAIR), 1)
     k_far(UpdDims u, double2* Z, const double2* __restrict__ Pbuf) {
-    constexpr int R = 2 * G, RG = 32 / G, M = G * C;
+    constexpr int RG = 32 / G, M = G * C, TILE = RG * R;
     constexpr int m = M;
+    static_assert(R % 2 == 0 && 2 * NST + 2 * NPAIR <= 32, "k_far: shape");
     extern __shared__ __align__(16) unsigned char smem[];
     const int nb = u.nb, nc = u.nc, r0 = u.r0, sb = u.sb;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [kFarStages]
-    uint64_t* empty = full + kFarStages;                   // [kFarStages]
-    uint64_t* zfree = empty + kFarStages;                  // [kFarPairs]
-    uint64_t* partr = zfree + kFarPairs;                   // [kFarPairs]
-    double* Pan = reinterpret_cast<double*>(smem + 256);   // [nb][64] pair-interleaved
-    double2* Stg = reinterpret_cast<double2*>(smem + 256 + (size_t)nb * kUpdRows * 8);
-    const size_t stage_el = (size_t)nc * m + (size_t)m * kUpdRows;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NST]
+    uint64_t* empty = full + NST;                          // [NST]
+    uint64_t* zfree = empty + NST;                         // [NPAIR]
+    uint64_t* partr = zfree + NPAIR;                       // [NPAIR]
+    double* Pan = reinterpret_cast<double*>(smem + 256);   // [nb][TILE] pair-interleaved
+    double2* Stg = reinterpret_cast<double2*>(smem + 256 + (size_t)nb * TILE * 8);
+    const size_t stage_el = (size_t)nc * m + (size_t)m * TILE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ntiles = (r0 - u.rlo + kUpdRows - 1) / kUpdRows;
+    const int ntiles = (r0 - u.rlo + TILE - 1) / TILE;
     const int64_t units = (int64_t)ntiles * sb;
     const int64_t ua = units * blockIdx.x / gridDim.x, ub = units * (blockIdx.x + 1) / gridDim.x;
     const int nun = (int)(ub - ua);
 
     if (tid == 0) {
-        for (int s = 0; s < kFarStages; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 2);
         }
-        for (int p = 0; p < kFarPairs; ++p) {
+        for (int p = 0; p < NPAIR; ++p) {
             mbar_init(zfree + p, 1);
             mbar_init(partr + p, 1);
         }
@@ -72,15 +83,15 @@ __global__ void __launch_bounds__(kFarThreads, 1)
             const unsigned p12bytes = (unsigned)(nb * m * 16);
             const unsigned p22bytes = ZID ? 0u : (unsigned)(m * m * 16);
             for (int k = 0; k < nun; ++k) {
-                const int s = k % kFarStages, use = k / kFarStages;
+                const int s = k % NST, use = k / NST;
                 if (use > 0) {
                     if (u.flags & 1) mbar_wait(empty + s, (use - 1) & 1);
                     else mbar_wait_sleep(empty + s, (use - 1) & 1);
                 }
                 const int64_t unit = ua + k;
                 const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
-                const int i0 = u.rlo + tile * kUpdRows;
-                const unsigned zbytes = (unsigned)(min(kUpdRows, r0 - i0) * 16);
+                const int i0 = u.rlo + tile * TILE;
+                const unsigned zbytes = (unsigned)(min(TILE, r0 - i0) * 16);
                 double2* st = Stg + (size_t)s * stage_el;
                 const double2* pl = Pbuf + (int64_t)l * u.pstride;
                 mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
@@ -88,7 +99,7 @@ __global__ void __launch_bounds__(kFarThreads, 1)
                 if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
                 double2* zt = st + (size_t)nc * m;
                 for (int c = 0; c < m; ++c)
-                    tma_bulk_g2s(zt + c * kUpdRows, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
+                    tma_bulk_g2s(zt + c * TILE, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
                                  full + s);
             }
         }
@@ -107,13 +118,13 @@ __global__ void __launch_bounds__(kFarThreads, 1)
     const int tfirst = (int)(ua / sb), tlast = (int)((ub - 1) / sb);
     for (int tile = tfirst; tile <= tlast; ++tile) {
         // (re)stage the panel tile: every consumer is done with the old one
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * kFarPairs) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * NPAIR) : "memory");
         {
-            const int i0n = u.rlo + tile * kUpdRows;
-            for (int v = tid - 32; v < nb * kUpdRows; v += 32 * 2 * kFarPairs) {
-                const int j = v >> 6, rr = v & 63;
+            const int i0n = u.rlo + tile * TILE;
+            for (int v = tid - 32; v < nb * TILE; v += 32 * 2 * NPAIR) {
+                const int j = v / TILE, rr = v - j * TILE;
                 const int i = i0n + rr, col = u.c0 + j;
-                double* dst = Pan + j * kUpdRows + pan_index_ws<G>(rr);
+                double* dst = Pan + j * TILE + far_pan_index<G>(rr);
                 if (i >= r0) {
                     *dst = 0.0;
                 } else if (i >= u.ptop) {
@@ -126,16 +137,16 @@ __global__ void __launch_bounds__(kFarThreads, 1)
             }
             cp_async_commit_wait_all();
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * kFarPairs) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * NPAIR) : "memory");
         // this tile's units of the CTA range: k in [ka, kb); pair p takes k = p mod 4
         const int ka = (int)(max(ua, (int64_t)tile * sb) - ua);
         const int kb = (int)(min(ub, (int64_t)(tile + 1) * sb) - ua);
         const int l0t = (int)(ua + ka - (int64_t)tile * sb) - ka;  // l = l0t + k
-        for (int k = ka + ((pair - ka) & (kFarPairs - 1)); k < kb; k += kFarPairs) {
+        for (int k = ka + (((pair - ka) % NPAIR) + NPAIR) % NPAIR; k < kb; k += NPAIR) {
         const int l = l0t + k;
-        const int i0 = u.rlo + tile * kUpdRows;
-        const bool interior = i0 + kUpdRows <= (u.mnb > 0 ? dlo : r0);
-        const int s = k % kFarStages, use = k / kFarStages;
+        const int i0 = u.rlo + tile * TILE;
+        const bool interior = i0 + TILE <= (u.mnb > 0 ? dlo : r0);
+        const int s = k % NST, use = k / NST;
         mbar_wait(full + s, use & 1);
         double2* st = Stg + (size_t)s * stage_el;
         const double2* Pl = st + cb;
@@ -151,12 +162,12 @@ __global__ void __launch_bounds__(kFarThreads, 1)
 #pragma unroll
                 for (int c = 0; c < C; ++c)
 #pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r][c] = Zs[(cb + c) * kUpdRows + rg + RG * r];
+                    for (int r = 0; r < R; ++r) acc[r][c] = Zs[(cb + c) * TILE + rg + RG * r];
             } else {
                 for (int j = 0; j < m; ++j) {
                     double2 z[R];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) z[r] = Zs[j * kUpdRows + rg + RG * r];
+                    for (int r = 0; r < R; ++r) z[r] = Zs[j * TILE + rg + RG * r];
 #pragma unroll
                     for (int c = 0; c < C; ++c) {
                         const double2 pv = Pl[(nb + j) * m + c];
@@ -173,7 +184,7 @@ __global__ void __launch_bounds__(kFarThreads, 1)
             double a[R];
 #pragma unroll
             for (int p = 0; p < R / 2; ++p) {
-                const double2 v = *reinterpret_cast<const double2*>(pan_l + j * kUpdRows + p * (2 * RG));
+                const double2 v = *reinterpret_cast<const double2*>(pan_l + j * TILE + p * (2 * RG));
                 a[2 * p] = v.x;
                 a[2 * p + 1] = v.y;
             }

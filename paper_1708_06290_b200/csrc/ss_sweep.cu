@@ -396,28 +396,43 @@ int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, co
     return launch_update_ws_z<G, C, false>(h, grid, smem, st, u, zin, zout, pbuf);
 }
 
-template <int G, int C, bool ZID>
+template <int G, int C, int R, int NPAIR, int NST, bool ZID>
 int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                  const double2* pbuf) {
     static bool configured = false;
     if (!configured) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, ZID>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID>));
         configured = true;
     }
-    k_far<G, C, ZID><<<grid, kFarThreads, smem, st>>>(u, z, pbuf);
+    k_far<G, C, R, NPAIR, NST, ZID><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
 
+// Far-row kernel shape: R rows x C columns per lane, 32/G row groups -> a
+// tile of (32/G) R rows; NPAIR consumer pairs; NST ring stages.
+struct FarShape {
+    int G, C, R, NPAIR, NST;
+    int tile() const { return (32 / G) * R; }
+};
+
+FarShape far_shape(const UpdTile& t) {
+    // measured on B200 (config 2): R = 8 rows per lane with 3 pairs / 5 stages
+    // (255 registers, spills) is slower than R = 2G with 4 pairs / 8 stages
+    if (t.G == 2 && t.C == 5 && getenv("SS_FAR_R8")) return FarShape{2, 5, 8, 3, 5};
+    return FarShape{t.G, t.C, 2 * t.G, 4, 8};
+}
+
 // Persistent far-row update (ss_far.cuh): one CTA per SM over (tile, shift) units.
-int launch_far(ss_handle* h, const UpdTile& t, int grid, size_t smem, cudaStream_t st,
+int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStream_t st,
                const UpdDims& u, double2* z, const double2* pbuf) {
-#define SS_FAR(GG, CC)                                                                  \
-    if (t.G == GG && t.C == CC)                                                         \
-        return u.zid ? launch_far_z<GG, CC, true>(h, grid, smem, st, u, z, pbuf)        \
-                     : launch_far_z<GG, CC, false>(h, grid, smem, st, u, z, pbuf);
-    SS_FAR(2, 5) SS_FAR(2, 4) SS_FAR(1, 1) SS_FAR(1, 2) SS_FAR(1, 3) SS_FAR(1, 4) SS_FAR(1, 5)
-    SS_FAR(1, 6) SS_FAR(1, 7) SS_FAR(1, 8)
+#define SS_FAR(GG, CC, RR, NP, NS)                                                             \
+    if (f.G == GG && f.C == CC && f.R == RR && f.NPAIR == NP && f.NST == NS)                   \
+        return u.zid ? launch_far_z<GG, CC, RR, NP, NS, true>(h, grid, smem, st, u, z, pbuf)   \
+                     : launch_far_z<GG, CC, RR, NP, NS, false>(h, grid, smem, st, u, z, pbuf);
+    SS_FAR(2, 5, 8, 3, 5) SS_FAR(2, 5, 4, 4, 8) SS_FAR(2, 4, 4, 4, 8)
+    SS_FAR(1, 1, 2, 4, 8) SS_FAR(1, 2, 2, 4, 8) SS_FAR(1, 3, 2, 4, 8) SS_FAR(1, 4, 2, 4, 8)
+    SS_FAR(1, 5, 2, 4, 8) SS_FAR(1, 6, 2, 4, 8) SS_FAR(1, 7, 2, 4, 8) SS_FAR(1, 8, 2, 4, 8)
 #undef SS_FAR
     return SS_EARG;
 }
@@ -631,9 +646,11 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (getenv("SS_FAR_CLASSIC")) {
                     rc = launch_update_ws(h, tile, gw, ws_smem_bytes(nbp, m), st, u, B.Z, B.Z, B.P);
                 } else {
-                    const int64_t units = (int64_t)gw.x * sb;
+                    const FarShape f = far_shape(tile);
+                    const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * sb;
                     const int grid = (int)std::min<int64_t>(units, h->num_sms);
-                    rc = launch_far(h, tile, grid, far_smem_bytes(nbp, m), st, u, B.Z, B.P);
+                    rc = launch_far(h, f, grid, far_smem_bytes(nbp, m, f.tile(), f.NST), st, u, B.Z,
+                                    B.P);
                 }
                 if (rc) return ss::set_err(h, rc, "two-level far update: unsupported tile");
                 // reference-phase split of the measured time by the far update's shares

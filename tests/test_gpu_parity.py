@@ -374,3 +374,36 @@ def test_block_rq_flavours_agree(case, monkeypatch):
     Gg = ss.eval_transfer_function(chf, shifts, nb=nb).G
     assert per_shift_rel(Gh, Gg, m, len(shifts)) <= 1e-12
     assert per_shift_rel(Gg, S[pre + "G"], m, len(shifts)) <= 1e-10
+
+
+def _mhess_triple(n, m, p, seed):
+    """Random m-Hessenberg / triangular / dense triple of the reduced shape."""
+    rng = np.random.default_rng(seed)
+    A = np.triu(rng.standard_normal((n, n)), -m) - 1.1 * np.sqrt(n) * np.eye(n)
+    B = np.zeros((n, m))
+    B[:m, :m] = np.triu(rng.standard_normal((m, m))) + 2 * np.eye(m)
+    C = rng.standard_normal((p, n))
+    return ss.ControllerHessForm(Ahat=np.asfortranarray(A), Bhat=np.asfortranarray(B),
+                                 Chat=np.asfortranarray(C), m=m, n=n, p=p)
+
+
+@pytest.mark.parametrize("n,m,p", [(300, 10, 10), (517, 10, 3), (161, 1, 1), (40, 5, 2),
+                                   (389, 2, 4), (455, 3, 3), (260, 7, 5), (700, 8, 8), (129, 4, 1)])
+def test_two_level_vs_one_level(n, m, p, monkeypatch):
+    """The two-level sweep (k_block + k_far over 128-column outer blocks, the
+    default for m in 1..8, 10) against the per-window sweep (SS_ONE_LEVEL=1)
+    and the C oracle, on ragged sizes (n - m not a multiple of 128 or 32)."""
+    chf = _mhess_triple(n, m, p, seed=n * 31 + m)
+    shifts = 1j * np.logspace(-2, 2, 37) * np.sqrt(n) + 0.2
+    G2 = ss.eval_transfer_function(chf, shifts, nb=64).G
+    bd = np.exp(1j * np.arange(m * 5).reshape(m, 5))
+    X2 = ss.solve_shifted_reduced(chf, shifts[:5], bd, nb=64).x
+    monkeypatch.setenv("SS_ONE_LEVEL", "1")
+    G1 = ss.eval_transfer_function(chf, shifts, nb=64).G
+    X1 = ss.solve_shifted_reduced(chf, shifts[:5], bd, nb=64).x
+    assert per_shift_rel(G2, G1, m, len(shifts)) <= 1e-12
+    assert max(rel(X2[:, k], X1[:, k]) for k in range(5)) <= 1e-12
+    idx = [0, 18, 36]
+    Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts[idx], nb=32)
+    for k, l in enumerate(idx):
+        assert rel(G2[:, l * m:(l + 1) * m], Go[:, k * m:(k + 1) * m]) <= 1e-10
