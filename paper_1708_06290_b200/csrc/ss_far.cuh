@@ -78,29 +78,43 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     if (nun <= 0) return;
 
     if (warp == 0) {
-        // ---------------- producer: stages in unit order ----------------
+        // ---------------- producer ----------------
+        // Unit k belongs to pair k % NPAIR and stage k % NST.  The producer
+        // refills whichever pair's next stage is free first (non-blocking
+        // polls), so one slow pair does not hold back the others' prefetch.
         if (lane == 0) {
             const unsigned p12bytes = (unsigned)(nb * m * 16);
             const unsigned p22bytes = ZID ? 0u : (unsigned)(m * m * 16);
-            for (int k = 0; k < nun; ++k) {
-                const int s = k % NST, use = k / NST;
-                if (use > 0) {
-                    if (u.flags & 1) mbar_wait(empty + s, (use - 1) & 1);
-                    else mbar_wait_sleep(empty + s, (use - 1) & 1);
+            int next[NPAIR];
+#pragma unroll
+            for (int p = 0; p < NPAIR; ++p) next[p] = p;
+            int left = nun;
+            while (left > 0) {
+                bool any = false;
+#pragma unroll
+                for (int p = 0; p < NPAIR; ++p) {
+                    const int k = next[p];
+                    if (k >= nun) continue;
+                    const int s = k % NST, use = k / NST;
+                    if (use > 0 && !mbar_test(empty + s, (use - 1) & 1)) continue;
+                    const int64_t unit = ua + k;
+                    const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
+                    const int i0 = u.rlo + tile * TILE;
+                    const unsigned zbytes = (unsigned)(min(TILE, r0 - i0) * 16);
+                    double2* st = Stg + (size_t)s * stage_el;
+                    const double2* pl = Pbuf + (int64_t)l * u.pstride;
+                    mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
+                    tma_bulk_g2s(st, pl + u.p12off, p12bytes, full + s);
+                    if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
+                    double2* zt = st + (size_t)nc * m;
+                    for (int c = 0; c < m; ++c)
+                        tma_bulk_g2s(zt + c * TILE, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
+                                     full + s);
+                    next[p] = k + NPAIR;
+                    --left;
+                    any = true;
                 }
-                const int64_t unit = ua + k;
-                const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
-                const int i0 = u.rlo + tile * TILE;
-                const unsigned zbytes = (unsigned)(min(TILE, r0 - i0) * 16);
-                double2* st = Stg + (size_t)s * stage_el;
-                const double2* pl = Pbuf + (int64_t)l * u.pstride;
-                mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
-                tma_bulk_g2s(st, pl + u.p12off, p12bytes, full + s);
-                if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
-                double2* zt = st + (size_t)nc * m;
-                for (int c = 0; c < m; ++c)
-                    tma_bulk_g2s(zt + c * TILE, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
-                                 full + s);
+                if (!any) __nanosleep(128);
             }
         }
         return;

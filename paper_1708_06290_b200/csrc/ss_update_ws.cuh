@@ -58,6 +58,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
         "r"(parity), "r"(1000000u)
         : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    unsigned r;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(r)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return r != 0;
+}
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
                                              uint64_t* bar) {
     asm volatile(
