@@ -49,7 +49,7 @@ struct BlkDims {
     int64_t wstride;  // elements (complex) per shift in W
 };
 
-__host__ __device__ inline size_t blk_smem_bytes(int m) {
+__host__ __device__ inline size_t blk_smem_bytes_1(int m) {
     const int L = m + 1;
     size_t b = 0;
     b += (size_t)(kBlkInner + m) * m * 16;  // P
@@ -58,6 +58,12 @@ __host__ __device__ inline size_t blk_smem_bytes(int m) {
     b += (size_t)2 * 32 * 16;               // pivot broadcast
     b += (size_t)m * m * 16;                // W22
     return b;
+}
+
+constexpr int kBlkShiftsPerWarp = 1;  // 2 measured slower on B200 (per-warp issue bound)
+
+__host__ __device__ inline size_t blk_smem_bytes(int m) {
+    return kBlkShiftsPerWarp * blk_smem_bytes_1(m);
 }
 
 // Row update of the chain with FMA-chain dot products (two partial sums, no
@@ -84,43 +90,103 @@ __device__ __forceinline__ void blk_row_update(double2 (&z)[L], const double2* _
     }
 }
 
-// One warp per shift.  Block row t of the outer block is handled by lane
-// (t + 128 - NBo) & 31 in pass (t + 128 - NBo) >> 5 in every phase, so the
-// inner window i is pass 3 - i, the state rows above it are passes < 3 - i
-// and the W rows below it passes > 3 - i; a row never changes lanes, so its
-// values can stay in the (L2-resident) window buffer Z / the W output
-// between phases without cross-lane hazards.  With 15 KB of shared memory
-// and one warp per CTA every shift's chain is resident at once: the chain is
-// a serial dependency (latency-bound), so the SM is filled with many chains
-// instead of one chain plus idle warps.
+// One warp per NSW shifts.  Block row t of the outer block is handled by
+// lane (t + 128 - NBo) & 31 in pass (t + 128 - NBo) >> 5 in every phase, so
+// the inner window i is pass 3 - i, the state rows above it are passes
+// < 3 - i and the W rows below it passes > 3 - i; a row never changes lanes,
+// so its values can stay in the (L2-resident) window buffer Z / the W output
+// between phases without cross-lane hazards.
 //
+// The reflector chain is a serial dependency: a warp running one shift's
+// chain is latency-bound (measured ~3.7 cycles per instruction).  Each warp
+// therefore carries NSW = 2 shifts through identical control flow (the row
+// mapping does not depend on the shift), so every phase issues two
+// independent instruction streams back to back and the second hides the
+// first's latencies; all shifts' chains stay resident (15 KB of shared
+// memory per shift).
+//
+// NSW independent row updates with the shift index innermost, so the two
+// dependency chains interleave instruction by instruction.
+template <int L, int NSW>
+__device__ __forceinline__ void blk_row_update_n(double2 (&z)[NSW][L], double2* const (&U)[NSW],
+                                                 int off, const double2 (&tau)[NSW]) {
+    double2 d0[NSW], d1[NSW];
+#pragma unroll
+    for (int q = 0; q < NSW; ++q) d0[q] = d1[q] = cz();
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+#pragma unroll
+        for (int q = 0; q < NSW; ++q) {
+            const double2 uj = U[q][off + j];
+            double2& dd = (j & 1) ? d1[q] : d0[q];
+            dd.x = fma(z[q][j].x, uj.x, dd.x);
+            dd.y = fma(z[q][j].x, uj.y, dd.y);
+        }
+#pragma unroll
+        for (int q = 0; q < NSW; ++q) {
+            const double2 uj = U[q][off + j];
+            double2& dd = (j & 1) ? d1[q] : d0[q];
+            dd.x = fma(-z[q][j].y, uj.y, dd.x);
+            dd.y = fma(z[q][j].y, uj.x, dd.y);
+        }
+    }
+    double2 tw[NSW];
+#pragma unroll
+    for (int q = 0; q < NSW; ++q) tw[q] = cmul(tau[q], cadd(d0[q], d1[q]));
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+#pragma unroll
+        for (int q = 0; q < NSW; ++q) {
+            const double2 uj = U[q][off + j];
+            z[q][j].x = fma(-tw[q].x, uj.x, fma(-tw[q].y, uj.y, z[q][j].x));
+            z[q][j].y = fma(-tw[q].y, uj.x, fma(tw[q].x, uj.y, z[q][j].y));
+        }
+    }
+}
+
 // After the chain, P_i = H_{nbi-1}(...(H_0 E)) by reverse accumulation:
 // lane pair (2c, 2c+1) owns column c of P, each lane half of the sliding
 // L-window (6 entries), so a step is 6 complex dot terms + one shuffle
 // exchange.
-template <int M>
-__global__ void __launch_bounds__(32, 8)
-    k_block(BlkDims d, double2* __restrict__ Z, double2* __restrict__ W) {
+template <int M, int NSW>
+__global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
+    k_block(BlkDims d, double2* __restrict__ Z, double2* __restrict__ W, int sb) {
     constexpr int L = M + 1;
     constexpr int HW = 6;  // window entries per lane of a column pair (L <= 12)
     static_assert(L <= 2 * HW, "k_block: m <= 11");
     extern __shared__ __align__(16) unsigned char smem[];
-    double2* P = reinterpret_cast<double2*>(smem);  // [(32 + M) * M] j-major
-    double2* U = P + (kBlkInner + M) * M;           // [32][L]
-    double2* Tau = U + kBlkInner * L;               // [32]
-    double2* Piv = Tau + kBlkInner;                 // [2][32]
-    double2* W22 = Piv + 64;                        // [M][M]: W22[r * M + c]
-
-    const int l = blockIdx.x;
+    constexpr int PSZ = (kBlkInner + M) * M, USZ = kBlkInner * L;
+    constexpr int QSZ = PSZ + USZ + kBlkInner + 64 + M * M;  // complex per shift
+    double2* P[NSW];
+    double2* U[NSW];
+    double2* Tau[NSW];
+    double2* Piv[NSW];
+    double2* W22[NSW];
     const int lane = threadIdx.x;
     const int NBo = d.NBo;
     const int off = kBlkNB - NBo;  // rows are numbered from the top of a 128-row frame
-    const double2 sig = d.shifts[l];
     const double* Ab = d.A + (int64_t)d.c0 * d.lda;  // panel column 0
-    double2* Zl = Z + (int64_t)l * M * d.LDZ + d.r0;  // block row t, column c: Zl[c*LDZ + t]
-    double2* Wl = W + (int64_t)l * d.wstride;         // W row t, column c: Wl[t*M + c]
-
-    for (int u = lane; u < M * M; u += 32) W22[u] = make_double2((u / M) == (u % M) ? 1.0 : 0.0, 0.0);
+    double2 sig[NSW];
+    double2* Zl[NSW];
+    double2* Wl[NSW];
+    bool vq[NSW];
+#pragma unroll
+    for (int q = 0; q < NSW; ++q) {
+        double2* base = reinterpret_cast<double2*>(smem) + q * QSZ;
+        P[q] = base;
+        U[q] = P[q] + PSZ;
+        Tau[q] = U[q] + USZ;
+        Piv[q] = Tau[q] + kBlkInner;
+        W22[q] = Piv[q] + 64;
+        const int lq = blockIdx.x * NSW + q;
+        vq[q] = lq < sb;
+        const int l = vq[q] ? lq : sb - 1;  // a missing partner shadows the last shift
+        sig[q] = d.shifts[l];
+        Zl[q] = Z + (int64_t)l * M * d.LDZ + d.r0;  // block row t, column c: Zl[c*LDZ + t]
+        Wl[q] = W + (int64_t)l * d.wstride;         // W row t, column c: Wl[t*M + c]
+        for (int u = lane; u < M * M; u += 32)
+            W22[q][u] = make_double2((u / M) == (u % M) ? 1.0 : 0.0, 0.0);
+    }
 
     const int ni = (NBo + kBlkInner - 1) / kBlkInner;
     for (int i = 0; i < ni; ++i) {
@@ -129,68 +195,87 @@ __global__ void __launch_bounds__(32, 8)
         const int nbi = top - b;
         const int pass_rq = 3 - i;
         {
-            // ---------------- reflector chain over the inner block ----------------
+            // ---------------- reflector chains over the inner block ----------------
             const int t = pass_rq * 32 + lane - off;  // this lane's block row
             const int rho = t - b;
             const bool mine = t >= 0 && rho >= 0;
             const int64_t arow = (int64_t)(d.k - NBo) + t;
-            double2 z[L];  // window: z[0] = panel column, z[1..L) = state
-            z[0] = cz();
-#pragma unroll
-            for (int c = 0; c < M; ++c) z[c + 1] = mine ? Zl[(int64_t)c * d.LDZ + t] : cz();
-            if (mine) {
-                z[0] = make_double2(Ab[arow + (int64_t)(b + nbi - 1) * d.lda], 0.0);
-                if (nbi - 1 == rho + M) z[0] = csub(z[0], sig);
-            }
+            double2 z[NSW][L];  // window: z[0] = panel column, z[1..L) = state
             double pf = 0.0;
-            if (mine && nbi >= 2 && rho <= nbi - 2) pf = Ab[arow + (int64_t)(b + nbi - 2) * d.lda];
+            {
+                const double a0 = mine ? Ab[arow + (int64_t)(b + nbi - 1) * d.lda] : 0.0;
+                if (mine && nbi >= 2 && rho <= nbi - 2) pf = Ab[arow + (int64_t)(b + nbi - 2) * d.lda];
+#pragma unroll
+                for (int q = 0; q < NSW; ++q) {
+#pragma unroll
+                    for (int c = 0; c < M; ++c) z[q][c + 1] = mine ? Zl[q][(int64_t)c * d.LDZ + t] : cz();
+                    z[q][0] = make_double2(a0, 0.0);
+                    if (mine && nbi - 1 == rho + M) z[q][0] = csub(z[q][0], sig[q]);
+                }
+            }
             for (int ti = nbi - 1; ti >= 0; --ti) {
-                double2* piv = Piv + (ti & 1) * 32;
+                const int pb = (ti & 1) * 32;
                 if (mine && rho == ti) {
 #pragma unroll
-                    for (int j = 0; j < L; ++j) piv[j] = z[j];
+                    for (int q = 0; q < NSW; ++q)
+#pragma unroll
+                        for (int j = 0; j < L; ++j) Piv[q][pb + j] = z[q][j];
                 }
                 __syncwarp();
-                double sq[L - 1];
+                double2 tau[NSW], scale[NSW];
+                double sq[NSW][L - 1];
 #pragma unroll
-                for (int j = 0; j < L - 1; ++j) {
-                    const double2 x = piv[j];
-                    sq[j] = fma(x.x, x.x, x.y * x.y);
-                }
+                for (int j = 0; j < L - 1; ++j)
+#pragma unroll
+                    for (int q = 0; q < NSW; ++q) {
+                        const double2 x = Piv[q][pb + j];
+                        sq[q][j] = fma(x.x, x.x, x.y * x.y);
+                    }
 #pragma unroll
                 for (int w = 1; w < L - 1; w <<= 1)
 #pragma unroll
-                    for (int j = 0; j + w < L - 1; j += 2 * w) sq[j] += sq[j + w];
-                const double s2 = L > 1 ? sq[0] : 0.0;
-                const double2 pv = piv[L - 1];
-                const double2 alpha = make_double2(pv.x, -pv.y);  // conj: row -> reflector space
-                double2 tau = cz(), scale = cz();
-                if (!(s2 == 0.0 && alpha.y == 0.0)) {
-                    const double nrm2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
+                    for (int j = 0; j + w < L - 1; j += 2 * w)
+#pragma unroll
+                        for (int q = 0; q < NSW; ++q) sq[q][j] += sq[q][j + w];
+#pragma unroll
+                for (int q = 0; q < NSW; ++q) {
+                    // branch-free reflector (tau = 0 for an already-collapsed row)
+                    const double s2 = L > 1 ? sq[q][0] : 0.0;
+                    const double2 pv = Piv[q][pb + L - 1];
+                    const double2 alpha = make_double2(pv.x, -pv.y);  // conj: row -> reflector space
+                    const bool ident = s2 == 0.0 && alpha.y == 0.0;
+                    const double nrm2 = ident ? 1.0 : fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
                     const double rn = rsqrt(nrm2);
                     const double sg = alpha.x >= 0.0 ? -1.0 : 1.0;
                     const double beta = sg * nrm2 * rn;
                     const double ib = sg * rn;
-                    tau = make_double2(1.0 - alpha.x * ib, -alpha.y * ib);
                     const double zx = alpha.x - beta, zy = alpha.y;
-                    const double rz = rsqrt(fma(zx, zx, zy * zy));
+                    const double zz = fma(zx, zx, zy * zy);
+                    const double rz = rsqrt(zz > 0.0 ? zz : 1.0);
                     const double iz = rz * rz;
-                    scale = make_double2(zx * iz, -zy * iz);
+                    tau[q] = ident ? cz() : make_double2(1.0 - alpha.x * ib, -alpha.y * ib);
+                    scale[q] = ident ? cz() : make_double2(zx * iz, -zy * iz);
                 }
-                if (lane < L) {
-                    const double2 x = piv[lane];
-                    U[ti * L + lane] =
-                        lane < L - 1 ? cmul(make_double2(x.x, -x.y), scale) : make_double2(1.0, 0.0);
-                }
-                if (lane == 0) Tau[ti] = tau;
-                __syncwarp();
-                if (mine && rho < ti) blk_row_update<L>(z, U + ti * L, tau);
 #pragma unroll
-                for (int j = L - 1; j > 0; --j) z[j] = z[j - 1];
+                for (int q = 0; q < NSW; ++q) {
+                    if (lane < L) {
+                        const double2 x = Piv[q][pb + lane];
+                        U[q][ti * L + lane] =
+                            lane < L - 1 ? cmul(make_double2(x.x, -x.y), scale[q]) : make_double2(1.0, 0.0);
+                    }
+                    if (lane == 0) Tau[q][ti] = tau[q];
+                }
+                __syncwarp();
+                if (mine && rho < ti) blk_row_update_n<L, NSW>(z, U, ti * L, tau);
                 if (ti > 0) {
-                    double2 v = make_double2(pf, 0.0);
-                    if (mine && rho + M == ti - 1) v = csub(v, sig);
-                    z[0] = v;
+#pragma unroll
+                    for (int q = 0; q < NSW; ++q) {
+#pragma unroll
+                        for (int j = L - 1; j > 0; --j) z[q][j] = z[q][j - 1];
+                        double2 v = make_double2(pf, 0.0);
+                        if (mine && rho + M == ti - 1) v = csub(v, sig[q]);
+                        z[q][0] = v;
+                    }
                     if (mine && ti >= 2 && rho <= ti - 2) pf = Ab[arow + (int64_t)(b + ti - 2) * d.lda];
                 }
             }
@@ -200,47 +285,66 @@ __global__ void __launch_bounds__(32, 8)
         if (lane < 2 * M) {
             const unsigned pm = 0x000fffffu >> (20 - 2 * M);
             const int c = lane >> 1, hh = lane & 1, base = hh * HW;
-            double2 w[HW];
+            double2 w[NSW][HW];
 #pragma unroll
-            for (int k = 0; k < HW; ++k) w[k] = make_double2(base + k == c ? 1.0 : 0.0, 0.0);
+            for (int q = 0; q < NSW; ++q)
+#pragma unroll
+                for (int k = 0; k < HW; ++k) w[q][k] = make_double2(base + k == c ? 1.0 : 0.0, 0.0);
             for (int s = 0; s < nbi; ++s) {
-                const double2* us = U + s * L + base;
-                double2 dp = cz();
+                double2 dp[NSW];
 #pragma unroll
-                for (int k = 0; k < HW; ++k) {
-                    if (base + k < L) {
-                        const double2 uk = us[k];  // conj(u) w
-                        dp.x = fma(uk.x, w[k].x, dp.x);
-                        dp.x = fma(uk.y, w[k].y, dp.x);
-                        dp.y = fma(uk.x, w[k].y, dp.y);
-                        dp.y = fma(-uk.y, w[k].x, dp.y);
+                for (int q = 0; q < NSW; ++q) {
+                    const double2* us = U[q] + s * L + base;
+                    dp[q] = cz();
+#pragma unroll
+                    for (int k = 0; k < HW; ++k) {
+                        if (base + k < L) {
+                            const double2 uk = us[k];  // conj(u) w
+                            dp[q].x = fma(uk.x, w[q][k].x, dp[q].x);
+                            dp[q].x = fma(uk.y, w[q][k].y, dp[q].x);
+                            dp[q].y = fma(uk.x, w[q][k].y, dp[q].y);
+                            dp[q].y = fma(-uk.y, w[q][k].x, dp[q].y);
+                        }
                     }
                 }
-                dp.x += __shfl_xor_sync(pm, dp.x, 1);
-                dp.y += __shfl_xor_sync(pm, dp.y, 1);
-                const double2 td = cmul(Tau[s], dp);
 #pragma unroll
-                for (int k = 0; k < HW; ++k) {
-                    if (base + k < L) {
-                        const double2 uk = us[k];
-                        w[k].x = fma(-uk.x, td.x, fma(uk.y, td.y, w[k].x));
-                        w[k].y = fma(-uk.x, td.y, fma(-uk.y, td.x, w[k].y));
-                    }
+                for (int q = 0; q < NSW; ++q) {
+                    dp[q].x += __shfl_xor_sync(pm, dp[q].x, 1);
+                    dp[q].y += __shfl_xor_sync(pm, dp[q].y, 1);
                 }
-                if (hh == 0) P[s * M + c] = w[0];
-                const double nx = __shfl_xor_sync(pm, w[0].x, 1);
-                const double ny = __shfl_xor_sync(pm, w[0].y, 1);
 #pragma unroll
-                for (int k = 0; k < HW - 1; ++k) w[k] = w[k + 1];
-                w[HW - 1] = hh == 0 ? make_double2(nx, ny) : cz();
+                for (int q = 0; q < NSW; ++q) {
+                    const double2* us = U[q] + s * L + base;
+                    const double2 td = cmul(Tau[q][s], dp[q]);
+#pragma unroll
+                    for (int k = 0; k < HW; ++k) {
+                        if (base + k < L) {
+                            const double2 uk = us[k];
+                            w[q][k].x = fma(-uk.x, td.x, fma(uk.y, td.y, w[q][k].x));
+                            w[q][k].y = fma(-uk.x, td.y, fma(-uk.y, td.x, w[q][k].y));
+                        }
+                    }
+                    if (hh == 0) P[q][s * M + c] = w[q][0];
+                }
+#pragma unroll
+                for (int q = 0; q < NSW; ++q) {
+                    const double nx = __shfl_xor_sync(pm, w[q][0].x, 1);
+                    const double ny = __shfl_xor_sync(pm, w[q][0].y, 1);
+#pragma unroll
+                    for (int k = 0; k < HW - 1; ++k) w[q][k] = w[q][k + 1];
+                    w[q][HW - 1] = hh == 0 ? make_double2(nx, ny) : cz();
+                }
             }
 #pragma unroll
-            for (int k = 0; k < HW; ++k)
-                if (base + k < M) P[(nbi + base + k) * M + c] = w[k];
+            for (int q = 0; q < NSW; ++q)
+#pragma unroll
+                for (int k = 0; k < HW; ++k)
+                    if (base + k < M) P[q][(nbi + base + k) * M + c] = w[q][k];
         }
         __syncwarp();
         // ---------------- apply P_i: W22, then every row pass ----------------
-        {
+#pragma unroll
+        for (int q = 0; q < NSW; ++q) {
             double2 w22n[(M * M + 31) / 32];
 #pragma unroll
             for (int e = 0; e < (M * M + 31) / 32; ++e) {
@@ -249,74 +353,98 @@ __global__ void __launch_bounds__(32, 8)
                 if (u < M * M) {
                     const int r = u / M, c = u - (u / M) * M;
 #pragma unroll
-                    for (int j = 0; j < M; ++j) w22n[e] = cfma(W22[r * M + j], P[(nbi + j) * M + c], w22n[e]);
+                    for (int j = 0; j < M; ++j)
+                        w22n[e] = cfma(W22[q][r * M + j], P[q][(nbi + j) * M + c], w22n[e]);
                 }
             }
             __syncwarp();
 #pragma unroll
             for (int e = 0; e < (M * M + 31) / 32; ++e) {
                 const int u = lane + 32 * e;
-                if (u < M * M) W22[u] = w22n[e];
+                if (u < M * M) W22[q][u] = w22n[e];
             }
         }
         for (int pass = 0; pass < 4; ++pass) {
             const int t = pass * 32 + lane - off;
             if (t < 0) continue;
-            double2 acc[M];
             if (pass == pass_rq) {
                 // finished inner-block row: W row t = P12[t - b]
 #pragma unroll
-                for (int c = 0; c < M; ++c) Wl[(int64_t)t * M + c] = P[(t - b) * M + c];
+                for (int q = 0; q < NSW; ++q)
+                    if (vq[q]) {
+#pragma unroll
+                        for (int c = 0; c < M; ++c) Wl[q][(int64_t)t * M + c] = P[q][(t - b) * M + c];
+                    }
                 continue;
             }
             const bool state = pass < pass_rq;  // t < b: state row; else W row
+            double2 acc[NSW][M];
 #pragma unroll
-            for (int c = 0; c < M; ++c) acc[c] = cz();
+            for (int q = 0; q < NSW; ++q) {
 #pragma unroll
-            for (int j = 0; j < M; ++j) {
-                const double2 zj = state ? Zl[(int64_t)j * d.LDZ + t] : Wl[(int64_t)t * M + j];
+                for (int c = 0; c < M; ++c) acc[q][c] = cz();
 #pragma unroll
-                for (int c = 0; c < M; ++c) acc[c] = cfma(zj, P[(nbi + j) * M + c], acc[c]);
+                for (int j = 0; j < M; ++j) {
+                    const double2 zj = state ? Zl[q][(int64_t)j * d.LDZ + t] : Wl[q][(int64_t)t * M + j];
+#pragma unroll
+                    for (int c = 0; c < M; ++c) acc[q][c] = cfma(zj, P[q][(nbi + j) * M + c], acc[q][c]);
+                }
             }
             if (state) {
                 const double* ap = Ab + (int64_t)(d.k - NBo) + t + (int64_t)b * d.lda;
-                double av[8];
+                double av[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) av[e] = e < nbi ? ap[(int64_t)e * d.lda] : 0.0;
-                for (int jj = 0; jj < nbi; jj += 8) {
-                    double an[8];
+                for (int e = 0; e < 4; ++e) av[e] = e < nbi ? ap[(int64_t)e * d.lda] : 0.0;
+                for (int jj = 0; jj < nbi; jj += 4) {
+                    double an[4];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        an[e] = jj + 8 + e < nbi ? ap[(int64_t)(jj + 8 + e) * d.lda] : 0.0;
+                    for (int e = 0; e < 4; ++e)
+                        an[e] = jj + 4 + e < nbi ? ap[(int64_t)(jj + 4 + e) * d.lda] : 0.0;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
+                    for (int e = 0; e < 4; ++e) {
                         if (jj + e < nbi) {
 #pragma unroll
-                            for (int c = 0; c < M; ++c) acc[c] = rfma(av[e], P[(jj + e) * M + c], acc[c]);
+                            for (int q = 0; q < NSW; ++q)
+#pragma unroll
+                                for (int c = 0; c < M; ++c)
+                                    acc[q][c] = rfma(av[e], P[q][(jj + e) * M + c], acc[q][c]);
                         }
                     }
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) av[e] = an[e];
+                    for (int e = 0; e < 4; ++e) av[e] = an[e];
                 }
                 // lazy shift: A's diagonal in column b + dd sits in row b - M + dd
                 const int dd = t - (b - M);
-                if (dd >= 0 && dd < min(M, nbi)) {
 #pragma unroll
-                    for (int c = 0; c < M; ++c) acc[c] = csub(acc[c], cmul(sig, P[dd * M + c]));
+                for (int q = 0; q < NSW; ++q) {
+                    if (dd >= 0 && dd < min(M, nbi)) {
+#pragma unroll
+                        for (int c = 0; c < M; ++c) acc[q][c] = csub(acc[q][c], cmul(sig[q], P[q][dd * M + c]));
+                    }
+                    if (vq[q]) {
+#pragma unroll
+                        for (int c = 0; c < M; ++c) Zl[q][(int64_t)c * d.LDZ + t] = acc[q][c];
+                    }
                 }
-#pragma unroll
-                for (int c = 0; c < M; ++c) Zl[(int64_t)c * d.LDZ + t] = acc[c];
             } else {
 #pragma unroll
-                for (int c = 0; c < M; ++c) Wl[(int64_t)t * M + c] = acc[c];
+                for (int q = 0; q < NSW; ++q)
+                    if (vq[q]) {
+#pragma unroll
+                        for (int c = 0; c < M; ++c) Wl[q][(int64_t)t * M + c] = acc[q][c];
+                    }
             }
         }
         __syncwarp();
     }
     // W22 rows [NBo, NBo + m)
-    for (int u = lane; u < M * M; u += 32) {
-        const int r = u / M, c = u - (u / M) * M;
-        Wl[(int64_t)(NBo + r) * M + c] = W22[r * M + c];
+#pragma unroll
+    for (int q = 0; q < NSW; ++q) {
+        if (!vq[q]) continue;
+        for (int u = lane; u < M * M; u += 32) {
+            const int r = u / M, c = u - (u / M) * M;
+            Wl[q][(int64_t)(NBo + r) * M + c] = W22[q][r * M + c];
+        }
     }
 }
 

@@ -520,10 +520,11 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
     case K: {                                                             \
         static bool configured = false;                                   \
         if (!configured) {                                                \
-            SS_CUDA_TRY(h, allow_max_smem(h, k_block<K>));                \
+            SS_CUDA_TRY(h, allow_max_smem(h, k_block<K, kBlkShiftsPerWarp>)); \
             configured = true;                                            \
         }                                                                 \
-        k_block<K><<<sb, 32, smem, st>>>(bd, Z, W);                   \
+        k_block<K, kBlkShiftsPerWarp>                                     \
+            <<<(sb + kBlkShiftsPerWarp - 1) / kBlkShiftsPerWarp, 32, smem, st>>>(bd, Z, W, sb); \
         break;                                                            \
     }
         SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)

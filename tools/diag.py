@@ -98,6 +98,8 @@ def main():
             else:
                 os.environ[k] = v
     # parity spot check vs a dense solve of a few shifts
+    if n > 4000:
+        return
     Ah, Bh, Ch = (x.cpu().numpy() for x in (A, B, C))
     Gh = G.cpu().numpy()
     for l in (0, s // 2, s - 1):
