@@ -407,3 +407,31 @@ def test_two_level_vs_one_level(n, m, p, monkeypatch):
     Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts[idx], nb=32)
     for k, l in enumerate(idx):
         assert rel(G2[:, l * m:(l + 1) * m], Go[:, k * m:(k + 1) * m]) <= 1e-10
+
+
+@pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4)])
+def test_wide_m_paths_vs_oracle(n, m, p):
+    """Block widths outside the two-level set: m + 1 > 32 takes the scheduled
+    Givens block RQ (config 5: m = 50), m = 16 / 20 the one-level update with
+    several column blocks per shift (config 4: m = 20).  Transfer function and
+    reduced solve vs the C oracle, conjugate pairs of complex shifts as in
+    config 4 / 5."""
+    sysb = ss.random_stable_system(n, m, p, seed=n + 7 * m, circular=True)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=64)
+    rng = np.random.default_rng(m)
+    a = rng.uniform(0.05, 1.0, 6) * np.sqrt(n)
+    b = rng.uniform(0.0, 1.5, 6) * np.sqrt(n)
+    shifts = np.concatenate([a + 1j * b, a - 1j * b])
+    res = ss.eval_transfer_function(chf, shifts, nb=64)
+    assert res.failures == {}
+    Go, fo = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts, nb=64)
+    assert (fo < 0).all()
+    assert per_shift_rel(res.G, Go, m, len(shifts)) <= 1e-10
+    # conjugate pairs give conjugate transfer functions (real system)
+    assert per_shift_rel(res.G[:, 6 * m:], np.conj(res.G[:, :6 * m]), m, 6) <= 1e-10
+    bd = (rng.standard_normal((m, 4)) + 1j * rng.standard_normal((m, 4)))
+    bd /= np.linalg.norm(bd, axis=0)
+    red = ss.solve_shifted_reduced(chf, shifts[:4], bd, nb=64)
+    for k in range(4):
+        cert = ss.residual_certificate(chf, shifts[k], red.x[:, k], chf.Bhat @ bd[:, k])
+        assert cert <= 1e3 * n * EPS
