@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--cfg", type=int, default=2)
     ap.add_argument("--nb", type=int, default=64)
     ap.add_argument("--shifts", type=int, default=0)
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--variants", default="")
     ap.add_argument("--profile", action="store_true", help="one call, no timing (for ncu)")
     args = ap.parse_args()
@@ -70,13 +70,16 @@ def main():
         call()
         call()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
+        per = []
         for _ in range(args.reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
             call()
-        e1.record(st)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.reps
+            e1.record(st)
+            torch.cuda.synchronize()
+            per.append(e0.elapsed_time(e1))
+        per.sort()
+        ms = per[len(per) // 2]
         L.ss_reset_stats(h.ptr)
         L.ss_set_timing(h.ptr, 1)
         call()
@@ -89,7 +92,7 @@ def main():
         L.ss_update_kernel_stats(h.ptr, ctypes.byref(ul), ctypes.byref(us), ctypes.byref(ua))
         ach = ua.value / us.value / 1e12 if us.value else 0
         print(f"cfg{args.cfg} n={n} m={m} s={s} nb={args.nb} [{var or 'default'}] "
-              f"{ms:.3f} ms/call  {s / ms * 1e3:.0f} shifts/s  sweep {f_alg * s / ms / 1e9:.2f} TF | "
+              f"{ms:.3f} ms/call (median; min {per[0]:.3f} max {per[-1]:.3f})  {s / ms * 1e3:.0f} shifts/s  sweep {f_alg * s / ms / 1e9:.2f} TF | "
               f"timed: rq {sec5[1]*1e3:.2f} ms, update {(sec5[2]+sec5[3])*1e3:.2f} ms "
               f"({ach:.2f} TF alg), head {sec5[4]*1e3:.3f} ms", flush=True)
         for k, v in saved.items():
