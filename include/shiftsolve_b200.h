@@ -78,6 +78,18 @@ int ss_solve_reduced(ss_handle* h, int n, int m, const double* Ahat, int64_t lda
                      const double* bdirs, int64_t ldbd, int nb, int64_t batch, double rtol,
                      double* X, int64_t ldx, int32_t* fail_row, void* stream);
 
+/* Transposed shifted solves (Ahat - sigma_l I)^T x_l = c_l, general
+ * right-hand sides.  Replaces solvers.py:320-486 solve_shifted_transposed
+ * (top-down LQ sweep with fused forward substitution, batched.py:125-182).
+ * rhs: n x s complex128 (ldr); X: n x s complex128 (ldx), NaN column on
+ * failure; fail_row[l]: -1 or the 0-based row of the first pivot that fell
+ * below rtol*||Ahat - sigma_l I||_F.  Requires m + 1 <= 32; nb is clamped
+ * to 32 (one warp per window). */
+int ss_solve_transposed(ss_handle* h, int n, int m, const double* Ahat, int64_t lda,
+                        const double* shifts, int64_t s, const double* rhs, int64_t ldr,
+                        int nb, int64_t batch, double rtol, double* X, int64_t ldx,
+                        int32_t* fail_row, void* stream);
+
 /* In-place orthogonal reduction of (A, B, C) to controller-Hessenberg form.
  * Replaces hessenberg.py:260-328 reduce_controller_hessenberg.
  * A n x n -> Ahat (exact zeros below the m-th subdiagonal), B n x m -> Bhat

@@ -15,7 +15,7 @@ from .errors import (
     SingularShiftError,
 )
 from .hessenberg import ControllerHessForm, reduce_controller_hessenberg
-from .schedule import AnnihilationSchedule, greedy_schedule
+from .schedule import AnnihilationSchedule, greedy_schedule, mirrored_schedule
 from .solvers import (
     ShiftedSolveResult,
     TransferFunctionResult,
@@ -23,6 +23,7 @@ from .solvers import (
     eval_transfer_function,
     residual_certificate,
     solve_shifted_reduced,
+    solve_shifted_transposed,
     structured_pseudospectrum_grid,
     two_norm_small,
 )
@@ -48,6 +49,8 @@ __all__ = [
     "reduce_controller_hessenberg",
     "residual_certificate",
     "solve_shifted_reduced",
+    "solve_shifted_transposed",
+    "mirrored_schedule",
     "structured_pseudospectrum_grid",
     "two_norm_small",
 ]

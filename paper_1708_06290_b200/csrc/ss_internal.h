@@ -85,6 +85,8 @@ cudaEvent_t timing_begin(ss_handle* h, cudaStream_t st);
 void timing_end(ss_handle* h, cudaStream_t st, cudaEvent_t a, int phase, double fl_batched = 0.0,
                 double fl_outer = 0.0, double fl_alg = 0.0);
 void timing_resolve(ss_handle* h);
+// ||A||_F^2, trace(A) -> h->d_scal[0:2] (ss_sweep.cu)
+int fro2_trace(ss_handle* h, int n, const double* A, int64_t lda, cudaStream_t st);
 
 }  // namespace ss
 

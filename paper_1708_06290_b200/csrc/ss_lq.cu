@@ -1,0 +1,539 @@
+// Transposed shifted solves (A - sigma_l I)^T x_l = c_l, general right-hand
+// sides, sm_100a.
+//
+// Reference path (solvers.py:320-486 solve_shifted_transposed / _sweep_lq,
+// batched.py:125-182 batched_lq): the stacked matrix [A^T - sigma I; -I] is
+// brought to lower-triangular form top-down by a sliding window; the stacked
+// vector w = [rhs; 0] is forward-substituted in the same sweep, so its lower
+// half accumulates the solution.  Per shift the state is S = [z2 | w]:
+// (2n) x (m+1) complex (z2 = the m active transformed columns).
+//
+// B200 mapping (one launch of each per window step of nb <= 32 rows):
+//   k_tseed   S = [A^T(:, 0:m) - sigma E; -E | rhs; 0]
+//   k_lq      one warp per shift: lane = block row.  The nb x (nb+m) lower
+//             trapezoid [z2 rows | panel of A^T] is reduced top-down by row
+//             Householder reflectors (row i's window = columns i..i+m, pivot
+//             first; same sign rule as kernels.py:74-99), the window's w
+//             segment is forward-substituted in the same pass (every pivot
+//             checked against tol_l, batched.py:168-178), then the m new
+//             active columns P[:, nb:nb+m] and dW = P[:, :nb] y are formed by
+//             reverse accumulation (lanes = the m+1 vectors).  Householder
+//             and the reference's mirrored Givens schedule give the same
+//             |L_ii| (the LQ factor is unique up to phases), so the
+//             singularity decisions agree.
+//   k_tupd    rows below the window: S <- S T + Pan(A^T, -I) U12 (the
+//             reference's update_shift + trail_shift, solvers.py:431-468),
+//             with w treated as an extra state column; lazy-shift rows get
+//             -sigma P12.
+//   k_ttail   one CTA per shift: the unblocked m-column tail with the
+//             reference's Givens rotations fused with the last substitutions
+//             (solvers.py:470-486); x = w[n:].
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "ss_device.cuh"
+#include "ss_internal.h"
+#include "ss_rq_house.cuh"
+
+using namespace ssd;
+
+namespace {
+
+constexpr int kLqMaxNb = 32;
+
+struct TDims {
+    int n, m, mp;  // mp = m + 1 state columns per shift
+    const double* A;
+    int64_t lda;
+    const double2* shifts;  // batch-local
+    int sb;
+    int64_t LDS;     // leading dimension of one state column (>= 2n)
+    int32_t* fail;   // batch-local fail rows (-1 = ok)
+    const double* tol;  // batch-local pivot tolerances
+};
+
+// ---------------------------------------------------------------------------
+// seed (solvers.py:375-381)
+// ---------------------------------------------------------------------------
+__global__ void k_tseed(TDims d, const double2* __restrict__ rhs, int64_t ldr,
+                        double2* __restrict__ S) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    if (i >= d.LDS) return;
+    const double2 sig = d.shifts[l];
+    double2* Sl = S + (int64_t)l * d.mp * d.LDS;
+    for (int c = 0; c < d.m; ++c) {
+        double2 v = cz();
+        if (i < d.n) {
+            v.x = d.A[c + (int64_t)i * d.lda];  // A^T(i, c)
+            if (i == c) v = csub(v, sig);
+        } else if (i < 2 * d.n && i - d.n == c) {
+            v.x = -1.0;
+        }
+        Sl[(int64_t)c * d.LDS + i] = v;
+    }
+    Sl[(int64_t)d.m * d.LDS + i] = i < d.n ? rhs[i + (int64_t)l * ldr] : cz();
+    if (i == 0) d.fail[l] = -1;
+}
+
+// ---------------------------------------------------------------------------
+// per-window block LQ with fused forward substitution (batched.py:125-182)
+// ---------------------------------------------------------------------------
+struct LqStep {
+    int k0;   // 0-based first row of the window (k1 - 1)
+    int nb;   // window rows (<= 32)
+    int c0;   // 0-based first panel column of A^T (k0 + m)
+};
+
+// Output per shift: Pout ((nb + mp) x mp, j-major) for k_tupd:
+//   rows j < nb          panel part  [P[m+j, nb:nb+m] | -dW[m+j]]
+//   rows nb + r, r < m   state part  [P[r, nb:nb+m]   | -dW[r]]
+//   row  nb + m          w row       [0 ... 0         | 1]
+template <int LMAX>
+__global__ void __launch_bounds__(32) k_lq(TDims d, LqStep st, const double2* __restrict__ S,
+                                           double2* __restrict__ Pout) {
+    __shared__ double2 Piv[LMAX];
+    __shared__ double2 U[kLqMaxNb][LMAX];
+    __shared__ double2 Tau[kLqMaxNb];
+    __shared__ double2 Y[kLqMaxNb];
+    const int l = blockIdx.x;
+    const int lane = threadIdx.x;
+    const int m = d.m, L = m + 1, nb = st.nb, mp = d.mp;
+    const double2 sig = d.shifts[l];
+    const double2* Sl = S + (int64_t)l * mp * d.LDS;
+    double2* Po = Pout + (int64_t)l * (nb + mp) * mp;
+    if (d.fail[l] >= 0) return;  // failed in an earlier window: left as is (NaN at the end)
+    const bool mine = lane < nb;
+    const int row = st.k0 + lane;  // A^T row / stacked row of this lane
+    // window of row `lane` at step 0: columns 0..m = [z2 row | panel col 0]
+    double2 r[LMAX];
+#pragma unroll
+    for (int j = 0; j < LMAX; ++j) r[j] = cz();
+    double2 y = cz();
+    if (mine) {
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j)
+            if (j < m) r[j] = Sl[(int64_t)j * d.LDS + row];
+        double2 v = make_double2(d.A[st.c0 + (int64_t)row * d.lda], 0.0);  // A^T(row, c0)
+        if (lane == m) v = csub(v, sig);  // block diagonal (lazy shift), solvers.py:398-400
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j)
+            if (j == m) r[j] = v;
+        y = Sl[(int64_t)m * d.LDS + row];
+    }
+    const double tol = d.tol[l];
+    int fail = -1;
+    for (int t = 0; t < nb; ++t) {
+        if (lane == t) {
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j < L) Piv[j] = r[j];
+        }
+        __syncwarp();
+        // reflector of row t (pivot first): zlarfg on y = conj(row)
+        double s2 = 0.0;
+        for (int j = 1; j < L; ++j) s2 = fma(Piv[j].x, Piv[j].x, fma(Piv[j].y, Piv[j].y, s2));
+        const double2 alpha = make_double2(Piv[0].x, -Piv[0].y);
+        double2 tau = cz(), scale = cz();
+        if (!(s2 == 0.0 && alpha.y == 0.0)) {
+            const double nrm2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
+            const double rn = rsqrt(nrm2);
+            const double sg = alpha.x >= 0.0 ? -1.0 : 1.0;
+            const double beta = sg * nrm2 * rn;
+            const double ib = sg * rn;
+            tau = make_double2(1.0 - alpha.x * ib, -alpha.y * ib);
+            const double zx = alpha.x - beta, zy = alpha.y;
+            const double rz = rsqrt(fma(zx, zx, zy * zy));
+            const double iz = rz * rz;
+            scale = make_double2(zx * iz, -zy * iz);
+        }
+        double2 uu[LMAX];
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) {
+            if (j == 0) {
+                uu[j] = make_double2(1.0, 0.0);
+            } else if (j < L) {
+                const double2 x = Piv[j];
+                uu[j] = cmul(make_double2(x.x, -x.y), scale);
+            } else {
+                uu[j] = cz();
+            }
+        }
+        if (lane < L) {
+            double2 mineu = cz();
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j) mineu = (j == lane) ? uu[j] : mineu;
+            U[t][lane] = mineu;
+        }
+        if (lane == 0) Tau[t] = tau;
+        if (mine && lane >= t) rq_row_update<LMAX>(r, uu, tau, L);
+        // forward substitution on the window's w segment (batched.py:170-178):
+        // lane t holds L(t,t), lanes below hold L(lane, t) in r[0]
+        const double2 piv = make_double2(__shfl_sync(0xffffffffu, r[0].x, t),
+                                         __shfl_sync(0xffffffffu, r[0].y, t));
+        if (fail < 0 && hypot(piv.x, piv.y) <= tol) fail = st.k0 + t;
+        double2 yt = make_double2(__shfl_sync(0xffffffffu, y.x, t), __shfl_sync(0xffffffffu, y.y, t));
+        yt = cdiv(yt, piv);
+        if (lane == t) y = yt;
+        if (mine && lane > t) y = csub(y, cmul(r[0], yt));
+        // slide: column t retires, column t + m + 1 (panel column t + 1) enters
+#pragma unroll
+        for (int j = 0; j < LMAX - 1; ++j) r[j] = r[j + 1];
+        r[LMAX - 1] = cz();
+        if (t + 1 < nb) {
+            double2 v = cz();
+            if (mine && lane > t) {
+                v.x = d.A[st.c0 + t + 1 + (int64_t)row * d.lda];  // A^T(row, c0 + t + 1)
+                if (lane == m + t + 1) v = csub(v, sig);
+            }
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j == m) r[j] = v;
+        }
+        __syncwarp();
+    }
+    if (fail >= 0) {
+        if (lane == 0) d.fail[l] = fail;
+        return;
+    }
+    if (mine) Y[lane] = y;
+    __syncwarp();
+    // reverse accumulation: vector q < m is e_{nb+q}, vector m is [y; 0];
+    // P = H_0 H_1 ... H_{nb-1}: apply H_{nb-1} first; window = entries t..t+m
+    if (lane <= m) {
+        const int q = lane;
+        double2 w[LMAX];
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) {
+            w[j] = cz();
+            if (q < m && j == q + 1) w[j] = make_double2(1.0, 0.0);
+        }
+        if (q == m) w[0] = Y[nb - 1];
+        for (int t = nb - 1; t >= 0; --t) {
+            const double2 ts = Tau[t];
+            double2 dp = cz();
+            for (int j = 0; j < L; ++j) {
+                const double2 uj = U[t][j];
+                dp = cfma(make_double2(uj.x, -uj.y), w[j], dp);
+            }
+            const double2 td = cmul(ts, dp);
+#pragma unroll
+            for (int j = 0; j < LMAX; ++j)
+                if (j < L) w[j] = csub(w[j], cmul(U[t][j], td));
+            // entry t + m is final: block column index e = t + m
+            {
+                const int e = t + m;
+                double2 v = cz();
+#pragma unroll
+                for (int j = 0; j < LMAX; ++j)
+                    if (j == m) v = w[j];
+                if (q == m) v = make_double2(-v.x, -v.y);
+                const int prow = e < m ? nb + e : e - m;  // Pout row of block column e
+                Po[(int64_t)prow * mp + q] = v;
+            }
+#pragma unroll
+            for (int j = LMAX - 1; j > 0; --j) w[j] = w[j - 1];
+            w[0] = (q == m && t > 0) ? Y[t - 1] : cz();
+        }
+        // remaining entries 0..m-1 (block columns 0..m-1 = state rows)
+#pragma unroll
+        for (int j = 0; j < LMAX; ++j) {
+            if (j >= 1 && j <= m) {
+                const int e = j - 1;
+                double2 v = w[j];
+                if (q == m) v = make_double2(-v.x, -v.y);
+                const int prow = e < m ? nb + e : e - m;
+                Po[(int64_t)prow * mp + q] = v;
+            }
+        }
+        // w row: identity on the w column
+        Po[(int64_t)(nb + m) * mp + q] = make_double2(q == m ? 1.0 : 0.0, 0.0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// rows below the window (solvers.py:431-468): S <- S T + Pan U12, with
+//   Pan(i, j) = A^T(i, c0 + j) for i < n, -[i - n == c0 + j] for i >= n,
+// lazy-shift rows k0 + nb + (m - mnb) + dd: S -= sigma P12[nb - mnb + dd].
+// One thread per row, all mp columns; panel tile staged in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kTuRows = 128;
+
+__global__ void __launch_bounds__(kTuRows) k_tupd(TDims d, LqStep st, double2* __restrict__ S,
+                                                  const double2* __restrict__ Pbuf, int sg_size) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int m = d.m, mp = d.mp, nb = st.nb;
+    double* Pan = reinterpret_cast<double*>(smem);                                // [nb][kTuRows]
+    double2* Ps = reinterpret_cast<double2*>(smem + (size_t)nb * kTuRows * 8);   // (nb+mp) x mp
+    double2* Rb = Ps + (nb + mp) * mp;                                            // [mp][kTuRows] row copy
+    const int rlo = st.k0 + nb;
+    const int i = rlo + blockIdx.x * kTuRows + threadIdx.x;
+    const int ihi = 2 * d.n;
+    const int mnb = min(m, nb);
+    const int crow0 = st.k0 + nb + (m - mnb);
+    for (int v = threadIdx.x; v < nb * kTuRows; v += blockDim.x) {
+        const int j = v / kTuRows, rr = v - j * kTuRows;
+        const int ii = rlo + blockIdx.x * kTuRows + rr;
+        double a = 0.0;
+        if (ii < d.n) a = d.A[st.c0 + j + (int64_t)ii * d.lda];
+        else if (ii < ihi && ii - d.n == st.c0 + j) a = -1.0;
+        Pan[j * kTuRows + rr] = a;
+    }
+    const int l0 = blockIdx.y * sg_size, l1 = min(l0 + sg_size, d.sb);
+    for (int l = l0; l < l1; ++l) {
+        __syncthreads();
+        if (d.fail[l] >= 0) continue;
+        const double2* pl = Pbuf + (int64_t)l * (nb + mp) * mp;
+        for (int v = threadIdx.x; v < (nb + mp) * mp; v += blockDim.x) Ps[v] = pl[v];
+        __syncthreads();
+        if (i >= ihi) continue;
+        double2* Sl = S + (int64_t)l * mp * d.LDS;
+        const double2 sig = d.shifts[l];
+        for (int j = 0; j < mp; ++j) Rb[j * kTuRows + threadIdx.x] = Sl[(int64_t)j * d.LDS + i];
+        const int dd = i - crow0;
+        for (int c0 = 0; c0 < mp; c0 += 8) {
+            double2 acc[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = cz();
+            for (int j = 0; j < mp; ++j) {
+                const double2 sj = Rb[j * kTuRows + threadIdx.x];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c0 + c < mp) acc[c] = cfma(sj, Ps[(nb + j) * mp + c0 + c], acc[c]);
+            }
+            for (int j = 0; j < nb; ++j) {
+                const double a = Pan[j * kTuRows + threadIdx.x];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c0 + c < mp) acc[c] = rfma(a, Ps[j * mp + c0 + c], acc[c]);
+            }
+            if (dd >= 0 && dd < mnb) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c0 + c < mp) acc[c] = csub(acc[c], cmul(sig, Ps[(nb - mnb + dd) * mp + c0 + c]));
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c0 + c < mp) Sl[(int64_t)(c0 + c) * d.LDS + i] = acc[c];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// unblocked tail (solvers.py:470-486): one CTA per shift
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ttail(TDims d, double2* __restrict__ S, double2* __restrict__ X,
+                                               int64_t ldx) {
+    __shared__ double s_c;
+    __shared__ double2 s_s, s_r, s_w;
+    __shared__ int s_fail;
+    const int l = blockIdx.x, tid = threadIdx.x;
+    const int n = d.n, m = d.m, mp = d.mp;
+    double2* Sl = S + (int64_t)l * mp * d.LDS;
+    double2* wv = Sl + (int64_t)m * d.LDS;
+    const int lo = n - m, hi = 2 * n;
+    if (tid == 0) s_fail = d.fail[l];
+    __syncthreads();
+    const double tol = d.tol[l];
+    if (s_fail < 0) {
+        for (int kk = 1; kk < m && s_fail < 0; ++kk) {
+            const int rr = n - m + kk - 1;
+            double2* hcol = Sl + (int64_t)(kk - 1) * d.LDS;
+            for (int c = kk; c < m; ++c) {
+                double2* tcol = Sl + (int64_t)c * d.LDS;
+                if (tid == 0) {
+                    double cc;
+                    double2 ss, rv;
+                    givens(hcol[rr], tcol[rr], cc, ss, rv);
+                    s_c = cc;
+                    s_s = ss;
+                    s_r = rv;
+                }
+                __syncthreads();
+                const double cc = s_c;
+                const double2 ss = s_s;
+                for (int i = lo + tid; i < hi; i += blockDim.x) {
+                    double2 h = hcol[i], t = tcol[i];
+                    rot_apply(cc, ss, h, t);
+                    hcol[i] = h;
+                    tcol[i] = t;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    tcol[rr] = cz();
+                    hcol[rr] = s_r;
+                }
+                __syncthreads();
+            }
+            if (tid == 0) {
+                const double2 piv = hcol[rr];
+                if (hypot(piv.x, piv.y) <= tol) {
+                    s_fail = rr;
+                } else {
+                    s_w = cdiv(wv[rr], piv);
+                    wv[rr] = s_w;
+                }
+            }
+            __syncthreads();
+            if (s_fail >= 0) break;
+            const double2 wr = s_w;
+            for (int i = rr + 1 + tid; i < hi; i += blockDim.x) wv[i] = csub(wv[i], cmul(hcol[i], wr));
+            __syncthreads();
+        }
+        if (s_fail < 0) {
+            double2* hcol = Sl + (int64_t)(m - 1) * d.LDS;
+            if (tid == 0) {
+                const double2 piv = hcol[n - 1];
+                if (hypot(piv.x, piv.y) <= tol) {
+                    s_fail = n - 1;
+                } else {
+                    s_w = cdiv(wv[n - 1], piv);
+                    wv[n - 1] = s_w;
+                }
+            }
+            __syncthreads();
+            if (s_fail < 0) {
+                const double2 wr = s_w;
+                for (int i = n + tid; i < hi; i += blockDim.x) wv[i] = csub(wv[i], cmul(hcol[i], wr));
+            }
+        }
+    }
+    __syncthreads();
+    const bool ok = s_fail < 0;
+    const double qn = __longlong_as_double(0x7ff8000000000000ULL);
+    for (int i = tid; i < n; i += blockDim.x)
+        X[i + (int64_t)l * ldx] = ok ? wv[n + i] : make_double2(qn, qn);
+    if (tid == 0) d.fail[l] = s_fail;
+}
+
+__global__ void k_tol(int sb, const double2* __restrict__ shifts, const double* __restrict__ scal,
+                      int n, double rtol, double* __restrict__ tol) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= sb) return;
+    const double2 sg = shifts[l];
+    const double sc2 = scal[0] - 2.0 * (sg.x * scal[1]) + (sg.x * sg.x + sg.y * sg.y) * n;
+    tol[l] = rtol * sqrt(sc2 > 0.0 ? sc2 : 0.0);
+}
+
+template <typename F>
+cudaError_t allow_smem(ss_handle* h, F* fn) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(h->smem_optin - fa.sharedSizeBytes));
+}
+
+int launch_lq(ss_handle* h, int m, int sb, cudaStream_t st, const TDims& d, const LqStep& s,
+              const double2* S, double2* P) {
+    const int L = m + 1;
+    if (L <= 2) k_lq<2><<<sb, 32, 0, st>>>(d, s, S, P);
+    else if (L <= 4) k_lq<4><<<sb, 32, 0, st>>>(d, s, S, P);
+    else if (L <= 8) k_lq<8><<<sb, 32, 0, st>>>(d, s, S, P);
+    else if (L <= 12) k_lq<12><<<sb, 32, 0, st>>>(d, s, S, P);
+    else if (L <= 16) k_lq<16><<<sb, 32, 0, st>>>(d, s, S, P);
+    else if (L <= 24) k_lq<24><<<sb, 32, 0, st>>>(d, s, S, P);
+    else if (L <= 32) k_lq<32><<<sb, 32, 0, st>>>(d, s, S, P);
+    else return ss::set_err(h, SS_EARG, "transposed solve: m + 1 must be <= 32");
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+}  // namespace
+
+extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Ahat, int64_t lda,
+                                   const double* shifts, int64_t s, const double* rhs, int64_t ldr,
+                                   int nb, int64_t batch, double rtol, double* X, int64_t ldx,
+                                   int32_t* fail_row, void* stream) {
+    if (!h) return SS_EARG;
+    if (n < 1 || m < 1 || m > n || s < 0)
+        return ss::set_err(h, SS_EDIM, "inconsistent controller-Hessenberg form");
+    if (lda < n || ldr < n || ldx < n) return ss::set_err(h, SS_EDIM, "leading dimension too small");
+    if (nb < 1) return ss::set_err(h, SS_EARG, "window block size must be >= 1");
+    if (m + 1 > 32) return ss::set_err(h, SS_EARG, "transposed solve: m + 1 must be <= 32");
+    if (s == 0) return SS_OK;
+    if (!Ahat || !shifts || !rhs || !X || !fail_row) return ss::set_err(h, SS_EARG, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    SS_CUDA_TRY(h, cudaSetDevice(h->device));
+    const double rt = rtol > 0.0 ? rtol : 1e3 * n * 2.220446049250313e-16;
+    const int nb0 = std::max(1, std::min(std::min(nb, kLqMaxNb), std::max(n - m, 1)));
+    const int mp = m + 1;
+    const int64_t LDS = ((int64_t)2 * n + 7) & ~(int64_t)7;
+    // ||A||_F^2 and trace(A) for the per-shift pivot tolerances
+    {
+        int rc = ss::fro2_trace(h, n, Ahat, lda, st);
+        if (rc) return rc;
+    }
+    const size_t per_shift = (size_t)LDS * mp * 16 + (size_t)(nb0 + mp) * mp * 16 + 8 + 64;
+    int64_t sb_max = batch > 0 ? batch : s;
+    {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const size_t cap = std::max<size_t>(fr / 2 + h->ws_bytes / 2, per_shift);
+        sb_max = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(sb_max, s),
+                                                        (int64_t)(cap / per_shift)));
+    }
+    {
+        int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256, 0);
+        if (rc) return rc;
+    }
+    double2* Sb = (double2*)h->ws;
+    double2* Pb = Sb + (size_t)sb_max * mp * LDS;
+    double* tolb = (double*)(Pb + (size_t)sb_max * (nb0 + mp) * mp);
+    static bool attrs = false;
+    if (!attrs) {
+        SS_CUDA_TRY(h, allow_smem(h, k_tupd));
+        attrs = true;
+    }
+    for (int64_t lo = 0; lo < s; lo += sb_max) {
+        const int sb = (int)std::min<int64_t>(sb_max, s - lo);
+        TDims d;
+        d.n = n;
+        d.m = m;
+        d.mp = mp;
+        d.A = Ahat;
+        d.lda = lda;
+        d.shifts = (const double2*)shifts + lo;
+        d.sb = sb;
+        d.LDS = LDS;
+        d.fail = fail_row + lo;
+        d.tol = tolb;
+        k_tol<<<(sb + 127) / 128, 128, 0, st>>>(sb, d.shifts, h->d_scal, n, rt, tolb);
+        SS_LAUNCH_CHECK(h);
+        {
+            dim3 g((unsigned)((LDS + 255) / 256), (unsigned)sb);
+            k_tseed<<<g, 256, 0, st>>>(d, (const double2*)rhs + lo * ldr, ldr, Sb);
+            SS_LAUNCH_CHECK(h);
+        }
+        for (int k0 = 0; k0 < n - m;) {
+            LqStep ls;
+            ls.k0 = k0;
+            ls.nb = std::min(nb0, n - m - k0);
+            ls.c0 = k0 + m;
+            cudaEvent_t ev = ss::timing_begin(h, st);
+            int rc = launch_lq(h, m, sb, st, d, ls, Sb, Pb);
+            if (rc) return rc;
+            ss::timing_end(h, st, ev, ss::PH_RQ);
+            const int rows = 2 * n - (k0 + ls.nb);
+            const int sg = 8;
+            dim3 g((unsigned)((rows + kTuRows - 1) / kTuRows), (unsigned)((sb + sg - 1) / sg));
+            const size_t sm = (size_t)ls.nb * kTuRows * 8 + (size_t)(ls.nb + mp) * mp * 16 +
+                              (size_t)mp * kTuRows * 16;
+            ev = ss::timing_begin(h, st);
+            k_tupd<<<g, kTuRows, sm, st>>>(d, ls, Sb, Pb, sg);
+            SS_LAUNCH_CHECK(h);
+            const double fl_b = (double)sb * 8.0 * rows * mp * mp;
+            const double fl_o = (double)sb * 8.0 * rows * mp * ls.nb;
+            h->flops[ss::PH_BATCHED_GEMM] += fl_b;
+            h->flops[ss::PH_OUTER_GEMM] += fl_o;
+            ss::timing_end(h, st, ev, ss::PH_UPDATE, fl_b, fl_o, 0.0);
+            k0 += ls.nb;
+        }
+        cudaEvent_t ev = ss::timing_begin(h, st);
+        k_ttail<<<sb, 256, 0, st>>>(d, Sb, (double2*)X + lo * ldx, ldx);
+        SS_LAUNCH_CHECK(h);
+        ss::timing_end(h, st, ev, ss::PH_TAIL);
+    }
+    return SS_OK;
+}

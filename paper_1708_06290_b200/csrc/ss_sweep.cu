@@ -813,6 +813,27 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     return SS_OK;
 }
 
+}  // namespace
+
+namespace ss {
+// ||A||_F^2 and trace(A) into h->d_scal[0:2] (the per-shift singularity
+// thresholds, solvers.py:104-110), deterministic two-pass reduction.
+int fro2_trace(ss_handle* h, int n, const double* A, int64_t lda, cudaStream_t st) {
+    const int parts = std::min(4 * h->num_sms, std::max(n, 1));
+    int rc = ss::ensure_ws(h, 1 << 20, 1);
+    if (rc) return rc;
+    double* part = (double*)h->ws2;
+    if (parts * 2 * sizeof(double) > h->ws2_bytes) return ss::set_err(h, SS_EARG, "scratch");
+    k_fro2_trace_part<<<parts, 256, 0, st>>>(n, A, lda, part);
+    SS_LAUNCH_CHECK(h);
+    k_fro2_trace_final<<<1, 32, 0, st>>>(parts, part, h->d_scal);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+}  // namespace ss
+
+namespace {
+
 int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : n;
@@ -850,15 +871,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     // fro2 / trace for the per-shift singularity thresholds
     {
-        const int parts = std::min(4 * h->num_sms, std::max(n, 1));
-        int rc = ss::ensure_ws(h, 1 << 20, 1);  // scratch for partial sums
+        int rc = ss::fro2_trace(h, n, a.A, a.lda, st);
         if (rc) return rc;
-        double* part = (double*)h->ws2;
-        if (parts * 2 * sizeof(double) > h->ws2_bytes) return ss::set_err(h, SS_EARG, "scratch");
-        k_fro2_trace_part<<<parts, 256, 0, st>>>(n, a.A, a.lda, part);
-        SS_LAUNCH_CHECK(h);
-        k_fro2_trace_final<<<1, 32, 0, st>>>(parts, part, h->d_scal);
-        SS_LAUNCH_CHECK(h);
     }
 
     // two-level sweep (ss_block.cuh) when the fused block kernel and the

@@ -59,3 +59,18 @@ def greedy_schedule(n_rows: int, n_cols: int) -> AnnihilationSchedule:
     job.setflags(write=False)
     info.setflags(write=False)
     return AnnihilationSchedule(n_rows, n_cols, steps.value, rots.value, job, info)
+
+
+@lru_cache(maxsize=None)
+def mirrored_schedule(n_rows: int, n_cols: int) -> AnnihilationSchedule:
+    """Top-down plan for lower trapezoids (reference schedule.py:162-184): the
+    greedy plan flipped in both axes, (r, c1, c2) -> (nr+1-r, nc+1-c1,
+    nc+1-c2), same step structure."""
+    base = greedy_schedule(n_rows, n_cols)
+    info = np.asarray(base.rot_info).reshape(-1, 3).copy()
+    info[:, 0] = n_rows + 1 - info[:, 0]
+    info[:, 1:] = n_cols + 1 - info[:, 1:]
+    info = info.reshape(-1)
+    info.setflags(write=False)
+    return AnnihilationSchedule(base.n_rows, base.n_cols, base.num_steps, base.num_rots,
+                                base.job_size, info)

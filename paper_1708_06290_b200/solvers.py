@@ -2,8 +2,8 @@
 
 Same names, signatures, result types, error behaviour and phase counters as
 the reference's solvers.py (``eval_transfer_function`` :234-271,
-``solve_shifted_reduced`` :274-313, ``structured_pseudospectrum_grid``
-:508-530); the window sweep, the batched Givens RQ and the head solve run
+``solve_shifted_reduced`` :274-313, ``solve_shifted_transposed`` :320-486,
+``structured_pseudospectrum_grid`` :508-530); the window sweep, the batched Givens RQ and the head solve run
 inside libshiftsolve_b200.so (csrc/ss_sweep.cu) on the GPU.
 
 Behaviour kept from the reference:
@@ -164,6 +164,49 @@ def solve_shifted_reduced(chf: ControllerHessForm, shifts, b_dirs, nb: int = 32,
             rc = L.ss_solve_reduced(h.ptr, n, m, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(sh),
                                     s, D.ptr(bd), D.ld(bd), int(nb), _batch(batch_size), rtol,
                                     D.ptr(X), n, D.ptr(fail), D.stream_ptr(dev))
+        D.check(h, rc)
+        failures = _failures(fail)
+    Xout = X.cpu().numpy() if host else X
+    if failures and on_singular == "raise":
+        raise SingularShiftError(sorted((l, i) for l, i in failures.items()))
+    return ShiftedSolveResult(x=Xout, shifts=shifts, failures=failures)
+
+
+def solve_shifted_transposed(chf: ControllerHessForm, shifts, rhs, nb: int = 32,
+                             batch_size: int | None = None, *, pool=None,
+                             counter: PhaseCounters | None = None,
+                             on_singular: str = "raise",
+                             singular_rtol: float | None = None) -> ShiftedSolveResult:
+    """Solve (A - sigma_l I)^T x_l = c_l for general right-hand sides
+    (solvers.py:320-355): top-down windowed LQ of [A^T - sigma I; -I] with the
+    forward substitution fused into the sweep (csrc/ss_lq.cu).  Every pivot
+    of the LQ factor is checked against ``rtol * ||Ahat - sigma I||_F``; a
+    failing shift gets a NaN column and its first failing row in
+    ``failures``.  Requires m + 1 <= 32; ``nb`` is clamped to 32."""
+    del pool
+    _check_chf(chf)
+    shifts = _shifts_in(shifts)
+    n, m = chf.n, chf.m
+    s = len(shifts)
+    if tuple(rhs.shape) != (n, s):
+        raise DimensionMismatchError("rhs must be n x s")
+    if nb < 1:
+        raise ValueError("window block size must be >= 1")
+    rtol = default_singular_rtol(n) if singular_rtol is None else float(singular_rtol)
+    host = all(D.is_host(a) for a in (chf.Ahat, shifts, rhs))
+    dev = D.device_of(chf.Ahat, shifts, rhs)
+    with torch.cuda.device(dev):
+        A = D.fmat(chf.Ahat, torch.float64, dev)
+        c = D.fmat(rhs, torch.complex128, dev)
+        sh = D.fvec(shifts, torch.complex128, dev)
+        X = torch.empty((s, n), dtype=torch.complex128, device=dev).t()
+        fail = torch.empty(s, dtype=torch.int32, device=dev)
+        h = _lib.handle(dev.index)
+        L = _lib.load()
+        with D.timed_call(h, counter):
+            rc = L.ss_solve_transposed(h.ptr, n, m, D.ptr(A), D.ld(A), D.ptr(sh), s, D.ptr(c),
+                                       D.ld(c), int(nb), _batch(batch_size), rtol, D.ptr(X), n,
+                                       D.ptr(fail), D.stream_ptr(dev))
         D.check(h, rc)
         failures = _failures(fail)
     Xout = X.cpu().numpy() if host else X

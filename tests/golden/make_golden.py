@@ -20,6 +20,10 @@ Cases (each cites the reference test it mirrors):
                      (test_solvers.py:73-85)
   config1.npz        config 1 (n=500, m=p=5, 100 i*omega shifts) reference G
                      and input checksums (BASELINE.json configs[0])
+  transposed.npz     solve_shifted_transposed on reduced triples (general
+                     right-hand sides), the scalar known answer, a failure
+                     case, and mirrored_schedule plans (test_solvers.py:139-189,
+                     test_schedule.py:106-120)
 """
 
 from __future__ import annotations
@@ -42,7 +46,9 @@ from shiftsolve import (  # noqa: E402
     random_stable_system,
     reduce_controller_hessenberg,
     solve_shifted_reduced,
+    solve_shifted_transposed,
 )
+from shiftsolve.schedule import mirrored_schedule  # noqa: E402
 from shiftsolve.hessenberg import ControllerHessForm  # noqa: E402
 from shiftsolve.oracles import lu_solve_shifted, oracle_transfer_function  # noqa: E402
 
@@ -183,7 +189,55 @@ def config1():
                         dims=np.asarray([n, m, p]))
 
 
+def transposed():
+    rng = np.random.default_rng(17)
+    d = {}
+    specs = [(40, 3, 2, 12, 8), (30, 2, 2, 13, 8), (33, 3, 2, 14, 8), (64, 4, 3, 40, 16),
+             (96, 6, 4, 41, 16), (128, 8, 3, 42, 32), (75, 1, 1, 43, 8), (57, 5, 2, 44, 4),
+             (200, 10, 10, 45, 32)]
+    for idx, (n, m, p, seed, nb) in enumerate(specs):
+        sysb = random_stable_system(n, m, p, seed=seed)
+        chf = reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+        shifts = bounded_shifts(rng, chf.Ahat, 6)
+        rhs = rng.standard_normal((n, 6)) + 1j * rng.standard_normal((n, 6))
+        res = solve_shifted_transposed(chf, shifts, rhs, nb=nb)
+        xlu = np.stack([lu_solve_shifted(chf.Ahat, s_, rhs[:, l], transpose=True)
+                        for l, s_ in enumerate(shifts)], axis=1)
+        pre = f"t{idx}_"
+        d[pre + "dims"] = np.asarray([n, m, p, seed, nb])
+        d[pre + "Ahat"], d[pre + "Bhat"], d[pre + "Chat"] = chf.Ahat, chf.Bhat, chf.Chat
+        d[pre + "shifts"], d[pre + "rhs"], d[pre + "x"], d[pre + "xlu"] = shifts, rhs, res.x, xlu
+    d["count"] = np.asarray(len(specs))
+    # scalar known answer (test_solvers.py:139-142)
+    chf1 = ControllerHessForm(Ahat=np.array([[2.0]], order="F"), Bhat=np.array([[1.0]], order="F"),
+                              Chat=np.array([[1.0]], order="F"), m=1, n=1, p=1)
+    r1 = solve_shifted_transposed(chf1, [0.5], np.array([[3.0 + 0j]]), nb=4)
+    d["scalar_x"] = r1.x
+    # failure isolation (test_solvers.py:173-184)
+    sysb = random_stable_system(24, 2, 2, seed=15)
+    chf = reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    good = bounded_shifts(rng, chf.Ahat, 5)
+    ev = np.linalg.eigvals(chf.Ahat)
+    bad = ev[int(np.argmax(np.abs(ev.imag)))]
+    full = np.concatenate([good, [bad]])
+    rhs = rng.standard_normal((24, 6)) + 1j * rng.standard_normal((24, 6))
+    rf = solve_shifted_transposed(chf, full, rhs, nb=4, on_singular="mark")
+    d["f_Ahat"], d["f_Bhat"], d["f_Chat"] = chf.Ahat, chf.Bhat, chf.Chat
+    d["f_shifts"], d["f_rhs"], d["f_x"] = full, rhs, rf.x
+    d["f_failures"] = np.asarray(sorted(rf.failures.items()), dtype=np.int64).reshape(-1, 2)
+    # mirrored schedules
+    for nr, nc in [(3, 5), (8, 14), (16, 26), (32, 42), (64, 74)]:
+        sch = mirrored_schedule(nr, nc)
+        d[f"ms_{nr}_{nc}_job"] = np.asarray(sch.job_size, dtype=np.int64)
+        d[f"ms_{nr}_{nc}_info"] = np.asarray(sch.rot_info, dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "transposed.npz"), **d)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     schedules()
     batched()
     scalar()

@@ -113,3 +113,17 @@ def test_error_types_mirror_reference():
     e = ss.SingularShiftError([(3, 1), (1, 0)])
     assert e.failures == [(3, 1), (1, 0)] and "[1, 3]" in str(e)
     assert issubclass(ss.SingularShiftError, ArithmeticError)
+
+
+def test_mirrored_schedule_matches_reference():
+    """schedule.py:162-184 mirrored_schedule, bitwise against the reference's
+    plans (tests/golden/transposed.npz) and the (3, 5) targets of
+    test_schedule.py:106-120 (superdiagonal band, helpers to the left)."""
+    g = golden("transposed.npz")
+    for nr, nc in [(3, 5), (8, 14), (16, 26), (32, 42), (64, 74)]:
+        sch = ss.mirrored_schedule(nr, nc)
+        assert np.array_equal(np.asarray(sch.job_size), g[f"ms_{nr}_{nc}_job"])
+        assert np.array_equal(np.asarray(sch.rot_info), g[f"ms_{nr}_{nc}_info"])
+    sch = ss.mirrored_schedule(3, 5)
+    for r, c1, c2 in np.asarray(sch.rot_info).reshape(-1, 3):
+        assert c2 < c1 and c1 > r  # target above the diagonal, helper to its left
