@@ -15,6 +15,16 @@ from .errors import (
     SingularShiftError,
 )
 from .hessenberg import ControllerHessForm, reduce_controller_hessenberg
+from .irka import (
+    IrkaState,
+    IterationRecord,
+    ReducedModel,
+    default_initial_data,
+    irka_iterate,
+    pair_conjugates,
+    relative_hausdorff,
+    small_eig_pencil,
+)
 from .schedule import AnnihilationSchedule, greedy_schedule, mirrored_schedule
 from .solvers import (
     ShiftedSolveResult,
@@ -33,6 +43,14 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AnnihilationSchedule",
+    "IrkaState",
+    "IterationRecord",
+    "ReducedModel",
+    "default_initial_data",
+    "irka_iterate",
+    "pair_conjugates",
+    "relative_hausdorff",
+    "small_eig_pencil",
     "ControllerHessForm",
     "DimensionMismatchError",
     "EigensolverError",

@@ -20,6 +20,9 @@ Cases (each cites the reference test it mirrors):
                      (test_solvers.py:73-85)
   config1.npz        config 1 (n=500, m=p=5, 100 i*omega shifts) reference G
                      and input checksums (BASELINE.json configs[0])
+  irka.npz           irka_iterate trajectories (shift history per iteration,
+                     final reduced model) on reduced triples
+                     (test_irka.py:81-131)
   transposed.npz     solve_shifted_transposed on reduced triples (general
                      right-hand sides), the scalar known answer, a failure
                      case, and mirrored_schedule plans (test_solvers.py:139-189,
@@ -231,6 +234,27 @@ def transposed():
         d[f"ms_{nr}_{nc}_job"] = np.asarray(sch.job_size, dtype=np.int64)
         d[f"ms_{nr}_{nc}_info"] = np.asarray(sch.rot_info, dtype=np.int64)
     np.savez_compressed(os.path.join(OUT, "transposed.npz"), **d)
+
+
+def irka():
+    from shiftsolve.irka import default_initial_data, irka_iterate
+    d = {}
+    specs = [(30, 1, 1, 4, 4, 8), (30, 2, 2, 5, 4, 10), (24, 2, 2, 2, 4, 6), (60, 3, 2, 50, 6, 6),
+             (120, 4, 3, 51, 8, 5)]
+    for idx, (n, m, p, seed, r, iters) in enumerate(specs):
+        sysb = random_stable_system(n, m, p, seed=seed)
+        chf = reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+        s0, b0, c0 = default_initial_data(chf, r)
+        model, state = irka_iterate(chf, r, s0, b0, c0, maxiter=iters, fixed_iters=True, nb=8)
+        pre = f"i{idx}_"
+        d[pre + "dims"] = np.asarray([n, m, p, seed, r, iters])
+        d[pre + "A"], d[pre + "B"], d[pre + "C"] = sysb.A, sysb.B, sysb.C
+        d[pre + "Ahat"], d[pre + "Bhat"], d[pre + "Chat"] = chf.Ahat, chf.Bhat, chf.Chat
+        d[pre + "hist"] = np.stack([rec.shifts for rec in state.history])
+        d[pre + "final"] = state.shifts
+        d[pre + "Ar"], d[pre + "Br"], d[pre + "Cr"] = model.Ar, model.Br, model.Cr
+    d["count"] = np.asarray(len(specs))
+    np.savez_compressed(os.path.join(OUT, "irka.npz"), **d)
 
 
 if __name__ == "__main__":
