@@ -23,6 +23,8 @@ Cases (each cites the reference test it mirrors):
   irka.npz           irka_iterate trajectories (shift history per iteration,
                      final reduced model) on reduced triples
                      (test_irka.py:81-131)
+  cli/               a reference CLI session: `gen` -> `reduce` (archive with
+                     manifest) -> `tf` and `pspec` CSVs (test_sysio_cli.py)
   transposed.npz     solve_shifted_transposed on reduced triples (general
                      right-hand sides), the scalar known answer, a failure
                      case, and mirrored_schedule plans (test_solvers.py:139-189,
@@ -234,6 +236,25 @@ def transposed():
         d[f"ms_{nr}_{nc}_job"] = np.asarray(sch.job_size, dtype=np.int64)
         d[f"ms_{nr}_{nc}_info"] = np.asarray(sch.rot_info, dtype=np.int64)
     np.savez_compressed(os.path.join(OUT, "transposed.npz"), **d)
+
+
+def cli():
+    import shutil
+
+    from shiftsolve.cli import main as ref_main
+    root = os.path.join(OUT, "cli")
+    shutil.rmtree(root, ignore_errors=True)
+    os.makedirs(root)
+    sysdir, arch = os.path.join(root, "sys"), os.path.join(root, "archive")
+    assert ref_main(["gen", "--n", "40", "--m", "3", "--p", "2", "--seed", "5", "--out", sysdir]) == 0
+    assert ref_main(["reduce", *(os.path.join(sysdir, f) for f in ("A.mtx", "B.mtx", "C.mtx")),
+                     "--out", arch, "--block-size", "8"]) == 0
+    assert ref_main(["tf", arch, "--out", os.path.join(root, "tf.csv"), "--w-min", "0.1",
+                     "--w-max", "100", "--count", "9", "--nb", "8"]) == 0
+    assert ref_main(["pspec", arch, "--out", os.path.join(root, "pspec.csv"), "--re-min", "-3",
+                     "--re-max", "1", "--re-count", "4", "--im-min", "-2", "--im-max", "2",
+                     "--im-count", "3", "--nb", "8"]) == 0
+    shutil.rmtree(sysdir)  # the archive is the fixture; gen is re-run by the test
 
 
 def irka():
