@@ -527,8 +527,7 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
             <<<(sb + kBlkShiftsPerWarp - 1) / kBlkShiftsPerWarp, 32, smem, st>>>(bd, Z, W, sb); \
         break;                                                            \
     }
-        SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
-        SS_CASE(10)
+        SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) SS_CASE(10)
 #undef SS_CASE
         default: return ss::set_err(h, SS_EARG, "two-level sweep: unsupported m");
     }
@@ -536,7 +535,9 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
     return SS_OK;
 }
 
-bool block_supported(int m) { return (m >= 1 && m <= 8) || m == 10; }
+// m < 4: the per-window overhead 2m/nb is already < 13% at nb = 64 and the
+// one-level sweep measured faster (config 3, m = 1: 13.7 vs 19.3 ms)
+bool block_supported(int m) { return (m >= 4 && m <= 8) || m == 10; }
 
 // Reference phase flops of the window sweep at block size nb0 (shape only:
 // batched.py:58-61, solvers.py:186-199), independent of how the device
