@@ -47,7 +47,10 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     k_far(UpdDims u, double2* Z, const double2* __restrict__ Pbuf) {
     constexpr int RG = 32 / G, M = G * C, TILE = RG * R;
     constexpr int m = M;
-    static_assert(R % 2 == 0 && 2 * NST + 2 * NPAIR <= 32, "k_far: shape");
+    // every pair owns NST / NPAIR stages outright: a stage shared by several
+    // pairs would let a fast pair pass a full-barrier parity test two uses
+    // ahead (phase aliasing)
+    static_assert(R % 2 == 0 && 2 * NST + 2 * NPAIR <= 32 && NST % NPAIR == 0, "k_far: shape");
     extern __shared__ __align__(16) unsigned char smem[];
     const int nb = u.nb, nc = u.nc, r0 = u.r0, sb = u.sb;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NST]
@@ -85,9 +88,15 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
         if (lane == 0) {
             const unsigned p12bytes = (unsigned)(nb * m * 16);
             const unsigned p22bytes = ZID ? 0u : (unsigned)(m * m * 16);
+            // a stage may serve several pairs in turn (NST % NPAIR != 0): its
+            // uses must be issued in unit order, or the parity test on its
+            // empty barrier could alias two phases ahead
             int next[NPAIR];
+            int last[NST];  // last unit issued into each stage
 #pragma unroll
             for (int p = 0; p < NPAIR; ++p) next[p] = p;
+#pragma unroll
+            for (int q = 0; q < NST; ++q) last[q] = q - NST;
             int left = nun;
             while (left > 0) {
                 bool any = false;
@@ -96,7 +105,13 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
                     const int k = next[p];
                     if (k >= nun) continue;
                     const int s = k % NST, use = k / NST;
+                    int lk = 0;
+#pragma unroll
+                    for (int q = 0; q < NST; ++q) lk = (q == s) ? last[q] : lk;
+                    if (lk != k - NST) continue;
                     if (use > 0 && !mbar_test(empty + s, (use - 1) & 1)) continue;
+#pragma unroll
+                    for (int q = 0; q < NST; ++q) last[q] = (q == s) ? k : last[q];
                     const int64_t unit = ua + k;
                     const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
                     const int i0 = u.rlo + tile * TILE;

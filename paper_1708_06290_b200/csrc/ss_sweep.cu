@@ -417,9 +417,9 @@ struct FarShape {
 };
 
 FarShape far_shape(const UpdTile& t) {
-    // measured on B200 (config 2): R = 8 rows per lane with 3 pairs / 5 stages
-    // (255 registers, spills) is slower than R = 2G with 4 pairs / 8 stages
-    if (t.G == 2 && t.C == 5 && getenv("SS_FAR_R8")) return FarShape{2, 5, 8, 3, 5};
+    // measured on B200 (config 2): R = 8 rows per lane (3 pairs, 255
+    // registers, spills) was slower than R = 2G with 4 pairs / 8 stages
+    if (t.G == 2 && t.C == 5 && getenv("SS_FAR_P3")) return FarShape{2, 5, 4, 3, 6};
     return FarShape{t.G, t.C, 2 * t.G, 4, 8};
 }
 
@@ -430,7 +430,8 @@ int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStrea
     if (f.G == GG && f.C == CC && f.R == RR && f.NPAIR == NP && f.NST == NS)                   \
         return u.zid ? launch_far_z<GG, CC, RR, NP, NS, true>(h, grid, smem, st, u, z, pbuf)   \
                      : launch_far_z<GG, CC, RR, NP, NS, false>(h, grid, smem, st, u, z, pbuf);
-    SS_FAR(2, 5, 8, 3, 5) SS_FAR(2, 5, 4, 4, 8) SS_FAR(2, 4, 4, 4, 8)
+    SS_FAR(2, 5, 4, 4, 8) SS_FAR(2, 5, 4, 3, 6)
+    SS_FAR(2, 4, 4, 4, 8)
     SS_FAR(1, 1, 2, 4, 8) SS_FAR(1, 2, 2, 4, 8) SS_FAR(1, 3, 2, 4, 8) SS_FAR(1, 4, 2, 4, 8)
     SS_FAR(1, 5, 2, 4, 8) SS_FAR(1, 6, 2, 4, 8) SS_FAR(1, 7, 2, 4, 8) SS_FAR(1, 8, 2, 4, 8)
 #undef SS_FAR
