@@ -70,6 +70,15 @@ int ss_tf_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t ld
                const double* shifts, int64_t s, int nb, int64_t batch, double rtol,
                double* G, int64_t ldg, int32_t* fail_row, void* stream);
 
+/* Structured pseudospectrum: ss_tf_eval (G into the caller's scratch G)
+ * followed by a device epilogue norms[l] = ||G_l||_2 (p x m block; +inf for
+ * a singular shift).  Replaces solvers.py:501-530 (two_norm_small's numpy
+ * SVD).  Requires min(p, m) <= 32. */
+int ss_pspec_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t lda,
+                  const double* Bhat, int64_t ldb, const double* Chat, int64_t ldc,
+                  const double* shifts, int64_t s, int nb, int64_t batch, double rtol, double* G,
+                  int64_t ldg, double* norms, int32_t* fail_row, void* stream);
+
 /* Reduced shifted solves (Ahat - sigma_l I) x_l = Bhat b_l.
  * Replaces solvers.py:274-313 solve_shifted_reduced.  bdirs: m x s
  * complex128 (ldbd); X: n x s complex128 (ldx), NaN column on failure. */

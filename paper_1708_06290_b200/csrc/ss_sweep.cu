@@ -815,6 +815,85 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     return SS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Pseudospectrum epilogue (solvers.py:501-530 structured_pseudospectrum_grid
+// with two_norm_small): ||G_l||_2 of every p x m block on the device.  One
+// 32-thread CTA per shift forms the k x k Gram matrix (k = min(p, m)) in
+// shared memory and thread 0 runs cyclic complex Hermitian Jacobi to
+// convergence; ||G||_2 = sqrt(lambda_max).  Failed shifts give +inf.
+// ---------------------------------------------------------------------------
+constexpr int kPnMax = 32;
+
+__global__ void __launch_bounds__(32) k_pnorm(int p, int m, const double2* __restrict__ G,
+                                              int64_t ldg, const int32_t* __restrict__ fail,
+                                              double* __restrict__ norms) {
+    __shared__ double2 H[kPnMax][kPnMax + 1];
+    const int l = blockIdx.x, tid = threadIdx.x;
+    const double2* Gl = G + (int64_t)l * m * ldg;  // G_l(i, j) = Gl[i + j * ldg]
+    if (fail[l] >= 0) {
+        if (tid == 0) norms[l] = __longlong_as_double(0x7ff0000000000000ULL);
+        return;
+    }
+    const bool gram_cols = p >= m;  // H = G^H G (m x m) or G G^H (p x p)
+    const int k = gram_cols ? m : p, r = gram_cols ? p : m;
+    for (int u = tid; u < k * k; u += 32) {
+        const int i = u % k, j = u / k;
+        double2 acc = cz();
+        for (int t = 0; t < r; ++t) {
+            const double2 a = gram_cols ? Gl[t + (int64_t)i * ldg] : Gl[i + (int64_t)t * ldg];
+            const double2 b = gram_cols ? Gl[t + (int64_t)j * ldg] : Gl[j + (int64_t)t * ldg];
+            // gram_cols: conj(G_ti) G_tj ; else G_it conj(G_jt)
+            const double2 x = gram_cols ? make_double2(a.x, -a.y) : a;
+            const double2 y = gram_cols ? b : make_double2(b.x, -b.y);
+            acc = cfma(x, y, acc);
+        }
+        H[i][j] = acc;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+    double fro2 = 0.0;
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) fro2 += H[i][j].x * H[i][j].x + H[i][j].y * H[i][j].y;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        double off = 0.0;
+        for (int i = 0; i < k; ++i)
+            for (int j = i + 1; j < k; ++j) off += H[i][j].x * H[i][j].x + H[i][j].y * H[i][j].y;
+        if (off <= 1e-32 * fro2 || off == 0.0) break;
+        for (int a = 0; a < k; ++a) {
+            for (int b = a + 1; b < k; ++b) {
+                const double2 c = H[a][b];
+                const double ac = hypot(c.x, c.y);
+                if (ac == 0.0) continue;
+                const double2 e = make_double2(c.x / ac, c.y / ac);
+                const double ha = H[a][a].x, hb = H[b][b].x;
+                const double tau = (hb - ha) / (2.0 * ac);
+                const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
+                const double2 ce = make_double2(e.x, -e.y);
+                // columns: H V with V_aa = cs, V_ab = sn, V_ba = -sn conj(e), V_bb = cs conj(e)
+                for (int i = 0; i < k; ++i) {
+                    const double2 x = H[i][a], y = cmul(H[i][b], ce);
+                    H[i][a] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+                    H[i][b] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+                }
+                // rows: V^H (H V)
+                for (int j = 0; j < k; ++j) {
+                    const double2 x = H[a][j], y = cmul(H[b][j], e);
+                    H[a][j] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+                    H[b][j] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+                }
+                H[a][b] = H[b][a] = cz();
+                H[a][a] = make_double2(ha - t * ac, 0.0);
+                H[b][b] = make_double2(hb + t * ac, 0.0);
+            }
+        }
+    }
+    double lmax = 0.0;
+    for (int i = 0; i < k; ++i) lmax = fmax(lmax, H[i][i].x);
+    norms[l] = sqrt(lmax);
+}
+
 }  // namespace
 
 namespace ss {
@@ -984,6 +1063,25 @@ int ss_tf_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t ld
     a.ldo = ldg > 0 ? ldg : 1;
     a.fail = fail_row;
     return run_sweep(h, a, (cudaStream_t)stream);
+}
+
+int ss_pspec_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t lda,
+                  const double* Bhat, int64_t ldb, const double* Chat, int64_t ldc,
+                  const double* shifts, int64_t s, int nb, int64_t batch, double rtol, double* G,
+                  int64_t ldg, double* norms, int32_t* fail_row, void* stream) {
+    if (!h) return SS_EARG;
+    if (p < 1 || std::min(p, m) > kPnMax)
+        return ss::set_err(h, SS_EARG, "pseudospectrum epilogue: min(p, m) must be <= 32");
+    if (s > 0 && !norms) return ss::set_err(h, SS_EARG, "null pointer");
+    int rc = ss_tf_eval(h, n, m, p, Ahat, lda, Bhat, ldb, Chat, ldc, shifts, s, nb, batch, rtol, G,
+                        ldg, fail_row, stream);
+    if (rc || s == 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t ev = ss::timing_begin(h, st);
+    k_pnorm<<<(unsigned)s, 32, 0, st>>>(p, m, (const double2*)G, ldg, fail_row, norms);
+    SS_LAUNCH_CHECK(h);
+    ss::timing_end(h, st, ev, ss::PH_TAIL);
+    return SS_OK;
 }
 
 int ss_solve_reduced(ss_handle* h, int n, int m, const double* Ahat, int64_t lda,

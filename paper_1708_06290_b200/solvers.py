@@ -228,33 +228,49 @@ def structured_pseudospectrum_grid(chf: ControllerHessForm, grid, nb: int = 32,
                                    counter: PhaseCounters | None = None,
                                    singular_rtol: float | None = None):
     """||C (z I - A)^{-1} B||_2 over grid points; singular points -> +inf
-    (solvers.py:508-530).  The spectral norms of the p x m values are taken
-    on the device (|G| for SISO)."""
+    (solvers.py:508-530).  The spectral norms of the p x m values come from a
+    device epilogue of the sweep (``ss_pspec_eval``: Gram matrix + Hermitian
+    Jacobi per point) instead of the reference's numpy SVD."""
+    del pool
+    _check_chf(chf)
     grid = _shifts_in(grid)
-    host = D.is_host(grid) and all(D.is_host(a) for a in (chf.Ahat, chf.Bhat, chf.Chat))
-    res = eval_transfer_function(chf, grid if host else grid, nb=nb, batch_size=batch_size,
-                                 counter=counter, on_singular="mark",
-                                 singular_rtol=singular_rtol)
-    m, p, s = chf.m, chf.p, len(grid)
-    G = res.G if isinstance(res.G, torch.Tensor) else None
-    if G is None:
-        dev = D.device_of(chf.Ahat)
-        G = torch.from_numpy(np.asfortranarray(res.G)).to(dev)
-    if s == 0:
-        out = torch.zeros(0, dtype=torch.float64, device=G.device)
-    elif p == 0 or m == 0:
-        out = torch.zeros(s, dtype=torch.float64, device=G.device)
-    else:
-        blocks = G.reshape(p, s, m).permute(1, 0, 2)  # (s, p, m)
-        if m == 1 and p == 1:
-            out = blocks.reshape(s).abs()
+    n, m, p = chf.n, chf.m, chf.p
+    s = len(grid)
+    if nb < 1:
+        raise ValueError("window block size must be >= 1")
+    rtol = default_singular_rtol(n) if singular_rtol is None else float(singular_rtol)
+    host = all(D.is_host(a) for a in (chf.Ahat, chf.Bhat, chf.Chat, grid))
+    dev = D.device_of(chf.Ahat, chf.Bhat, chf.Chat, grid)
+    if s == 0 or p == 0 or min(p, m) > 32:
+        # degenerate sizes or blocks beyond the epilogue: G on the device, norms by torch
+        res = eval_transfer_function(chf, grid, nb=nb, batch_size=batch_size, counter=counter,
+                                     on_singular="mark", singular_rtol=singular_rtol)
+        G = res.G if isinstance(res.G, torch.Tensor) else torch.from_numpy(
+            np.asfortranarray(res.G)).to(dev)
+        if s == 0 or p == 0:
+            out = torch.zeros(s, dtype=torch.float64, device=G.device)
         else:
-            out = torch.linalg.matrix_norm(blocks, ord=2)
-        if res.failures:
-            idx = torch.tensor(sorted(res.failures), dtype=torch.long, device=G.device)
-            out = out.clone()
-            out[idx] = float("inf")
-    return out.cpu().numpy() if host else out
+            out = torch.linalg.matrix_norm(G.reshape(p, s, m).permute(1, 0, 2), ord=2)
+            if res.failures:
+                out = out.clone()
+                out[torch.tensor(sorted(res.failures), device=G.device)] = float("inf")
+        return out.cpu().numpy() if host else out
+    with torch.cuda.device(dev):
+        A = D.fmat(chf.Ahat, torch.float64, dev)
+        B = D.fmat(chf.Bhat, torch.float64, dev)
+        C = D.fmat(chf.Chat, torch.float64, dev)
+        sh = D.fvec(grid, torch.complex128, dev)
+        G = torch.empty((s * m, p), dtype=torch.complex128, device=dev).t()
+        norms = torch.empty(s, dtype=torch.float64, device=dev)
+        fail = torch.empty(s, dtype=torch.int32, device=dev)
+        h = _lib.handle(dev.index)
+        L = _lib.load()
+        with D.timed_call(h, counter):
+            rc = L.ss_pspec_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C),
+                                 D.ld(C), D.ptr(sh), s, int(nb), _batch(batch_size), rtol,
+                                 D.ptr(G), p, D.ptr(norms), D.ptr(fail), D.stream_ptr(dev))
+        D.check(h, rc)
+    return norms.cpu().numpy() if host else norms
 
 
 def residual_certificate(chf: ControllerHessForm, sigma: complex, x, rhs,

@@ -435,3 +435,24 @@ def test_wide_m_paths_vs_oracle(n, m, p):
     for k in range(4):
         cert = ss.residual_certificate(chf, shifts[k], red.x[:, k], chf.Bhat @ bd[:, k])
         assert cert <= 1e3 * n * EPS
+
+
+@pytest.mark.parametrize("n,m,p", [(120, 7, 3), (90, 2, 6), (300, 10, 10), (64, 4, 1)])
+def test_pseudospectrum_epilogue_vs_svd(n, m, p):
+    """The device ||G||_2 epilogue (Gram matrix + Hermitian Jacobi) against
+    numpy's SVD of the same G blocks (solvers.py:501-505), wide and tall
+    blocks; singular points -> +inf."""
+    chf = _mhess_triple(n, m, p, seed=n + m + p)
+    rng = np.random.default_rng(n)
+    grid = (rng.uniform(-1, 1, 40) + 1j * rng.uniform(-1, 1, 40)) * np.sqrt(n)
+    vals = ss.structured_pseudospectrum_grid(chf, grid, nb=32)
+    G = ss.eval_transfer_function(chf, grid, nb=32).G
+    ref = np.array([np.linalg.svd(G[:, l * m:(l + 1) * m], compute_uv=False)[0]
+                    for l in range(len(grid))])
+    assert np.max(np.abs(vals - ref) / ref) <= 1e-12
+    # at a (numerically computed) eigenvalue: flagged singular (+inf) or a
+    # resolvent norm orders of magnitude above the grid's
+    ev = np.linalg.eigvals(chf.Ahat)
+    v2 = ss.structured_pseudospectrum_grid(chf, np.array([ev[0], grid[0]]), nb=32)
+    assert np.isinf(v2[0]) or v2[0] > 1e4 * np.median(ref)
+    assert abs(v2[1] - ref[0]) <= 1e-12 * ref[0]
