@@ -42,20 +42,26 @@ __device__ __forceinline__ int far_pan_index(int row) {
     return p * (2 * RG) + rg * 2 + e;
 }
 
-template <int G, int C, int R, int NPAIR, int NST, bool ZID>
+// NCB column blocks: a unit's m = NCB G C columns are split over a group of
+// NCB pairs (pair cbk owns columns [cbk G C, (cbk + 1) G C)); the group shares
+// the unit's stage (P for all m columns, the 64 x m Z tile: every pair's Z2
+// part needs all m state columns).
+template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB = 1>
 __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     k_far(UpdDims u, double2* Z, const double2* __restrict__ Pbuf) {
-    constexpr int RG = 32 / G, M = G * C, TILE = RG * R;
+    constexpr int RG = 32 / G, MB = G * C, M = MB * NCB, TILE = RG * R;
+    constexpr int NG = NPAIR / NCB;  // consumer groups (one unit each at a time)
     constexpr int m = M;
-    // every pair owns NST / NPAIR stages outright: a stage shared by several
-    // pairs would let a fast pair pass a full-barrier parity test two uses
+    // every group owns NST / NG stages outright: a stage shared by several
+    // groups would let a fast group pass a full-barrier parity test two uses
     // ahead (phase aliasing)
-    static_assert(R % 2 == 0 && 2 * NST + 2 * NPAIR <= 32 && NST % NPAIR == 0, "k_far: shape");
+    static_assert(R % 2 == 0 && 2 * NST + 2 * NPAIR <= 32 && NPAIR % NCB == 0 && NST % NG == 0,
+                  "k_far: shape");
     extern __shared__ __align__(16) unsigned char smem[];
     const int nb = u.nb, nc = u.nc, r0 = u.r0, sb = u.sb;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NST]
     uint64_t* empty = full + NST;                          // [NST]
-    uint64_t* zfree = empty + NST;                         // [NPAIR]
+    uint64_t* zfree = empty + NST;                         // [NG] (count NCB)
     uint64_t* partr = zfree + NPAIR;                       // [NPAIR]
     double* Pan = reinterpret_cast<double*>(smem + 256);   // [nb][TILE] pair-interleaved
     double2* Stg = reinterpret_cast<double2*>(smem + 256 + (size_t)nb * TILE * 8);
@@ -69,10 +75,10 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 2);
+            mbar_init(empty + s, 2 * NCB);
         }
         for (int p = 0; p < NPAIR; ++p) {
-            mbar_init(zfree + p, 1);
+            mbar_init(zfree + p, NCB);
             mbar_init(partr + p, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -91,17 +97,17 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
             // a stage may serve several pairs in turn (NST % NPAIR != 0): its
             // uses must be issued in unit order, or the parity test on its
             // empty barrier could alias two phases ahead
-            int next[NPAIR];
+            int next[NG];
             int last[NST];  // last unit issued into each stage
 #pragma unroll
-            for (int p = 0; p < NPAIR; ++p) next[p] = p;
+            for (int p = 0; p < NG; ++p) next[p] = p;
 #pragma unroll
             for (int q = 0; q < NST; ++q) last[q] = q - NST;
             int left = nun;
             while (left > 0) {
                 bool any = false;
 #pragma unroll
-                for (int p = 0; p < NPAIR; ++p) {
+                for (int p = 0; p < NG; ++p) {
                     const int k = next[p];
                     if (k >= nun) continue;
                     const int s = k % NST, use = k / NST;
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
                     for (int c = 0; c < m; ++c)
                         tma_bulk_g2s(zt + c * TILE, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
                                      full + s);
-                    next[p] = k + NPAIR;
+                    next[p] = k + NG;
                     --left;
                     any = true;
                 }
@@ -137,8 +143,9 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
 
     // ---------------- consumers ----------------
     const int cw = warp - 1, pair = cw >> 1, half = cw & 1;
+    const int grp = pair / NCB, cbk = pair - grp * NCB;
     const int rg = lane / G, q = lane - rg * G;
-    const int cb = q * C;
+    const int cb = cbk * MB + q * C;  // first output column of this lane
     const int dlo = r0 - m;
     const int jlo = half == 0 ? 0 : u.jh;
     const int jhi = half == 1 ? nb : u.jh;
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
         const int ka = (int)(max(ua, (int64_t)tile * sb) - ua);
         const int kb = (int)(min(ub, (int64_t)(tile + 1) * sb) - ua);
         const int l0t = (int)(ua + ka - (int64_t)tile * sb) - ka;  // l = l0t + k
-        for (int k = ka + (((pair - ka) % NPAIR) + NPAIR) % NPAIR; k < kb; k += NPAIR) {
+        for (int k = ka + (((grp - ka) % NG) + NG) % NG; k < kb; k += NG) {
         const int l = l0t + k;
         const int i0 = u.rlo + tile * TILE;
         const bool interior = i0 + TILE <= (u.mnb > 0 ? dlo : r0);
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(zfree + pair);
+            if (lane == 0) mbar_arrive(zfree + grp);
         }
 #pragma unroll 2
         for (int j = jlo; j < jhi; ++j) {
@@ -224,9 +231,9 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
                 for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
             }
         }
-        double2* red = Zs + lane;  // [(r*C + c)][lane] over the consumed Z tile
+        double2* red = Zs + cbk * (MB * TILE) + lane;  // [(r*C + c)][lane] over the consumed Z tile
         if (half == 1) {
-            mbar_wait(zfree + pair, npair & 1);
+            mbar_wait(zfree + grp, npair & 1);
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll

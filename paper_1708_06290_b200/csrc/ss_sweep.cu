@@ -396,15 +396,15 @@ int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, co
     return launch_update_ws_z<G, C, false>(h, grid, smem, st, u, zin, zout, pbuf);
 }
 
-template <int G, int C, int R, int NPAIR, int NST, bool ZID>
+template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB>
 int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                  const double2* pbuf) {
     static bool configured = false;
     if (!configured) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID, NCB>));
         configured = true;
     }
-    k_far<G, C, R, NPAIR, NST, ZID><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
+    k_far<G, C, R, NPAIR, NST, ZID, NCB><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -412,28 +412,29 @@ int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const Upd
 // Far-row kernel shape: R rows x C columns per lane, 32/G row groups -> a
 // tile of (32/G) R rows; NPAIR consumer pairs; NST ring stages.
 struct FarShape {
-    int G, C, R, NPAIR, NST;
+    int G, C, R, NPAIR, NST, NCB;
     int tile() const { return (32 / G) * R; }
+    int m() const { return G * C * NCB; }
 };
 
 FarShape far_shape(const UpdTile& t) {
     // measured on B200 (config 2): R = 8 rows per lane (3 pairs, 255
     // registers, spills) was slower than R = 2G with 4 pairs / 8 stages
-    if (t.G == 2 && t.C == 5 && getenv("SS_FAR_P3")) return FarShape{2, 5, 4, 3, 6};
-    return FarShape{t.G, t.C, 2 * t.G, 4, 8};
+    if (t.G == 2 && t.C == 5 && getenv("SS_FAR_P3")) return FarShape{2, 5, 4, 3, 6, 1};
+    return FarShape{t.G, t.C, 2 * t.G, 4, 8, 1};
 }
 
 // Persistent far-row update (ss_far.cuh): one CTA per SM over (tile, shift) units.
 int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStream_t st,
                const UpdDims& u, double2* z, const double2* pbuf) {
-#define SS_FAR(GG, CC, RR, NP, NS)                                                             \
-    if (f.G == GG && f.C == CC && f.R == RR && f.NPAIR == NP && f.NST == NS)                   \
-        return u.zid ? launch_far_z<GG, CC, RR, NP, NS, true>(h, grid, smem, st, u, z, pbuf)   \
-                     : launch_far_z<GG, CC, RR, NP, NS, false>(h, grid, smem, st, u, z, pbuf);
-    SS_FAR(2, 5, 4, 4, 8) SS_FAR(2, 5, 4, 3, 6)
-    SS_FAR(2, 4, 4, 4, 8)
-    SS_FAR(1, 1, 2, 4, 8) SS_FAR(1, 2, 2, 4, 8) SS_FAR(1, 3, 2, 4, 8) SS_FAR(1, 4, 2, 4, 8)
-    SS_FAR(1, 5, 2, 4, 8) SS_FAR(1, 6, 2, 4, 8) SS_FAR(1, 7, 2, 4, 8) SS_FAR(1, 8, 2, 4, 8)
+#define SS_FAR(GG, CC, RR, NP, NS, KB)                                                           \
+    if (f.G == GG && f.C == CC && f.R == RR && f.NPAIR == NP && f.NST == NS && f.NCB == KB)      \
+        return u.zid ? launch_far_z<GG, CC, RR, NP, NS, true, KB>(h, grid, smem, st, u, z, pbuf)  \
+                     : launch_far_z<GG, CC, RR, NP, NS, false, KB>(h, grid, smem, st, u, z, pbuf);
+    SS_FAR(2, 5, 4, 4, 8, 1) SS_FAR(2, 5, 4, 3, 6, 1) SS_FAR(2, 5, 4, 4, 4, 2)
+    SS_FAR(2, 4, 4, 4, 8, 1)
+    SS_FAR(1, 1, 2, 4, 8, 1) SS_FAR(1, 2, 2, 4, 8, 1) SS_FAR(1, 3, 2, 4, 8, 1) SS_FAR(1, 4, 2, 4, 8, 1)
+    SS_FAR(1, 5, 2, 4, 8, 1) SS_FAR(1, 6, 2, 4, 8, 1) SS_FAR(1, 7, 2, 4, 8, 1) SS_FAR(1, 8, 2, 4, 8, 1)
 #undef SS_FAR
     return SS_EARG;
 }
@@ -787,6 +788,21 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
             rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z, B.Z,
                                   B.P);
+        } else if (nws == 2 && tile.exact && tile.G == 2 && tile.C == 5 && !getenv("SS_UPDATE_CLASSIC") &&
+                   far_smem_bytes(s.nb, m, 64, 4) + 1024 <= h->smem_optin) {
+            // m = 20: persistent far kernel with two column blocks per unit
+            // (one group of two pairs shares the unit's stage)
+            const FarShape f{2, 5, 4, 4, 4, 2};
+            u.pstride = (int64_t)s.nc * m;
+            u.p12off = 0;
+            u.p22off = (int64_t)s.nb * m;
+            u.zid = 0;
+            u.flags = 0;
+            u.SG = 32;
+            u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2 - 1));
+            const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * sb;
+            const int grid = (int)std::min<int64_t>(units, h->num_sms);
+            rc = launch_far(h, f, grid, far_smem_bytes(s.nb, m, f.tile(), f.NST), st, u, B.Z, B.P);
         } else {
             rc = launch_update(h, tile, g, 32 * u.S * nws * u.ksplit, smem_u, st, u, B.Z,
                                B.Z, B.P);
@@ -984,10 +1000,13 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     // Independent halves of a batch on two streams: the latency-bound block
     // RQ of one half overlaps the FP64-bound window update of the other.
-    // (the two-level sweep's persistent far-row kernel owns every SM, so it
-    // runs on one stream; the one-level sweep overlaps two halves)
+    // (the persistent far-row kernel -- two-level sweep, and the one-level
+    // m = 20 update -- owns every SM, so it runs on one stream; otherwise
+    // two halves overlap)
     const char* sv = getenv("SS_STREAMS");
-    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : (two_level ? 1 : 2);
+    const bool far_m20 = !two_level && tile.exact && tile.G == 2 && tile.C == 5 &&
+                         (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2 && !getenv("SS_UPDATE_CLASSIC");
+    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : ((two_level || far_m20) ? 1 : 2);
     if (sb_max < 64) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
