@@ -46,7 +46,13 @@ __device__ __forceinline__ int far_pan_index(int row) {
 // NCB pairs (pair cbk owns columns [cbk G C, (cbk + 1) G C)); the group shares
 // the unit's stage (P for all m columns, the 64 x m Z tile: every pair's Z2
 // part needs all m state columns).
-template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB = 1>
+//
+// MSH (m = 1 only): the M = G C NCB "columns" of a unit are M different
+// shifts (one state column each); the stage holds their P vectors [q][nb+1]
+// and Z tiles [q][TILE], the Z2 part is the per-shift scalar W22 and the
+// lazy-shift correction uses each column's own sigma.  Turns the
+// LSU-bound one-column update of config 3 into the m = 10 register tile.
+template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB = 1, bool MSH = false>
 __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     k_far(UpdDims u, double2* Z, const double2* __restrict__ Pbuf) {
     constexpr int RG = 32 / G, MB = G * C, M = MB * NCB, TILE = RG * R;
@@ -68,7 +74,8 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     const size_t stage_el = (size_t)nc * m + (size_t)m * TILE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ntiles = (r0 - u.rlo + TILE - 1) / TILE;
-    const int64_t units = (int64_t)ntiles * sb;
+    const int su = MSH ? (sb + M - 1) / M : sb;  // units per row tile
+    const int64_t units = (int64_t)ntiles * su;
     const int64_t ua = units * blockIdx.x / gridDim.x, ub = units * (blockIdx.x + 1) / gridDim.x;
     const int nun = (int)(ub - ua);
 
@@ -119,18 +126,30 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
 #pragma unroll
                     for (int q = 0; q < NST; ++q) last[q] = (q == s) ? k : last[q];
                     const int64_t unit = ua + k;
-                    const int tile = (int)(unit / sb), l = (int)(unit - (int64_t)tile * sb);
+                    const int tile = (int)(unit / su), l = (int)(unit - (int64_t)tile * su);
                     const int i0 = u.rlo + tile * TILE;
                     const unsigned zbytes = (unsigned)(min(TILE, r0 - i0) * 16);
                     double2* st = Stg + (size_t)s * stage_el;
-                    const double2* pl = Pbuf + (int64_t)l * u.pstride;
-                    mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
-                    tma_bulk_g2s(st, pl + u.p12off, p12bytes, full + s);
-                    if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
                     double2* zt = st + (size_t)nc * m;
-                    for (int c = 0; c < m; ++c)
-                        tma_bulk_g2s(zt + c * TILE, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
-                                     full + s);
+                    if (MSH) {
+                        const int nq = min(M, sb - l * M);
+                        const unsigned pq = (unsigned)((ZID ? nb : nb + 1) * 16);
+                        mbar_expect_tx(full + s, (unsigned)nq * (pq + zbytes));
+                        for (int q = 0; q < nq; ++q) {
+                            const int64_t lq = (int64_t)l * M + q;
+                            tma_bulk_g2s(st + (size_t)q * nc, Pbuf + lq * u.pstride + u.p12off, pq,
+                                         full + s);
+                            tma_bulk_g2s(zt + q * TILE, Z + lq * u.LDZ + i0, zbytes, full + s);
+                        }
+                    } else {
+                        const double2* pl = Pbuf + (int64_t)l * u.pstride;
+                        mbar_expect_tx(full + s, p12bytes + p22bytes + (unsigned)m * zbytes);
+                        tma_bulk_g2s(st, pl + u.p12off, p12bytes, full + s);
+                        if (!ZID) tma_bulk_g2s(st + (size_t)nb * m, pl + u.p22off, p22bytes, full + s);
+                        for (int c = 0; c < m; ++c)
+                            tma_bulk_g2s(zt + c * TILE, Z + ((int64_t)l * m + c) * u.LDZ + i0, zbytes,
+                                         full + s);
+                    }
                     next[p] = k + NG;
                     --left;
                     any = true;
@@ -146,12 +165,12 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
     const int grp = pair / NCB, cbk = pair - grp * NCB;
     const int rg = lane / G, q = lane - rg * G;
     const int cb = cbk * MB + q * C;  // first output column of this lane
-    const int dlo = r0 - m;
+    const int dlo = r0 - (MSH ? 1 : m);
     const int jlo = half == 0 ? 0 : u.jh;
     const int jhi = half == 1 ? nb : u.jh;
     const double* pan_l = Pan + rg * 2;
     int npair = 0;  // units this pair has processed (mbarrier phase of zfree / partr)
-    const int tfirst = (int)(ua / sb), tlast = (int)((ub - 1) / sb);
+    const int tfirst = (int)(ua / su), tlast = (int)((ub - 1) / su);
     for (int tile = tfirst; tile <= tlast; ++tile) {
         // (re)stage the panel tile: every consumer is done with the old one
         asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * NPAIR) : "memory");
@@ -175,9 +194,9 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
         }
         asm volatile("bar.sync 1, %0;" ::"r"(32 * 2 * NPAIR) : "memory");
         // this tile's units of the CTA range: k in [ka, kb); pair p takes k = p mod 4
-        const int ka = (int)(max(ua, (int64_t)tile * sb) - ua);
-        const int kb = (int)(min(ub, (int64_t)(tile + 1) * sb) - ua);
-        const int l0t = (int)(ua + ka - (int64_t)tile * sb) - ka;  // l = l0t + k
+        const int ka = (int)(max(ua, (int64_t)tile * su) - ua);
+        const int kb = (int)(min(ub, (int64_t)(tile + 1) * su) - ua);
+        const int l0t = (int)(ua + ka - (int64_t)tile * su) - ka;  // l = l0t + k
         for (int k = ka + (((grp - ka) % NG) + NG) % NG; k < kb; k += NG) {
         const int l = l0t + k;
         const int i0 = u.rlo + tile * TILE;
@@ -199,6 +218,15 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
                 for (int c = 0; c < C; ++c)
 #pragma unroll
                     for (int r = 0; r < R; ++r) acc[r][c] = Zs[(cb + c) * TILE + rg + RG * r];
+            } else if (MSH) {
+                // per-shift scalar W22
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const double2 w22 = st[(cb + c) * nc + nb];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        acc[r][c] = cmul(Zs[(cb + c) * TILE + rg + RG * r], w22);
+                }
             } else {
                 for (int j = 0; j < m; ++j) {
                     double2 z[R];
@@ -226,7 +254,7 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                const double2 pv = Pl[j * m + c];
+                const double2 pv = MSH ? st[(cb + c) * nc + j] : Pl[j * m + c];
 #pragma unroll
                 for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
             }
@@ -249,6 +277,29 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
             for (int r = 0; r < R; ++r)
 #pragma unroll
                 for (int c = 0; c < C; ++c) acc[r][c] = cadd(acc[r][c], red[(r * C + c) * 32]);
+            if (MSH) {
+                // column c is shift l M + cb + c (state column 0)
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const int64_t lq = (int64_t)l * M + cb + c;
+                    if (lq >= sb) continue;
+                    const double2 sgq = u.shifts[lq];
+                    double2* zq = Z + lq * u.LDZ + i0 + rg;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int row = i0 + rg + RG * r;
+                        if (!interior && row >= r0) continue;
+                        double2 v = acc[r][c];
+                        if (!interior && row == dlo && u.mnb > 0)
+                            v = csub(v, cmul(sgq, st[(cb + c) * nc]));
+                        zq[RG * r] = v;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+                ++npair;
+                continue;
+            }
             const double2 sig = u.shifts[l];
             double2* zo = Z + ((int64_t)l * m + cb) * u.LDZ + i0 + rg;
             if (interior) {

@@ -396,15 +396,15 @@ int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, co
     return launch_update_ws_z<G, C, false>(h, grid, smem, st, u, zin, zout, pbuf);
 }
 
-template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB>
+template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB, bool MSH = false>
 int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                  const double2* pbuf) {
     static bool configured = false;
     if (!configured) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID, NCB>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID, NCB, MSH>));
         configured = true;
     }
-    k_far<G, C, R, NPAIR, NST, ZID, NCB><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
+    k_far<G, C, R, NPAIR, NST, ZID, NCB, MSH><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -413,6 +413,7 @@ int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const Upd
 // tile of (32/G) R rows; NPAIR consumer pairs; NST ring stages.
 struct FarShape {
     int G, C, R, NPAIR, NST, NCB;
+    bool MSH = false;  // m = 1: the G C columns are G C different shifts
     int tile() const { return (32 / G) * R; }
     int m() const { return G * C * NCB; }
 };
@@ -428,7 +429,8 @@ FarShape far_shape(const UpdTile& t) {
 int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStream_t st,
                const UpdDims& u, double2* z, const double2* pbuf) {
 #define SS_FAR(GG, CC, RR, NP, NS, KB)                                                           \
-    if (f.G == GG && f.C == CC && f.R == RR && f.NPAIR == NP && f.NST == NS && f.NCB == KB)      \
+    if (!f.MSH && f.G == GG && f.C == CC && f.R == RR && f.NPAIR == NP && f.NST == NS &&         \
+        f.NCB == KB)                                                                             \
         return u.zid ? launch_far_z<GG, CC, RR, NP, NS, true, KB>(h, grid, smem, st, u, z, pbuf)  \
                      : launch_far_z<GG, CC, RR, NP, NS, false, KB>(h, grid, smem, st, u, z, pbuf);
     SS_FAR(2, 5, 4, 4, 8, 1) SS_FAR(2, 5, 4, 3, 6, 1) SS_FAR(2, 5, 4, 4, 4, 2)
@@ -436,6 +438,9 @@ int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStrea
     SS_FAR(1, 1, 2, 4, 8, 1) SS_FAR(1, 2, 2, 4, 8, 1) SS_FAR(1, 3, 2, 4, 8, 1) SS_FAR(1, 4, 2, 4, 8, 1)
     SS_FAR(1, 5, 2, 4, 8, 1) SS_FAR(1, 6, 2, 4, 8, 1) SS_FAR(1, 7, 2, 4, 8, 1) SS_FAR(1, 8, 2, 4, 8, 1)
 #undef SS_FAR
+    if (f.MSH && f.G == 2 && f.C == 5 && f.R == 4 && f.NPAIR == 4 && f.NST == 8 && f.NCB == 1)
+        return u.zid ? launch_far_z<2, 5, 4, 4, 8, true, 1, true>(h, grid, smem, st, u, z, pbuf)
+                     : launch_far_z<2, 5, 4, 4, 8, false, 1, true>(h, grid, smem, st, u, z, pbuf);
     return SS_EARG;
 }
 
@@ -778,6 +783,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         ev = ss::timing_begin(h, st);
         int rc;
         const bool ws = nws == 1 && tile.exact && tile.G * tile.C == m && !getenv("SS_UPDATE_CLASSIC") &&
+                        !(m == 1 && !getenv("SS_NO_MSH")) &&
                         ws_smem_bytes(s.nb, m) + 1024 <= h->smem_optin;
         if (ws) {
             // warp-specialised pipeline: 1 producer + 4 consumer pairs, SG shifts per CTA
@@ -788,6 +794,23 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
             rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z, B.Z,
                                   B.P);
+        } else if (m == 1 && !getenv("SS_UPDATE_CLASSIC") && !getenv("SS_NO_MSH") &&
+                   far_smem_bytes(s.nb, 10, 64, 8) + 1024 <= h->smem_optin) {
+            // m = 1: ten shifts per unit as the ten columns of the m = 10 tile
+            FarShape f{2, 5, 4, 4, 8, 1};
+            f.MSH = true;
+            u.pstride = (int64_t)s.nc;  // nb + 1 complex per shift: P12 then the scalar P22
+            u.p12off = 0;
+            u.p22off = s.nb;
+            u.zid = 0;
+            u.flags = 0;
+            u.jh = std::max(0, std::min(s.nb, (s.nb - 2) / 2));
+            const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * ((sb + 9) / 10);
+            const int grid = (int)std::min<int64_t>(units, h->num_sms);
+            // the kernel's stage holds 10 "columns" of nc = nb + 1 entries
+            UpdDims um = u;
+            um.nc = s.nb + 1;
+            rc = launch_far(h, f, grid, far_smem_bytes(s.nb, 10, f.tile(), f.NST), st, um, B.Z, B.P);
         } else if (nws == 2 && tile.exact && tile.G == 2 && tile.C == 5 && !getenv("SS_UPDATE_CLASSIC") &&
                    far_smem_bytes(s.nb, m, 64, 4) + 1024 <= h->smem_optin) {
             // m = 20: persistent far kernel with two column blocks per unit
@@ -1006,7 +1029,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const char* sv = getenv("SS_STREAMS");
     const bool far_m20 = !two_level && tile.exact && tile.G == 2 && tile.C == 5 &&
                          (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2 && !getenv("SS_UPDATE_CLASSIC");
-    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : ((two_level || far_m20) ? 1 : 2);
+    const bool far_m1 = !two_level && m == 1 && !getenv("SS_UPDATE_CLASSIC") && !getenv("SS_NO_MSH");
+    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : ((two_level || far_m20 || far_m1) ? 1 : 2);
     if (sb_max < 64) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
