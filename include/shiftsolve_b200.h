@@ -70,6 +70,18 @@ int ss_tf_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t ld
                const double* shifts, int64_t s, int nb, int64_t batch, double rtol,
                double* G, int64_t ldg, int32_t* fail_row, void* stream);
 
+/* ss_tf_eval with Ahat in (pinned) host memory: Ahat is copied to the
+ * caller's device buffer Ahat_dev (n x n, lda_dev) on an internal copy
+ * stream in the order the sweep consumes its columns (the seed's last m
+ * columns, then one outer block / window at a time, right to left); each
+ * step waits only for its own columns, so the 8 n^2-byte transfer overlaps
+ * the sweep.  Everything else as ss_tf_eval (device B, C, shifts, G). */
+int ss_tf_eval_stream(ss_handle* h, int n, int m, int p, const double* Ahat_host,
+                      int64_t lda_host, double* Ahat_dev, int64_t lda_dev, const double* Bhat,
+                      int64_t ldb, const double* Chat, int64_t ldc, const double* shifts, int64_t s,
+                      int nb, int64_t batch, double rtol, double* G, int64_t ldg, int32_t* fail_row,
+                      void* stream);
+
 /* Structured pseudospectrum: ss_tf_eval (G into the caller's scratch G)
  * followed by a device epilogue norms[l] = ||G_l||_2 (p x m block; +inf for
  * a singular shift).  Replaces solvers.py:501-530 (two_norm_small's numpy

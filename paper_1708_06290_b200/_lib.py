@@ -19,7 +19,7 @@ SS_OK, SS_EDIM, SS_EARG, SS_ECUDA, SS_ENOMEM = 0, 1, 2, 3, 4
 #: every symbol include/shiftsolve_b200.h declares
 EXPORTED = (
     "ss_version", "ss_create", "ss_destroy", "ss_last_error", "ss_greedy_schedule",
-    "ss_tf_eval", "ss_pspec_eval", "ss_solve_reduced", "ss_solve_transposed", "ss_reduce_chf", "ss_set_timing", "ss_phase_stats",
+    "ss_tf_eval", "ss_tf_eval_stream", "ss_pspec_eval", "ss_solve_reduced", "ss_solve_transposed", "ss_reduce_chf", "ss_set_timing", "ss_phase_stats",
     "ss_reset_stats", "ss_launch_count", "ss_update_kernel_stats", "ss_probe_dfma_peak",
 )
 
@@ -56,6 +56,9 @@ def load():
         L.ss_solve_reduced.argtypes = [P, I, I, P, I64, P, I64, P, I64, P, I64, I, I64, D, P, I64,
                                        P, P]
         L.ss_solve_reduced.restype = I
+        L.ss_tf_eval_stream.argtypes = [P, I, I, I, P, I64, P, I64, P, I64, P, I64, P, I64, I, I64,
+                                        D, P, I64, P, P]
+        L.ss_tf_eval_stream.restype = I
         L.ss_pspec_eval.argtypes = [P, I, I, I, P, I64, P, I64, P, I64, P, I64, I, I64, D, P, I64,
                                     P, P, P]
         L.ss_pspec_eval.restype = I

@@ -65,6 +65,8 @@ struct ss_handle {
     int64_t launches = 0;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // fork / join events
     cudaStream_t aux_stream = nullptr;             // second stream of the sweep
+    cudaStream_t copy_stream = nullptr;            // streamed H2D of Ahat (ss_tf_eval_stream)
+    std::vector<cudaEvent_t> chunk_ev;             // one per streamed column chunk
     // deferred event timing (ss_set_timing): resolved by ss_phase_stats
     std::vector<cudaEvent_t> ev_pool;
     std::vector<ss::TimeRec> pending;

@@ -510,7 +510,40 @@ struct SweepArgs {
     double2* out;
     int64_t ldo;
     int32_t* fail;
+    // streamed Ahat (ss_tf_eval_stream): host source; A above is the device
+    // destination, filled chunk by chunk in sweep order on h->copy_stream
+    const double* A_host = nullptr;
+    int64_t lda_host = 0;
 };
+
+// Streamed-Ahat bookkeeping for one call: chunk c's event is recorded on the
+// copy stream after its columns landed; the compute stream waits on it right
+// before the first kernel that reads those columns.
+struct Feed {
+    bool on = false;
+    bool fro2_pending = false;  // ||A||_F / trace(A) after the last chunk
+    int next = 0;               // next chunk to wait for
+    int count = 0;
+};
+
+// Column chunks of Ahat in the order the sweep consumes them: the seed's last
+// m columns, then each outer block's (two-level) or window's panel columns.
+static void sweep_chunks(int n, int m, bool two_level, int nb0, std::vector<std::pair<int, int>>& out) {
+    out.clear();
+    out.push_back({n - m, n});
+    for (int k = n; k >= m + 1;) {
+        const int w = std::min(two_level ? kBlkNB : nb0, k - m);
+        out.push_back({k - m - w, k - m});
+        k -= w;
+    }
+}
+
+static int feed_wait(ss_handle* h, Feed& f, cudaStream_t st) {
+    if (!f.on || f.next >= f.count) return SS_OK;
+    SS_CUDA_TRY(h, cudaStreamWaitEvent(st, h->chunk_ev[f.next], 0));
+    ++f.next;
+    return SS_OK;
+}
 
 // Per-part device buffers: Z2 ping-pong + P for the part's shifts.
 struct PartBufs {
@@ -566,7 +599,7 @@ void account_ref_flops(ss_handle* h, int sb, int n, int m, int ptop, int nb0) {
 
 int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs B, int nb0,
                  int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, bool two_level,
-                 cudaStream_t st) {
+                 cudaStream_t st, Feed& feed) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : n;
     const int nws = (m + tile.G * tile.C - 1) / (tile.G * tile.C);  // warps per shift
@@ -583,6 +616,8 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     d.sb = sb;
     d.LDZ = LDZ;
     {
+        int rc = feed_wait(h, feed, st);  // the seed's last m columns
+        if (rc) return rc;
         dim3 g((unsigned)((LDZ + 255) / 256), (unsigned)sb);
         k_seed<<<g, 256, 0, st>>>(d, B.Z);
         SS_LAUNCH_CHECK(h);
@@ -606,8 +641,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             bd.shifts = d.shifts;
             bd.LDZ = LDZ;
             bd.wstride = wstride;
+            int rc = feed_wait(h, feed, st);  // this outer block's panel columns
+            if (rc) return rc;
             cudaEvent_t ev = ss::timing_begin(h, st);
-            int rc = launch_block(h, m, sb, blk_smem_bytes(m), st, bd, B.Z, B.P);
+            rc = launch_block(h, m, sb, blk_smem_bytes(m), st, bd, B.Z, B.P);
             if (rc) return rc;
             ss::timing_end(h, st, ev, ss::PH_RQ);
             const int rlo = a.mode == 1 ? bd.c0 : 0;
@@ -685,6 +722,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         s.rot = sc->d_rot;
         s.joff = sc->d_job_off;
         // ---- block RQ -> P (nc x m per shift, j-major) ----
+        {
+            int rc = feed_wait(h, feed, st);  // this window's panel columns
+            if (rc) return rc;
+        }
         cudaEvent_t ev = ss::timing_begin(h, st);
         if (use_house) {
             // one warp per shift: row-Householder block RQ (ss_rq_house.cuh)
@@ -845,6 +886,13 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     ho.out = a.mode == 0 ? a.out + lo * m * a.ldo : a.out + lo * a.ldo;
     ho.ldo = a.ldo;
     ho.fail = a.fail + lo;
+    if (feed.on && feed.fro2_pending) {
+        // streamed Ahat: all chunks are in (the last wait came with the last
+        // window); the pivot tolerances need ||A||_F and trace(A)
+        int rc = ss::fro2_trace(h, n, a.A, a.lda, st);
+        if (rc) return rc;
+        feed.fro2_pending = false;
+    }
     cudaEvent_t evh = ss::timing_begin(h, st);
     const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
     k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z);
@@ -989,18 +1037,45 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // the Householder block RQ maps one block row to one thread of two warps
     const int nb0 = use_house ? std::min(nb0_req, 64) : nb0_req;
 
-    // fro2 / trace for the per-shift singularity thresholds
-    {
-        int rc = ss::fro2_trace(h, n, a.A, a.lda, st);
-        if (rc) return rc;
-    }
-
     // two-level sweep (ss_block.cuh) when the fused block kernel and the
     // warp-specialised far update cover m; SS_ONE_LEVEL=1 forces the
     // per-window sweep
     const bool two_level = use_house && block_supported(m) && tile.exact && tile.G * tile.C == m &&
                            !getenv("SS_ONE_LEVEL") && !getenv("SS_UPDATE_CLASSIC") &&
                            ws_smem_bytes(64, m) + 1024 <= h->smem_optin;
+    // fro2 / trace for the per-shift singularity thresholds (streamed Ahat:
+    // after the last chunk, just before the first head)
+    Feed feed;
+    if (a.A_host) {
+        std::vector<std::pair<int, int>> chunks;
+        sweep_chunks(n, m, two_level, nb0, chunks);
+        if (!h->copy_stream)
+            SS_CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        while (h->chunk_ev.size() < chunks.size()) {
+            cudaEvent_t e;
+            SS_CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            h->chunk_ev.push_back(e);
+        }
+        // the destination may still be read by earlier work on st
+        SS_CUDA_TRY(h, cudaEventRecord(h->ev_a, st));
+        SS_CUDA_TRY(h, cudaStreamWaitEvent(h->copy_stream, h->ev_a, 0));
+        for (size_t c = 0; c < chunks.size(); ++c) {
+            const int c0 = chunks[c].first, c1 = chunks[c].second;
+            if (c1 > c0)
+                SS_CUDA_TRY(h, cudaMemcpy2DAsync(const_cast<double*>(a.A) + (int64_t)c0 * a.lda,
+                                                 (size_t)a.lda * 8, a.A_host + (int64_t)c0 * a.lda_host,
+                                                 (size_t)a.lda_host * 8, (size_t)n * 8, (size_t)(c1 - c0),
+                                                 cudaMemcpyHostToDevice, h->copy_stream));
+            SS_CUDA_TRY(h, cudaEventRecord(h->chunk_ev[c], h->copy_stream));
+        }
+        feed.on = true;
+        feed.fro2_pending = true;
+        feed.count = (int)chunks.size();
+    } else {
+        int rc = ss::fro2_trace(h, n, a.A, a.lda, st);
+        if (rc) return rc;
+    }
+
     // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
     const int64_t pst = two_level ? (int64_t)(kBlkNB + m) * m : (int64_t)ncmax * m;
@@ -1031,7 +1106,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
                          (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2 && !getenv("SS_UPDATE_CLASSIC");
     const bool far_m1 = !two_level && m == 1 && !getenv("SS_UPDATE_CLASSIC") && !getenv("SS_NO_MSH");
     int NS = sv ? std::max(1, std::min(2, atoi(sv))) : ((two_level || far_m20 || far_m1) ? 1 : 2);
-    if (sb_max < 64) NS = 1;
+    if (sb_max < 64 || feed.on) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
         if (!h->aux_stream) SS_CUDA_TRY(h, cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
@@ -1049,7 +1124,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             B.Z = Z0 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * pst;
             int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, tile,
-                                  two_level, streams[p]);
+                                  two_level, streams[p], feed);
             if (rc) return rc;
             off += cnt;
         }
@@ -1099,6 +1174,43 @@ int ss_tf_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t ld
     a.s = s;
     a.bd = nullptr;
     a.ldbd = 0;
+    a.nb = nb;
+    a.batch = batch;
+    a.rtol = rtol;
+    a.out = (double2*)G;
+    a.ldo = ldg > 0 ? ldg : 1;
+    a.fail = fail_row;
+    return run_sweep(h, a, (cudaStream_t)stream);
+}
+
+int ss_tf_eval_stream(ss_handle* h, int n, int m, int p, const double* Ahat_host,
+                      int64_t lda_host, double* Ahat_dev, int64_t lda_dev, const double* Bhat,
+                      int64_t ldb, const double* Chat, int64_t ldc, const double* shifts, int64_t s,
+                      int nb, int64_t batch, double rtol, double* G, int64_t ldg, int32_t* fail_row,
+                      void* stream) {
+    if (!h) return SS_EARG;
+    if (n < 1 || m < 1 || m > n || p < 0 || s < 0)
+        return ss::set_err(h, SS_EDIM, "inconsistent controller-Hessenberg form");
+    if (lda_host < n || lda_dev < n || ldb < m || (p > 0 && ldc < p) || (p > 0 && ldg < p))
+        return ss::set_err(h, SS_EDIM, "leading dimension too small");
+    if (nb < 1) return ss::set_err(h, SS_EARG, "window block size must be >= 1");
+    if (s > 0 && (!Ahat_host || !Ahat_dev || !Bhat || !shifts || !fail_row || (p > 0 && (!Chat || !G))))
+        return ss::set_err(h, SS_EARG, "null pointer");
+    SweepArgs a{};
+    a.mode = 0;
+    a.n = n;
+    a.m = m;
+    a.p = p;
+    a.A = Ahat_dev;
+    a.lda = lda_dev;
+    a.A_host = Ahat_host;
+    a.lda_host = lda_host;
+    a.B = Bhat;
+    a.ldb = ldb;
+    a.C = Chat;
+    a.ldc = ldc > 0 ? ldc : 1;
+    a.shifts = (const double2*)shifts;
+    a.s = s;
     a.nb = nb;
     a.batch = batch;
     a.rtol = rtol;

@@ -112,8 +112,17 @@ def eval_transfer_function(chf: ControllerHessForm, shifts, nb: int = 32,
     s = len(shifts)
     host = all(D.is_host(a) for a in (chf.Ahat, chf.Bhat, chf.Chat, shifts))
     dev = D.device_of(chf.Ahat, chf.Bhat, chf.Chat, shifts)
+    # A column-major, pinned host Ahat is streamed to the device in the order
+    # the sweep consumes its columns (right to left, one outer block at a
+    # time) on a copy stream, overlapped with the sweep (ss_tf_eval_stream)
+    Ah = chf.Ahat
+    stream_a = (isinstance(Ah, torch.Tensor) and Ah.device.type == "cpu" and Ah.is_pinned()
+                and Ah.dtype == torch.float64 and Ah.stride(0) == 1 and Ah.stride(1) >= n)
     with torch.cuda.device(dev):
-        A = D.fmat(chf.Ahat, torch.float64, dev)
+        if stream_a:
+            A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+        else:
+            A = D.fmat(Ah, torch.float64, dev)
         B = D.fmat(chf.Bhat, torch.float64, dev)
         C = D.fmat(chf.Chat, torch.float64, dev)
         sh = D.fvec(shifts, torch.complex128, dev)
@@ -122,9 +131,15 @@ def eval_transfer_function(chf: ControllerHessForm, shifts, nb: int = 32,
         h = _lib.handle(dev.index)
         L = _lib.load()
         with D.timed_call(h, counter):
-            rc = L.ss_tf_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C),
-                              D.ld(C), D.ptr(sh), s, int(nb), _batch(batch_size), rtol,
-                              D.ptr(G), max(p, 1), D.ptr(fail), D.stream_ptr(dev))
+            if stream_a:
+                rc = L.ss_tf_eval_stream(h.ptr, n, m, p, Ah.data_ptr(), Ah.stride(1), D.ptr(A), n,
+                                         D.ptr(B), D.ld(B), D.ptr(C), D.ld(C), D.ptr(sh), s,
+                                         int(nb), _batch(batch_size), rtol, D.ptr(G), max(p, 1),
+                                         D.ptr(fail), D.stream_ptr(dev))
+            else:
+                rc = L.ss_tf_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C),
+                                  D.ld(C), D.ptr(sh), s, int(nb), _batch(batch_size), rtol,
+                                  D.ptr(G), max(p, 1), D.ptr(fail), D.stream_ptr(dev))
         D.check(h, rc)
         failures = _failures(fail)
     Gout = G.cpu().numpy() if host else G

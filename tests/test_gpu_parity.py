@@ -456,3 +456,22 @@ def test_pseudospectrum_epilogue_vs_svd(n, m, p):
     v2 = ss.structured_pseudospectrum_grid(chf, np.array([ev[0], grid[0]]), nb=32)
     assert np.isinf(v2[0]) or v2[0] > 1e4 * np.median(ref)
     assert abs(v2[1] - ref[0]) <= 1e-12 * ref[0]
+
+
+@pytest.mark.parametrize("n,m,p,bs", [(517, 10, 3, None), (300, 5, 2, 7), (260, 1, 1, None),
+                                      (333, 20, 4, 5)])
+def test_streamed_host_ahat_bitwise(n, m, p, bs):
+    """A pinned, column-major host Ahat is streamed to the device chunk by
+    chunk in sweep order (ss_tf_eval_stream); results are bitwise those of
+    the device-resident call (two-level and one-level paths, several
+    batches)."""
+    chf = _mhess_triple(n, m, p, seed=7 * n + m)
+    shifts = 1j * np.logspace(-1, 1, 23) * np.sqrt(n) + 0.3
+    ref = ss.eval_transfer_function(chf, shifts, nb=64, batch_size=bs).G
+    Ah = torch.from_numpy(np.asfortranarray(chf.Ahat)).t().contiguous().t().pin_memory()
+    assert Ah.is_pinned() and Ah.stride(0) == 1
+    chf_h = ss.ControllerHessForm(Ahat=Ah, Bhat=torch.from_numpy(chf.Bhat).pin_memory(),
+                                  Chat=torch.from_numpy(chf.Chat).pin_memory(), m=m, n=n, p=p)
+    sh = torch.from_numpy(shifts).pin_memory()
+    res = ss.eval_transfer_function(chf_h, sh, nb=64, batch_size=bs)
+    assert np.array_equal(np.asarray(res.G), ref)
