@@ -152,8 +152,9 @@ template <int M, int NSW>
 __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
     k_block(BlkDims d, double2* __restrict__ Z, double2* __restrict__ W, int sb) {
     constexpr int L = M + 1;
-    constexpr int HW = 6;  // window entries per lane of a column pair (L <= 12)
-    static_assert(L <= 2 * HW, "k_block: m <= 11");
+    constexpr int HW = (L + 1) / 2;  // window entries per lane of a column pair
+    constexpr int CR = 16;           // columns per reverse-accumulation round (2 lanes each)
+    static_assert(L <= 32, "k_block: m <= 31");
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int PSZ = (kBlkInner + M) * M, USZ = kBlkInner * L;
     constexpr int QSZ = PSZ + USZ + kBlkInner + 64 + M * M;  // complex per shift
@@ -282,9 +283,11 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
             __syncwarp();
         }
         // ---------------- reverse accumulation -> P (j-major) ----------------
-        if (lane < 2 * M) {
-            const unsigned pm = 0x000fffffu >> (20 - 2 * M);
-            const int c = lane >> 1, hh = lane & 1, base = hh * HW;
+        for (int cr = 0; cr < M; cr += CR)
+        if (lane < 2 * min(CR, M - cr)) {
+            const int ncr = min(CR, M - cr);
+            const unsigned pm = ncr == 16 ? 0xffffffffu : ((1u << (2 * ncr)) - 1u);
+            const int c = cr + (lane >> 1), hh = lane & 1, base = hh * HW;
             double2 w[NSW][HW];
 #pragma unroll
             for (int q = 0; q < NSW; ++q)

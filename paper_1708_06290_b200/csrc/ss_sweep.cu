@@ -567,7 +567,7 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
             <<<(sb + kBlkShiftsPerWarp - 1) / kBlkShiftsPerWarp, 32, smem, st>>>(bd, Z, W, sb); \
         break;                                                            \
     }
-        SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) SS_CASE(10)
+        SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) SS_CASE(10) SS_CASE(20)
 #undef SS_CASE
         default: return ss::set_err(h, SS_EARG, "two-level sweep: unsupported m");
     }
@@ -577,7 +577,7 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
 
 // m < 4: the per-window overhead 2m/nb is already < 13% at nb = 64 and the
 // one-level sweep measured faster (config 3, m = 1: 13.7 vs 19.3 ms)
-bool block_supported(int m) { return (m >= 4 && m <= 8) || m == 10; }
+bool block_supported(int m) { return (m >= 4 && m <= 8) || m == 10 || m == 20; }
 
 // Reference phase flops of the window sweep at block size nb0 (shape only:
 // batched.py:58-61, solvers.py:186-199), independent of how the device
@@ -692,7 +692,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (getenv("SS_FAR_CLASSIC")) {
                     rc = launch_update_ws(h, tile, gw, ws_smem_bytes(nbp, m), st, u, B.Z, B.Z, B.P);
                 } else {
-                    const FarShape f = far_shape(tile);
+                    const FarShape f = m == 20 ? FarShape{2, 5, 4, 4, 4, 2} : far_shape(tile);
                     const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * sb;
                     const int grid = (int)std::min<int64_t>(units, h->num_sms);
                     rc = launch_far(h, f, grid, far_smem_bytes(nbp, m, f.tile(), f.NST), st, u, B.Z,
@@ -1040,9 +1040,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // two-level sweep (ss_block.cuh) when the fused block kernel and the
     // warp-specialised far update cover m; SS_ONE_LEVEL=1 forces the
     // per-window sweep
-    const bool two_level = use_house && block_supported(m) && tile.exact && tile.G * tile.C == m &&
+    // (m = 20: the far passes run k_far with two column blocks per unit)
+    const bool two_level = use_house && block_supported(m) && tile.exact &&
+                           (tile.G * tile.C == m || (m == 20 && tile.G == 2 && tile.C == 5)) &&
                            !getenv("SS_ONE_LEVEL") && !getenv("SS_UPDATE_CLASSIC") &&
-                           ws_smem_bytes(64, m) + 1024 <= h->smem_optin;
+                           far_smem_bytes(64, m, 64, m == 20 ? 4 : 8) + 1024 <= h->smem_optin;
     // fro2 / trace for the per-shift singularity thresholds (streamed Ahat:
     // after the last chunk, just before the first head)
     Feed feed;

@@ -388,7 +388,8 @@ def _mhess_triple(n, m, p, seed):
 
 
 @pytest.mark.parametrize("n,m,p", [(300, 10, 10), (517, 10, 3), (161, 1, 1), (40, 5, 2),
-                                   (389, 2, 4), (455, 3, 3), (260, 7, 5), (700, 8, 8), (129, 4, 1)])
+                                   (389, 2, 4), (455, 3, 3), (260, 7, 5), (700, 8, 8), (129, 4, 1),
+                                   (333, 20, 4), (700, 20, 20), (61, 20, 3)])
 def test_two_level_vs_one_level(n, m, p, monkeypatch):
     """The two-level sweep (k_block + k_far over 128-column outer blocks, the
     default for m in 1..8, 10) against the per-window sweep (SS_ONE_LEVEL=1)
