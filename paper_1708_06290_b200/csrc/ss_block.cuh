@@ -6,26 +6,25 @@
 // 4 m nb (real panel x P12) + 8 m^2 (state x P22) flops, so the state part is
 // a 2m/nb overhead on the algorithmic work -- 31% at nb = 64, m = 10.
 //
-// Here the windows are grouped into outer blocks of NB = 128 columns.  One
-// CTA per shift runs the NB/32 inner windows (nb = 32) of an outer block
-// entirely on chip:
-//   * the block rows [r0_out, r0_out + NBo) of the state live in registers,
-//     one row per thread (128 threads);
-//   * inner step i: warp 3-i owns the inner block's 32 rows and factors it
-//     with row Householder reflectors (same scheme and sign rule as
-//     ss_rq_house.cuh / kernels.py:74-99), then forms P_i by reverse
-//     accumulation (lanes = columns);
-//   * every thread then applies P_i to its row: rows above the inner block
-//     get state <- state P22 + A(row, inner cols) P12 - sigma P12[lazy row]
-//     (solvers.py:186-199 restricted to the block); the inner block's own rows
-//     are finished and their registers are reused for rows of the composite
+// Here the windows are grouped into outer blocks of NB = 128 columns; per
+// outer block one kernel per shift (k_block below, one warp per shift so all
+// shifts' serial reflector chains are resident at once) runs the NB/32 inner
+// windows (nb = 32):
+//   * inner window i (rows [b, b + 32) of the block, lane = row): row
+//     Householder chain (same scheme and sign rule as ss_rq_house.cuh /
+//     kernels.py:74-99), then P_i by reverse accumulation (a lane pair per
+//     column, in rounds of 16 columns);
+//   * P_i is applied row pass by row pass: rows above the inner window get
+//     state <- state P22 + A(row, inner cols) P12 - sigma P12[lazy row]
+//     (solvers.py:186-199 restricted to the block); the window's own rows
+//     are finished and become rows of the composite
 //         W <- E_b P12 + W P22,    W = [W_panel (NBo x m); W22 (m x m)]
 //     so that after the outer block the far rows [0, r0_out) need ONE update
 //         state <- state W22 + Pan(:, outer cols) W_panel - sigma W[lazy row]
-//     (done by k_update_ws in 64-column passes, the first with W22, the rest
+//     (k_far, ss_far.cuh, in 64-column passes: the first with W22, the rest
 //     with the identity).  The state overhead on the far rows drops to 2m/NB.
-// Only W ((NBo + m) x m per shift, j-major) leaves the kernel; the outer
-// block's rows are finished (part of R, never needed again).
+// The block's state rows stay in the (L2-resident) window buffer between
+// phases; only W ((NBo + m) x m per shift, j-major) is the kernel's product.
 #pragma once
 
 #include "ss_rq_house.cuh"

@@ -11,19 +11,24 @@
 // then the m x m head is reduced and back-substituted (solvers.py:204-231)
 // and G_l = -Chat X (or x_l = Q X for the reduced solve).
 //
-// B200 mapping ("streamed" path: per-shift window state in HBM/L2):
+// B200 mapping (per-shift window state in HBM/L2, updated in place):
 //   k_seed      one pass writing Z2 for all shifts of a batch
-//   k_rq        one CTA per shift per step: block packed in shared memory,
-//               greedy-schedule Givens with one warp per rotation, P_l by
-//               reverse accumulation (O(K m) instead of O(K (nb+m)))
-//   k_update    the dominant FP64 kernel: a CTA owns a 64-row tile of the
-//               real panel (staged once in shared memory, reused by every
-//               shift of its group) and streams each shift's Z2 rows through
-//               registers; 2 rows x CC columns complex register tile per
-//               thread, P_l broadcast from shared memory
+//   two-level sweep (m in 4..8, 10, 20), per outer block of 128 columns:
+//     k_block   one warp per shift: the four 32-row inner windows (Householder
+//               chain, reverse accumulation, in-block row passes) -> the
+//               composite W (ss_block.cuh)
+//     k_far     persistent, warp-specialised (TMA bulk copies + mbarrier ring)
+//               far-row update from W in two 64-column passes (ss_far.cuh)
+//   one-level sweep (other m), per window of nb columns:
+//     k_rq_house / k_rq   block RQ (row Householder; the reference's scheduled
+//               Givens batch for m + 1 > 32) -> P_l
+//     k_far (m = 1: ten shifts per unit; m = 20) / k_update_ws / k_update
+//               the window update of rows [0, r0)
 //   k_head      one CTA per shift: m x m head RQ fused with the triangular
 //               solve and the -Chat X (or Q X) epilogue; only G / x leave
 //               the device.
+// ss_tf_eval_stream additionally streams Ahat from pinned host memory in the
+// order the sweep consumes its columns (copy stream + one event per chunk).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -681,7 +686,8 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 // DFMA per column of m unless it is the identity) and the epilogue
                 u.jh = u.zid ? nbp / 2 : std::max(0, std::min(nbp, (nbp - 2 * m) / 2 - 1));
                 u.flags = 0;
-                if (const char* e = getenv("SS_FAR_JH")) u.jh = std::max(0, std::min(nbp, u.jh + atoi(e)));
+                if (const char* e = getenv(u.zid ? "SS_FAR_JH1" : "SS_FAR_JH"))
+                    u.jh = std::max(0, std::min(nbp, u.jh + atoi(e)));
                 if (getenv("SS_FAR_SPIN")) u.flags |= 1;
                 // algorithmic flops: every far panel row is structurally nonzero
                 const double nnz = ((a.mode == 0 ? (double)a.p : 0.0) + (double)(ko - NBo)) * nbp +
