@@ -58,35 +58,17 @@ __host__ __device__ inline size_t blk_smem_bytes_1(int m) {
     b += (size_t)m * m * 16;                // W22
     return b;
 }
+// The chain's staged panel rows (32 x 32 f64 per warp) alias P when P is
+// large enough (P of the previous inner window is dead during the chain).
+constexpr size_t kBlkPanelBytes = (size_t)kBlkInner * kBlkInner * 8;
+__host__ __device__ constexpr bool blk_panel_in_p(int m) {
+    return (size_t)(kBlkInner + m) * m * 16 >= kBlkPanelBytes;
+}
 
 constexpr int kBlkShiftsPerWarp = 1;  // 2 measured slower on B200 (per-warp issue bound)
 
 __host__ __device__ inline size_t blk_smem_bytes(int m) {
-    return kBlkShiftsPerWarp * blk_smem_bytes_1(m);
-}
-
-// Row update of the chain with FMA-chain dot products (two partial sums, no
-// add tree): z <- z - tau (z u) u^H over the L-column window.
-template <int L>
-__device__ __forceinline__ void blk_row_update(double2 (&z)[L], const double2* __restrict__ u,
-                                               double2 tau) {
-    double2 d0 = cz(), d1 = cz();
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-        const double2 uj = u[j];
-        double2& d = (j & 1) ? d1 : d0;
-        d.x = fma(z[j].x, uj.x, d.x);
-        d.x = fma(-z[j].y, uj.y, d.x);
-        d.y = fma(z[j].x, uj.y, d.y);
-        d.y = fma(z[j].y, uj.x, d.y);
-    }
-    const double2 tw = cmul(tau, cadd(d0, d1));
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-        const double2 uj = u[j];
-        z[j].x = fma(-tw.x, uj.x, fma(-tw.y, uj.y, z[j].x));
-        z[j].y = fma(-tw.y, uj.x, fma(tw.x, uj.y, z[j].y));
-    }
+    return kBlkShiftsPerWarp * blk_smem_bytes_1(m) + (blk_panel_in_p(m) ? 0 : kBlkPanelBytes);
 }
 
 // One warp per NSW shifts.  Block row t of the outer block is handled by
@@ -96,53 +78,10 @@ __device__ __forceinline__ void blk_row_update(double2 (&z)[L], const double2* _
 // so its values can stay in the (L2-resident) window buffer Z / the W output
 // between phases without cross-lane hazards.
 //
-// The reflector chain is a serial dependency: a warp running one shift's
-// chain is latency-bound (measured ~3.7 cycles per instruction).  Each warp
-// therefore carries NSW = 2 shifts through identical control flow (the row
-// mapping does not depend on the shift), so every phase issues two
-// independent instruction streams back to back and the second hides the
-// first's latencies; all shifts' chains stay resident (15 KB of shared
-// memory per shift).
+// The reflector chain is a serial dependency, so each warp runs one shift
+// (NSW = 1; two interleaved shifts per warp measured slower) and all shifts'
+// chains stay resident at once.
 //
-// NSW independent row updates with the shift index innermost, so the two
-// dependency chains interleave instruction by instruction.
-template <int L, int NSW>
-__device__ __forceinline__ void blk_row_update_n(double2 (&z)[NSW][L], double2* const (&U)[NSW],
-                                                 int off, const double2 (&tau)[NSW]) {
-    double2 d0[NSW], d1[NSW];
-#pragma unroll
-    for (int q = 0; q < NSW; ++q) d0[q] = d1[q] = cz();
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-#pragma unroll
-        for (int q = 0; q < NSW; ++q) {
-            const double2 uj = U[q][off + j];
-            double2& dd = (j & 1) ? d1[q] : d0[q];
-            dd.x = fma(z[q][j].x, uj.x, dd.x);
-            dd.y = fma(z[q][j].x, uj.y, dd.y);
-        }
-#pragma unroll
-        for (int q = 0; q < NSW; ++q) {
-            const double2 uj = U[q][off + j];
-            double2& dd = (j & 1) ? d1[q] : d0[q];
-            dd.x = fma(-z[q][j].y, uj.y, dd.x);
-            dd.y = fma(z[q][j].y, uj.x, dd.y);
-        }
-    }
-    double2 tw[NSW];
-#pragma unroll
-    for (int q = 0; q < NSW; ++q) tw[q] = cmul(tau[q], cadd(d0[q], d1[q]));
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-#pragma unroll
-        for (int q = 0; q < NSW; ++q) {
-            const double2 uj = U[q][off + j];
-            z[q][j].x = fma(-tw[q].x, uj.x, fma(-tw[q].y, uj.y, z[q][j].x));
-            z[q][j].y = fma(-tw[q].y, uj.x, fma(tw[q].x, uj.y, z[q][j].y));
-        }
-    }
-}
-
 // After the chain, P_i = H_{nbi-1}(...(H_0 E)) by reverse accumulation:
 // lane pair (2c, 2c+1) owns column c of P, each lane half of the sliding
 // L-window (6 entries), so a step is 6 complex dot terms + one shuffle
@@ -166,6 +105,8 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
     const int NBo = d.NBo;
     const int off = kBlkNB - NBo;  // rows are numbered from the top of a 128-row frame
     const double* Ab = d.A + (int64_t)d.c0 * d.lda;  // panel column 0
+    double* Apn = reinterpret_cast<double*>(reinterpret_cast<double2*>(smem) +
+                                            (blk_panel_in_p(M) ? 0 : NSW * QSZ));  // [32][32]
     double2 sig[NSW];
     double2* Zl[NSW];
     double2* Wl[NSW];
@@ -196,15 +137,26 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
         const int pass_rq = 3 - i;
         {
             // ---------------- reflector chains over the inner block ----------------
+            // Reflector of pivot row p (y = conj(p), alpha = y[L-1]) in the
+            // unnormalised form H = I - kappa v v^H, v = y - beta e_L,
+            // kappa = 1 / (beta (beta - conj(alpha))) (|beta - conj(alpha)| >=
+            // |beta| > 0, no cancellation): the same H as
+            // I - tau u u^H with u = v / (alpha - beta), tau = (beta - alpha) /
+            // beta (kernels.py:74-99's sign rule), but the row update needs only
+            // the broadcast pivot row and kappa, so each lane's dot product runs
+            // beside the rsqrt / reciprocal chain and no second broadcast (of u)
+            // sits on the serial path.  Rows not updated this step get tw = 0
+            // (z - 0 v = z exactly), so the update is branch-free.
             const int t = pass_rq * 32 + lane - off;  // this lane's block row
             const int rho = t - b;
             const bool mine = t >= 0 && rho >= 0;
             const int64_t arow = (int64_t)(d.k - NBo) + t;
+            // this lane's panel row over the inner window, staged once (all
+            // loads in flight together) instead of one dependent load per step
+            for (int c = 0; c < nbi; ++c) Apn[c * 32 + lane] = mine ? Ab[arow + (int64_t)(b + c) * d.lda] : 0.0;
             double2 z[NSW][L];  // window: z[0] = panel column, z[1..L) = state
-            double pf = 0.0;
             {
-                const double a0 = mine ? Ab[arow + (int64_t)(b + nbi - 1) * d.lda] : 0.0;
-                if (mine && nbi >= 2 && rho <= nbi - 2) pf = Ab[arow + (int64_t)(b + nbi - 2) * d.lda];
+                const double a0 = Apn[(nbi - 1) * 32 + lane];
 #pragma unroll
                 for (int q = 0; q < NSW; ++q) {
 #pragma unroll
@@ -221,62 +173,72 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
 #pragma unroll
                         for (int j = 0; j < L; ++j) Piv[q][pb + j] = z[q][j];
                 }
+                const double pf = ti > 0 ? Apn[(ti - 1) * 32 + lane] : 0.0;
                 __syncwarp();
-                double2 tau[NSW], scale[NSW];
-                double sq[NSW][L - 1];
-#pragma unroll
-                for (int j = 0; j < L - 1; ++j)
-#pragma unroll
-                    for (int q = 0; q < NSW; ++q) {
-                        const double2 x = Piv[q][pb + j];
-                        sq[q][j] = fma(x.x, x.x, x.y * x.y);
-                    }
-#pragma unroll
-                for (int w = 1; w < L - 1; w <<= 1)
-#pragma unroll
-                    for (int j = 0; j + w < L - 1; j += 2 * w)
-#pragma unroll
-                        for (int q = 0; q < NSW; ++q) sq[q][j] += sq[q][j + w];
+                const bool upd = mine && rho < ti;
 #pragma unroll
                 for (int q = 0; q < NSW; ++q) {
-                    // branch-free reflector (tau = 0 for an already-collapsed row)
-                    const double s2 = L > 1 ? sq[q][0] : 0.0;
-                    const double2 pv = Piv[q][pb + L - 1];
-                    const double2 alpha = make_double2(pv.x, -pv.y);  // conj: row -> reflector space
+                    double2 pv[L];
+#pragma unroll
+                    for (int j = 0; j < L; ++j) pv[j] = Piv[q][pb + j];
+                    // z . y over the first L-1 entries (two partial sums) and |y|^2
+                    double2 d0 = cz(), d1 = cz();
+                    double sq[L > 1 ? L - 1 : 1];
+#pragma unroll
+                    for (int j = 0; j < L - 1; ++j) {
+                        double2& dd = (j & 1) ? d1 : d0;  // z_j conj(p_j)
+                        dd.x = fma(z[q][j].x, pv[j].x, dd.x);
+                        dd.x = fma(z[q][j].y, pv[j].y, dd.x);
+                        dd.y = fma(z[q][j].y, pv[j].x, dd.y);
+                        dd.y = fma(-z[q][j].x, pv[j].y, dd.y);
+                        sq[j] = fma(pv[j].x, pv[j].x, pv[j].y * pv[j].y);
+                    }
+#pragma unroll
+                    for (int w = 1; w < L - 1; w <<= 1)
+#pragma unroll
+                        for (int j = 0; j + w < L - 1; j += 2 * w) sq[j] += sq[j + w];
+                    const double s2 = L > 1 ? sq[0] : 0.0;
+                    const double2 alpha = make_double2(pv[L - 1].x, -pv[L - 1].y);
                     const bool ident = s2 == 0.0 && alpha.y == 0.0;
                     const double nrm2 = ident ? 1.0 : fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
-                    const double rn = rsqrt(nrm2);
+                    const double rn = rsqrt_pos(nrm2);
                     const double sg = alpha.x >= 0.0 ? -1.0 : 1.0;
-                    const double beta = sg * nrm2 * rn;
-                    const double ib = sg * rn;
-                    const double zx = alpha.x - beta, zy = alpha.y;
-                    const double zz = fma(zx, zx, zy * zy);
-                    const double rz = rsqrt(zz > 0.0 ? zz : 1.0);
-                    const double iz = rz * rz;
-                    tau[q] = ident ? cz() : make_double2(1.0 - alpha.x * ib, -alpha.y * ib);
-                    scale[q] = ident ? cz() : make_double2(zx * iz, -zy * iz);
-                }
+                    const double beta = sg * nrm2 * rn, ib = sg * rn;  // beta, 1 / beta
+                    // kappa = (1 / beta) conj(beta - conj(alpha)) / |beta - conj(alpha)|^2
+                    const double zx = beta - alpha.x;
+                    const double f = ib * rcp_pos(fma(zx, zx, alpha.y * alpha.y));
+                    const double2 kap = ident ? cz() : make_double2(zx * f, -alpha.y * f);
+                    // rows not updated this step: kappa -> 0 (a select, so the
+                    // dot product stays unconditional and overlaps the chain)
+                    const double2 kup = upd ? kap : cz();
+                    const double2 vl = make_double2(alpha.x - beta, alpha.y);  // v[L-1]
+                    double2 dot = cadd(d0, d1);
+                    dot = cfma(z[q][L - 1], vl, dot);
+                    const double2 tw = cmul(kup, dot);
 #pragma unroll
-                for (int q = 0; q < NSW; ++q) {
+                    for (int j = 0; j < L - 1; ++j) {  // z_j -= tw conj(v_j) = tw p_j
+                        // wide windows re-read the pivot (register pressure)
+                        const double2 pj = L > 16 ? Piv[q][pb + j] : pv[j];
+                        z[q][j].x = fma(-tw.x, pj.x, fma(tw.y, pj.y, z[q][j].x));
+                        z[q][j].y = fma(-tw.x, pj.y, fma(-tw.y, pj.x, z[q][j].y));
+                    }
+                    z[q][L - 1].x = fma(-tw.x, vl.x, fma(-tw.y, vl.y, z[q][L - 1].x));
+                    z[q][L - 1].y = fma(tw.x, vl.y, fma(-tw.y, vl.x, z[q][L - 1].y));
+                    // v and kappa for the reverse accumulation (off the serial path)
                     if (lane < L) {
                         const double2 x = Piv[q][pb + lane];
-                        U[q][ti * L + lane] =
-                            lane < L - 1 ? cmul(make_double2(x.x, -x.y), scale[q]) : make_double2(1.0, 0.0);
+                        U[q][ti * L + lane] = lane < L - 1 ? make_double2(x.x, -x.y) : vl;
                     }
-                    if (lane == 0) Tau[q][ti] = tau[q];
+                    if (lane == 0) Tau[q][ti] = kap;
                 }
-                __syncwarp();
-                if (mine && rho < ti) blk_row_update_n<L, NSW>(z, U, ti * L, tau);
-                if (ti > 0) {
+                // slide (unconditionally: after the last step z is dead)
 #pragma unroll
-                    for (int q = 0; q < NSW; ++q) {
+                for (int q = 0; q < NSW; ++q) {
 #pragma unroll
-                        for (int j = L - 1; j > 0; --j) z[q][j] = z[q][j - 1];
-                        double2 v = make_double2(pf, 0.0);
-                        if (mine && rho + M == ti - 1) v = csub(v, sig[q]);
-                        z[q][0] = v;
-                    }
-                    if (mine && ti >= 2 && rho <= ti - 2) pf = Ab[arow + (int64_t)(b + ti - 2) * d.lda];
+                    for (int j = L - 1; j > 0; --j) z[q][j] = z[q][j - 1];
+                    double2 v = make_double2(pf, 0.0);
+                    if (mine && rho + M == ti - 1) v = csub(v, sig[q]);
+                    z[q][0] = v;
                 }
             }
             __syncwarp();
