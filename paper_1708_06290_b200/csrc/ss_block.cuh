@@ -46,6 +46,12 @@ struct BlkDims {
     const double2* shifts;
     int64_t LDZ;
     int64_t wstride;  // elements (complex) per shift in W
+    int woff;         // first W row of this block in the per-shift buffer
+    // paired outer blocks: > 0 = rows [kBlkNB, kBlkNB + wprod) of the buffer
+    // hold the previous (lower) block's W; they are multiplied in place by
+    // this block's W22 (the composite over both blocks) and this block's
+    // W22 rows are not written (ss_sweep.cu, enqueue_part)
+    int wprod;
 };
 
 __host__ __device__ inline size_t blk_smem_bytes_1(int m) {
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
         const int l = vq[q] ? lq : sb - 1;  // a missing partner shadows the last shift
         sig[q] = d.shifts[l];
         Zl[q] = Z + (int64_t)l * M * d.LDZ + d.r0;  // block row t, column c: Zl[c*LDZ + t]
-        Wl[q] = W + (int64_t)l * d.wstride;         // W row t, column c: Wl[t*M + c]
+        Wl[q] = W + (int64_t)l * d.wstride + (int64_t)d.woff * M;  // W row t, column c: Wl[t*M + c]
         for (int u = lane; u < M * M; u += 32)
             W22[q][u] = make_double2((u / M) == (u % M) ? 1.0 : 0.0, 0.0);
     }
@@ -400,6 +406,28 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
             }
         }
         __syncwarp();
+    }
+    if (d.wprod > 0) {
+        // composite of this block and the previous one: W_prev <- W_prev W22
+#pragma unroll
+        for (int q = 0; q < NSW; ++q) {
+            if (!vq[q]) continue;
+            double2* Wp = Wl[q] + (int64_t)(kBlkNB - d.woff) * M;
+            for (int row = lane; row < d.wprod; row += 32) {
+                double2 w[M], acc[M];
+#pragma unroll
+                for (int j = 0; j < M; ++j) w[j] = Wp[(int64_t)row * M + j];
+#pragma unroll
+                for (int c = 0; c < M; ++c) acc[c] = cz();
+#pragma unroll
+                for (int j = 0; j < M; ++j)
+#pragma unroll
+                    for (int c = 0; c < M; ++c) acc[c] = cfma(w[j], W22[q][j * M + c], acc[c]);
+#pragma unroll
+                for (int c = 0; c < M; ++c) Wp[(int64_t)row * M + c] = acc[c];
+            }
+        }
+        return;
     }
     // W22 rows [NBo, NBo + m)
 #pragma unroll

@@ -584,6 +584,13 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
 // one-level sweep measured faster (config 3, m = 1: 13.7 vs 19.3 ms)
 bool block_supported(int m) { return (m >= 4 && m <= 8) || m == 10 || m == 20; }
 
+// Paired outer blocks (composite W over 256 columns for the far rows);
+// SS_NO_PAIR=1 keeps one far update per 128-column block.
+static bool two_level_pairing(int m) {
+    (void)m;
+    return !getenv("SS_NO_PAIR");
+}
+
 // Reference phase flops of the window sweep at block size nb0 (shape only:
 // batched.py:58-61, solvers.py:186-199), independent of how the device
 // schedules the work.
@@ -630,32 +637,20 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     int k = two_level ? 0 : n;
     if (two_level) {
         // ---- two-level sweep: k_block per outer block, far rows from W ----
+        // Outer blocks are paired (A = the lower block, B the one above it):
+        // after k_block(A) only B's own rows get A's update ("near"); k_block
+        // (B) then folds A's W into the composite over both blocks, and the
+        // rows above B get ONE update from it -- the Z2 W22 part on the far
+        // rows is paid once per 256 columns instead of once per 128.
         account_ref_flops(h, sb, n, m, ptop, nb0);
-        const int64_t wstride = (int64_t)(kBlkNB + m) * m;
-        for (int ko = n; ko >= m + 1;) {
-            const int NBo = std::min(kBlkNB, ko - m);
-            BlkDims bd;
-            bd.m = m;
-            bd.ptop = ptop;
-            bd.k = ko;
-            bd.NBo = NBo;
-            bd.c0 = ko - m - NBo;
-            bd.r0 = ptop + ko - NBo;
-            bd.A = a.A;
-            bd.lda = a.lda;
-            bd.shifts = d.shifts;
-            bd.LDZ = LDZ;
-            bd.wstride = wstride;
-            int rc = feed_wait(h, feed, st);  // this outer block's panel columns
-            if (rc) return rc;
-            cudaEvent_t ev = ss::timing_begin(h, st);
-            rc = launch_block(h, m, sb, blk_smem_bytes(m), st, bd, B.Z, B.P);
-            if (rc) return rc;
-            ss::timing_end(h, st, ev, ss::PH_RQ);
-            const int rlo = a.mode == 1 ? bd.c0 : 0;
-            const int rows = bd.r0 - rlo;
-            for (int jb = 0; rows > 0 && jb < NBo; jb += 64) {
-                const int nbp = std::min(64, NBo - jb);
+        const bool pairing = two_level_pairing(m);
+        const int64_t wstride = (int64_t)((pairing ? 2 : 1) * kBlkNB + m) * m;
+        // far-row update of rows [rlo, r0) from the W rows [woff, woff + ncols
+        // + m) of the buffer, panel columns [c0, c0 + ncols), in 64-column passes
+        auto far_update = [&](int rlo, int r0, int c0, int ncols, int woff) -> int {
+            const int rows = r0 - rlo;
+            for (int jb = 0; rows > 0 && jb < ncols; jb += 64) {
+                const int nbp = std::min(64, ncols - jb);
                 UpdDims u;
                 u.n = n;
                 u.m = m;
@@ -669,16 +664,16 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 u.sb = sb;
                 u.LDZ = LDZ;
                 u.nb = nbp;
-                u.mnb = jb == 0 ? std::min(m, NBo) : 0;
-                u.r0 = bd.r0;
-                u.c0 = bd.c0 + jb;
+                u.mnb = jb == 0 ? std::min(m, ncols) : 0;
+                u.r0 = r0;
+                u.c0 = c0 + jb;
                 u.nc = nbp + m;
                 u.rlo = rlo;
                 u.nws = 1;
                 u.ksplit = 2;
                 u.pstride = wstride;
-                u.p12off = (int64_t)jb * m;
-                u.p22off = (int64_t)NBo * m;
+                u.p12off = (int64_t)(woff + jb) * m;
+                u.p22off = (int64_t)(woff + ncols) * m;
                 u.zid = jb == 0 ? 0 : 1;
                 u.S = 1;
                 u.SG = 32;
@@ -689,12 +684,24 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (const char* e = getenv(u.zid ? "SS_FAR_JH1" : "SS_FAR_JH"))
                     u.jh = std::max(0, std::min(nbp, u.jh + atoi(e)));
                 if (getenv("SS_FAR_SPIN")) u.flags |= 1;
-                // algorithmic flops: every far panel row is structurally nonzero
-                const double nnz = ((a.mode == 0 ? (double)a.p : 0.0) + (double)(ko - NBo)) * nbp +
-                                   (a.mode == 1 ? (double)nbp : 0.0);
+                // algorithmic flops: structurally nonzero panel entries of the
+                // far rows (Chat rows dense, identity rows one per column,
+                // Ahat rows above the band dense) x m complex columns
+                double nnz = 0.0;
+                const int top_hi = std::min(r0, ptop);
+                if (top_hi > rlo) {
+                    if (a.mode == 0) {
+                        nnz += (double)(top_hi - rlo) * nbp;
+                    } else {
+                        const int clo = std::max(rlo, u.c0), chi = std::min(top_hi, u.c0 + nbp);
+                        nnz += (double)std::max(0, chi - clo);
+                    }
+                }
+                if (r0 > std::max(rlo, ptop)) nnz += (double)(r0 - std::max(rlo, ptop)) * nbp;
                 const double fl_alg = 4.0 * m * nnz * sb;
                 dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
-                ev = ss::timing_begin(h, st);
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                int rc;
                 if (getenv("SS_FAR_CLASSIC")) {
                     rc = launch_update_ws(h, tile, gw, ws_smem_bytes(nbp, m), st, u, B.Z, B.Z, B.P);
                 } else {
@@ -709,7 +716,53 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 ss::timing_end(h, st, ev, ss::PH_UPDATE, u.zid ? 0.0 : 8.0 * rows * m * m * (double)sb,
                                8.0 * rows * (double)sb * m * nbp, fl_alg);
             }
-            ko -= NBo;
+            return SS_OK;
+        };
+        auto block = [&](int ko, int NBo, int woff, int wprod) -> int {
+            BlkDims bd;
+            bd.m = m;
+            bd.ptop = ptop;
+            bd.k = ko;
+            bd.NBo = NBo;
+            bd.c0 = ko - m - NBo;
+            bd.r0 = ptop + ko - NBo;
+            bd.A = a.A;
+            bd.lda = a.lda;
+            bd.shifts = d.shifts;
+            bd.LDZ = LDZ;
+            bd.wstride = wstride;
+            bd.woff = woff;
+            bd.wprod = wprod;
+            int rc = feed_wait(h, feed, st);  // this outer block's panel columns
+            if (rc) return rc;
+            cudaEvent_t ev = ss::timing_begin(h, st);
+            rc = launch_block(h, m, sb, blk_smem_bytes(m), st, bd, B.Z, B.P);
+            if (rc) return rc;
+            ss::timing_end(h, st, ev, ss::PH_RQ);
+            return SS_OK;
+        };
+        for (int ko = n; ko >= m + 1;) {
+            const int NBa = std::min(kBlkNB, ko - m);
+            const int c0a = ko - m - NBa, r0a = ptop + ko - NBa;
+            const int kb = ko - NBa;  // block B's k
+            if (pairing && kb - m >= kBlkNB) {
+                const int c0b = c0a - kBlkNB, r0b = r0a - kBlkNB;
+                int rc = block(ko, NBa, kBlkNB, 0);
+                if (rc) return rc;
+                rc = far_update(r0b, r0a, c0a, NBa, kBlkNB);  // near: B's rows
+                if (rc) return rc;
+                rc = block(kb, kBlkNB, 0, NBa + m);
+                if (rc) return rc;
+                rc = far_update(a.mode == 1 ? c0b : 0, r0b, c0b, kBlkNB + NBa, 0);
+                if (rc) return rc;
+                ko = kb - kBlkNB;
+            } else {
+                int rc = block(ko, NBa, 0, 0);
+                if (rc) return rc;
+                rc = far_update(a.mode == 1 ? c0a : 0, r0a, c0a, NBa, 0);
+                if (rc) return rc;
+                ko = kb;
+            }
         }
     }
     while (k >= m + 1) {
@@ -1086,7 +1139,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
-    const int64_t pst = two_level ? (int64_t)(kBlkNB + m) * m : (int64_t)ncmax * m;
+    const int64_t pst = two_level ? (int64_t)((two_level_pairing(m) ? 2 : 1) * kBlkNB + m) * m
+                                  : (int64_t)ncmax * m;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64;
     int64_t sb_max = a.batch > 0 ? a.batch : a.s;
     {
