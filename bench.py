@@ -58,17 +58,60 @@ def parse():
 # clocks (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clock and throttle-reason samples DURING the timed region: NVML
+    polled from a thread every 5 ms (a timed region is ~0.1-1 s, too short
+    for nvidia-smi's sampling loop to start), nvidia-smi as the fallback."""
+
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.rows = []
+        self.stop_ev = None
+        self.thread = None
         self.p = None
+        self.f = None
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv, h = self.nv, self.h
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = get_r(h)
+                self.rows.append((float(sm), float(mx), int(r)))
+            except Exception:
+                pass
+            if self.stop_ev.wait(0.005):
+                break
 
     def start(self):
+        if self.nv is not None:
+            import threading
+            self.stop_ev = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
@@ -76,6 +119,25 @@ class Clocks:
             self.p = None
 
     def stop(self) -> dict:
+        if self.thread is not None:
+            self.stop_ev.set()
+            self.thread.join(timeout=5)
+            nv = self.nv
+            if not self.rows:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": "nvml"}
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted({k for _, _, r in self.rows for k, b in bits.items() if r & b})
+            sm = [r[0] for r in self.rows]
+            mx = max(r[1] for r in self.rows)
+            load = [v for v in sm if v >= 0.5 * mx] or sm
+            return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(self.rows), "source": "nvml (5 ms poll)"}
+        return self._stop_smi()
+
+    def _stop_smi(self) -> dict:
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
@@ -345,7 +407,7 @@ def main():
         chf_h = ss.ControllerHessForm(Ahat=A_h, Bhat=B_h, Chat=C_h, m=m, n=n, p=p)
         ss.eval_transfer_function(chf_h, sh_h, nb=args.nb, on_singular="mark")
         times = []
-        for _ in range(max(1, min(args.steps, 3))):
+        for _ in range(max(3, min(args.steps, 5))):
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()

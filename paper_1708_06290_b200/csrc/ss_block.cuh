@@ -414,6 +414,9 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
             if (!vq[q]) continue;
             double2* Wp = Wl[q] + (int64_t)(kBlkNB - d.woff) * M;
             for (int row = lane; row < d.wprod; row += 32) {
+                // keep the W22 loads inside the loop (hoisting all m^2 of them
+                // out of it spills)
+                asm volatile("" ::: "memory");
                 double2 w[M], acc[M];
 #pragma unroll
                 for (int j = 0; j < M; ++j) w[j] = Wp[(int64_t)row * M + j];

@@ -466,8 +466,8 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
         if (rc) return rc;
     }
     const size_t per_shift = (size_t)LDS * mp * 16 + (size_t)(nb0 + mp) * mp * 16 + 8 + 64;
-    int64_t sb_max = batch > 0 ? batch : s;
-    {
+    int64_t sb_max = std::min<int64_t>(batch > 0 ? batch : s, s);
+    if (per_shift * (size_t)sb_max + 256 > h->ws_bytes) {  // query only to grow (slow driver call)
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         const size_t cap = std::max<size_t>(fr / 2 + h->ws_bytes / 2, per_shift);

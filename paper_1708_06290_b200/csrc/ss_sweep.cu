@@ -30,6 +30,7 @@
 // ss_tf_eval_stream additionally streams Ahat from pinned host memory in the
 // order the sweep consumes its columns (copy stream + one event per chunk).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -741,25 +742,44 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             ss::timing_end(h, st, ev, ss::PH_RQ);
             return SS_OK;
         };
+        const bool hprof = getenv("SS_HOST_PROF") != nullptr;
+        auto hnow = [] { return std::chrono::steady_clock::now(); };
+        auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        auto block_p = block;
+        auto far_p = far_update;
+        auto block_t = [&](int ko, int NBo, int woff, int wprod) -> int {
+            auto t0 = hnow();
+            int rc = block_p(ko, NBo, woff, wprod);
+            if (hprof && hms(t0, hnow()) > 1.0) fprintf(stderr, "[host] block ko=%d %.2f ms\n", ko, hms(t0, hnow()));
+            return rc;
+        };
+        auto far_t = [&](int rlo, int r0, int c0, int ncols, int woff) -> int {
+            auto t0 = hnow();
+            int rc = far_p(rlo, r0, c0, ncols, woff);
+            if (hprof && hms(t0, hnow()) > 1.0) fprintf(stderr, "[host] far r0=%d %.2f ms\n", r0, hms(t0, hnow()));
+            return rc;
+        };
         for (int ko = n; ko >= m + 1;) {
             const int NBa = std::min(kBlkNB, ko - m);
             const int c0a = ko - m - NBa, r0a = ptop + ko - NBa;
             const int kb = ko - NBa;  // block B's k
             if (pairing && kb - m >= kBlkNB) {
                 const int c0b = c0a - kBlkNB, r0b = r0a - kBlkNB;
-                int rc = block(ko, NBa, kBlkNB, 0);
+                int rc = block_t(ko, NBa, kBlkNB, 0);
                 if (rc) return rc;
-                rc = far_update(r0b, r0a, c0a, NBa, kBlkNB);  // near: B's rows
+                rc = far_t(r0b, r0a, c0a, NBa, kBlkNB);  // near: B's rows
                 if (rc) return rc;
-                rc = block(kb, kBlkNB, 0, NBa + m);
+                rc = block_t(kb, kBlkNB, 0, NBa + m);
                 if (rc) return rc;
-                rc = far_update(a.mode == 1 ? c0b : 0, r0b, c0b, kBlkNB + NBa, 0);
+                rc = far_t(a.mode == 1 ? c0b : 0, r0b, c0b, kBlkNB + NBa, 0);
                 if (rc) return rc;
                 ko = kb - kBlkNB;
             } else {
-                int rc = block(ko, NBa, 0, 0);
+                int rc = block_t(ko, NBa, 0, 0);
                 if (rc) return rc;
-                rc = far_update(a.mode == 1 ? c0a : 0, r0a, c0a, NBa, 0);
+                rc = far_t(a.mode == 1 ? c0a : 0, r0a, c0a, NBa, 0);
                 if (rc) return rc;
                 ko = kb;
             }
@@ -1142,8 +1162,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const int64_t pst = two_level ? (int64_t)((two_level_pairing(m) ? 2 : 1) * kBlkNB + m) * m
                                   : (int64_t)ncmax * m;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64;
-    int64_t sb_max = a.batch > 0 ? a.batch : a.s;
-    {
+    int64_t sb_max = std::min<int64_t>(a.batch > 0 ? a.batch : a.s, a.s);
+    if (per_shift * (size_t)sb_max + 256 > h->ws_bytes) {
+        // only when the workspace has to grow: cudaMemGetInfo is a driver
+        // query measured at 1-80 ms of host time on a busy box, which stalls
+        // the enqueue (and the GPU behind it)
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         const size_t cap = std::max<size_t>(fr / 2 + h->ws_bytes / 2, per_shift);
