@@ -88,10 +88,17 @@ __host__ __device__ inline size_t blk_smem_bytes(int m) {
 // (NSW = 1; two interleaved shifts per warp measured slower) and all shifts'
 // chains stay resident at once.
 //
-// After the chain, P_i = H_{nbi-1}(...(H_0 E)) by reverse accumulation:
-// lane pair (2c, 2c+1) owns column c of P, each lane half of the sliding
-// L-window (6 entries), so a step is 6 complex dot terms + one shuffle
-// exchange.
+// P_i = H_{nbi-1}(...(H_0 E)) (first m columns of the window's unitary):
+//  * m > 6: after the chain, by reverse accumulation: lane pair (2c, 2c+1)
+//    owns column c of P, each lane half of the sliding L-window, so a step
+//    is (L+1)/2 complex dot terms + one shuffle exchange;
+//  * m <= 6 (kFuse): row-wise, beside the chain.  Row r of P is
+//    e_r^T H_{nbi-1} ... H_0 restricted to columns < m: the chain's own row
+//    update applied to e_r, starting at step r (columns right of r are zero
+//    before), and a data row retires exactly when it is the pivot -- so lane
+//    rho carries data row rho while ti > rho and P row rho from ti = rho on,
+//    at no extra instruction; lanes < m carry the m rows of P22 (e_{nbi+j})
+//    in a second window.
 template <int M, int NSW>
 __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
     k_block(BlkDims d, double2* __restrict__ Z, double2* __restrict__ W, int sb) {
@@ -99,6 +106,11 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
     constexpr int HW = (L + 1) / 2;  // window entries per lane of a column pair
     constexpr int CR = 16;           // columns per reverse-accumulation round (2 lanes each)
     static_assert(L <= 32, "k_block: m <= 31");
+    // P rows beside the chain for narrow windows: measured on B200, config 1
+    // (m = 5) block kernel 0.34 -> 0.28 ms, config 2 (m = 10) 5.27 -> 5.53 ms
+    // (the extra P-row window's 8L DFMA per step outweigh the column-wise
+    // reverse accumulation they replace once the window is wide)
+    constexpr bool kFuse = M <= 6;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int PSZ = (kBlkInner + M) * M, USZ = kBlkInner * L;
     constexpr int QSZ = PSZ + USZ + kBlkInner + 64 + M * M;  // complex per shift
@@ -161,6 +173,17 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
             // loads in flight together) instead of one dependent load per step
             for (int c = 0; c < nbi; ++c) Apn[c * 32 + lane] = mine ? Ab[arow + (int64_t)(b + c) * d.lda] : 0.0;
             double2 z[NSW][L];  // window: z[0] = panel column, z[1..L) = state
+            // kFuse: P_i's rows are accumulated beside the chain (see k_block's
+            // comment): lane rho carries data row rho while ti > rho and row
+            // rho of P from ti = rho on; lanes < M also carry P row nbi + lane
+            double2 x2[NSW][kFuse ? L : 1];
+            if (kFuse) {
+#pragma unroll
+                for (int q = 0; q < NSW; ++q)
+#pragma unroll
+                    for (int j = 0; j < (kFuse ? L : 1); ++j)
+                        x2[q][j] = make_double2(j == lane + 1 ? 1.0 : 0.0, 0.0);
+            }
             {
                 const double a0 = Apn[(nbi - 1) * 32 + lane];
 #pragma unroll
@@ -178,10 +201,16 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
                     for (int q = 0; q < NSW; ++q)
 #pragma unroll
                         for (int j = 0; j < L; ++j) Piv[q][pb + j] = z[q][j];
+                    if (kFuse) {  // the pivot row retires; row rho of P starts as e_rho
+#pragma unroll
+                        for (int q = 0; q < NSW; ++q)
+#pragma unroll
+                            for (int j = 0; j < L; ++j) z[q][j] = make_double2(j == 0 ? 1.0 : 0.0, 0.0);
+                    }
                 }
                 const double pf = ti > 0 ? Apn[(ti - 1) * 32 + lane] : 0.0;
                 __syncwarp();
-                const bool upd = mine && rho < ti;
+                const bool upd = kFuse ? mine : (mine && rho < ti);
 #pragma unroll
                 for (int q = 0; q < NSW; ++q) {
                     double2 pv[L];
@@ -230,27 +259,70 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
                     }
                     z[q][L - 1].x = fma(-tw.x, vl.x, fma(-tw.y, vl.y, z[q][L - 1].x));
                     z[q][L - 1].y = fma(tw.x, vl.y, fma(-tw.y, vl.x, z[q][L - 1].y));
-                    // v and kappa for the reverse accumulation (off the serial path)
-                    if (lane < L) {
-                        const double2 x = Piv[q][pb + lane];
-                        U[q][ti * L + lane] = lane < L - 1 ? make_double2(x.x, -x.y) : vl;
+                    if (kFuse) {
+                        // P row nbi + lane (zero windows on lanes >= M stay zero)
+                        double2 e0 = cz(), e1 = cz();
+#pragma unroll
+                        for (int j = 0; j < L - 1; ++j) {
+                            double2& dd = (j & 1) ? e1 : e0;
+                            dd.x = fma(x2[q][j].x, pv[j].x, dd.x);
+                            dd.x = fma(x2[q][j].y, pv[j].y, dd.x);
+                            dd.y = fma(x2[q][j].y, pv[j].x, dd.y);
+                            dd.y = fma(-x2[q][j].x, pv[j].y, dd.y);
+                        }
+                        double2 dot2 = cadd(e0, e1);
+                        dot2 = cfma(x2[q][L - 1], vl, dot2);
+                        const double2 tw2 = cmul(kap, dot2);
+#pragma unroll
+                        for (int j = 0; j < L - 1; ++j) {
+                            x2[q][j].x = fma(-tw2.x, pv[j].x, fma(tw2.y, pv[j].y, x2[q][j].x));
+                            x2[q][j].y = fma(-tw2.x, pv[j].y, fma(-tw2.y, pv[j].x, x2[q][j].y));
+                        }
+                        x2[q][L - 1].x = fma(-tw2.x, vl.x, fma(-tw2.y, vl.y, x2[q][L - 1].x));
+                        x2[q][L - 1].y = fma(tw2.x, vl.y, fma(-tw2.y, vl.x, x2[q][L - 1].y));
+                    } else {
+                        // v and kappa for the reverse accumulation (off the serial path)
+                        if (lane < L) {
+                            const double2 x = Piv[q][pb + lane];
+                            U[q][ti * L + lane] = lane < L - 1 ? make_double2(x.x, -x.y) : vl;
+                        }
+                        if (lane == 0) Tau[q][ti] = kap;
                     }
-                    if (lane == 0) Tau[q][ti] = kap;
                 }
                 // slide (unconditionally: after the last step z is dead)
 #pragma unroll
                 for (int q = 0; q < NSW; ++q) {
 #pragma unroll
                     for (int j = L - 1; j > 0; --j) z[q][j] = z[q][j - 1];
-                    double2 v = make_double2(pf, 0.0);
+                    // P rows (kFuse, rho >= ti) take a zero: e_rho has no entry left of rho
+                    double2 v = (!kFuse || rho < ti) ? make_double2(pf, 0.0) : cz();
                     if (mine && rho + M == ti - 1) v = csub(v, sig[q]);
                     z[q][0] = v;
+                    if (kFuse) {
+#pragma unroll
+                        for (int j = (kFuse ? L : 1) - 1; j > 0; --j) x2[q][j] = x2[q][j - 1];
+                        x2[q][0] = cz();
+                    }
+                }
+            }
+            if (kFuse) {
+                // after the last step's slide, window entry c + 1 is column c
+#pragma unroll
+                for (int q = 0; q < NSW; ++q) {
+                    if (mine) {
+#pragma unroll
+                        for (int c = 0; c < M; ++c) P[q][rho * M + c] = z[q][c + 1];
+                    }
+                    if (lane < M) {
+#pragma unroll
+                        for (int c = 0; c < M; ++c) P[q][(nbi + lane) * M + c] = x2[q][(kFuse ? c + 1 : 0)];
+                    }
                 }
             }
             __syncwarp();
         }
         // ---------------- reverse accumulation -> P (j-major) ----------------
-        for (int cr = 0; cr < M; cr += CR)
+        for (int cr = 0; cr < (kFuse ? 0 : M); cr += CR)
         if (lane < 2 * min(CR, M - cr)) {
             const int ncr = min(CR, M - cr);
             const unsigned pm = ncr == 16 ? 0xffffffffu : ((1u << (2 * ncr)) - 1u);
@@ -265,17 +337,19 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
 #pragma unroll
                 for (int q = 0; q < NSW; ++q) {
                     const double2* us = U[q] + s * L + base;
-                    dp[q] = cz();
+                    double2 d2[2] = {cz(), cz()};  // two partial sums: half the FMA chain depth
 #pragma unroll
                     for (int k = 0; k < HW; ++k) {
                         if (base + k < L) {
                             const double2 uk = us[k];  // conj(u) w
-                            dp[q].x = fma(uk.x, w[q][k].x, dp[q].x);
-                            dp[q].x = fma(uk.y, w[q][k].y, dp[q].x);
-                            dp[q].y = fma(uk.x, w[q][k].y, dp[q].y);
-                            dp[q].y = fma(-uk.y, w[q][k].x, dp[q].y);
+                            double2& dd = d2[k & 1];
+                            dd.x = fma(uk.x, w[q][k].x, dd.x);
+                            dd.x = fma(uk.y, w[q][k].y, dd.x);
+                            dd.y = fma(uk.x, w[q][k].y, dd.y);
+                            dd.y = fma(-uk.y, w[q][k].x, dd.y);
                         }
                     }
+                    dp[q] = cadd(d2[0], d2[1]);
                 }
 #pragma unroll
                 for (int q = 0; q < NSW; ++q) {
