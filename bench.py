@@ -84,6 +84,7 @@ class Clocks:
                 self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
             except Exception:
                 self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.nv = pynvml
         except Exception:
             self.nv = None
@@ -92,7 +93,7 @@ class Clocks:
         nv, h = self.nv, self.h
         get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = self.mx
         while True:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
@@ -103,9 +104,20 @@ class Clocks:
             if self.stop_ev.wait(0.005):
                 break
 
+    def _sample_now(self):
+        nv, h = self.nv, self.h
+        try:
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                              float(self.mx), int(get_r(h))))
+        except Exception:
+            pass
+
     def start(self):
         if self.nv is not None:
             import threading
+            self.rows = []
             self.stop_ev = threading.Event()
             self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
@@ -117,6 +129,11 @@ class Clocks:
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+
+    def mark(self):
+        """A synchronous sample (call while the GPU is busy with queued work)."""
+        if self.thread is not None:
+            self._sample_now()
 
     def stop(self) -> dict:
         if self.thread is not None:
@@ -347,6 +364,7 @@ def main():
     ev0.record(stream)
     for _ in range(args.steps):
         step()
+        clk.mark()  # the queue holds this step's kernels: the GPU is under load
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

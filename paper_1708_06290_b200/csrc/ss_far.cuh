@@ -22,6 +22,10 @@
 
 namespace ssd {
 
+#ifndef SS_FAR_NAP
+#define SS_FAR_NAP 128  // producer back-off (ns) when no stage is free
+#endif
+
 // Tile shape (template): lane = (row group rg < 32/G, column group q < G),
 // R rows x C columns per lane, tile = (32/G) R rows.  NPAIR consumer pairs,
 // NST ring stages.
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(far_threads(NPAIR), 1)
                     --left;
                     any = true;
                 }
-                if (!any) __nanosleep(128);
+                if (!any) __nanosleep(SS_FAR_NAP);
             }
         }
         return;
