@@ -42,6 +42,7 @@
 #include "ss_update.cuh"
 #include "ss_update_ws.cuh"
 #include "ss_block.cuh"
+#include "ss_rq_m1.cuh"
 #include "ss_far.cuh"
 
 using namespace ssd;
@@ -822,7 +823,9 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             rd.shifts = d.shifts;
             rd.LDZ = LDZ;
             const size_t sm = rqh_warp_smem(s.nb, m);
-            if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+            if (m == 1 && s.nb <= 64 && !getenv("SS_RQ_M1_OFF"))
+                k_rq_m1<<<(sb + 4 * kM1Warps - 1) / (4 * kM1Warps), 32 * kM1Warps, 0, st>>>(rd, B.Z, B.P);
+            else if (m == 1) k_rq_house<2, 2><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
             else if (m == 5) k_rq_house<6, 6><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
             else if (m == 10) k_rq_house<11, 11><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
             else if (m == 20) k_rq_house<21, 21><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
