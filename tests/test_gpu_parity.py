@@ -410,6 +410,46 @@ def test_two_level_vs_one_level(n, m, p, monkeypatch):
         assert rel(G2[:, l * m:(l + 1) * m], Go[:, k * m:(k + 1) * m]) <= 1e-10
 
 
+@pytest.mark.parametrize("n,m,p", [(700, 10, 10), (650, 20, 5), (520, 5, 5), (400, 4, 3)])
+def test_paired_blocks_vs_unpaired(n, m, p, monkeypatch):
+    """Paired outer blocks (near update + one far update per 256 columns from
+    the composite W) against one far update per 128-column block
+    (SS_NO_PAIR=1): the composite is exact algebra, so G and the reduced
+    solve agree to rounding; odd block counts and a ragged last block."""
+    chf = _mhess_triple(n, m, p, seed=n * 13 + m)
+    shifts = np.concatenate([1j * np.logspace(-2, 2, 19) * np.sqrt(n) + 0.3,
+                             [0.5 * np.sqrt(n) - 0.2j]])
+    bd = np.exp(1j * np.arange(m * 3).reshape(m, 3))
+    Gp = ss.eval_transfer_function(chf, shifts, nb=64).G
+    Xp = ss.solve_shifted_reduced(chf, shifts[:3], bd, nb=64).x
+    monkeypatch.setenv("SS_NO_PAIR", "1")
+    Gu = ss.eval_transfer_function(chf, shifts, nb=64).G
+    Xu = ss.solve_shifted_reduced(chf, shifts[:3], bd, nb=64).x
+    assert per_shift_rel(Gp, Gu, m, len(shifts)) <= 1e-12
+    assert max(rel(Xp[:, k], Xu[:, k]) for k in range(3)) <= 1e-12
+
+
+@pytest.mark.parametrize("n,nb", [(333, 64), (300, 32), (129, 7), (66, 64)])
+def test_m1_throughput_rq_vs_warp_rq(n, nb, monkeypatch):
+    """m = 1 window RQ: the 8-lane-per-shift kernel (k_rq_m1, P rows beside
+    the chain) against the one-warp-per-shift Householder RQ
+    (SS_RQ_M1_OFF=1) and the C oracle, on ragged windows (nb < 64, n - 1 not
+    a multiple of nb), a shift count that leaves a partial warp, a zero
+    subdiagonal (identity reflectors) and real / complex / conjugate shifts."""
+    chf = _mhess_triple(n, 1, 1, seed=n + nb)
+    chf.Ahat[n // 2, n // 2 - 1] = 0.0
+    shifts = np.concatenate([1j * np.logspace(-2, 2, 19) * np.sqrt(n) + 0.1,
+                             [0.3 * np.sqrt(n), 0.2 - 0.7j * np.sqrt(n)]])
+    r1 = ss.eval_transfer_function(chf, shifts, nb=nb)
+    monkeypatch.setenv("SS_RQ_M1_OFF", "1")
+    r0 = ss.eval_transfer_function(chf, shifts, nb=nb)
+    assert r1.failures == r0.failures == {}
+    assert per_shift_rel(r1.G, r0.G, 1, len(shifts)) <= 1e-12
+    Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts[[0, 10, 20]], nb=nb)
+    for k, l in enumerate([0, 10, 20]):
+        assert rel(r1.G[:, l:l + 1], Go[:, k:k + 1]) <= 1e-10
+
+
 @pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4)])
 def test_wide_m_paths_vs_oracle(n, m, p):
     """Block widths outside the two-level set: m + 1 > 32 takes the scheduled
