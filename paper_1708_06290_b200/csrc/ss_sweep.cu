@@ -43,6 +43,7 @@
 #include "ss_update_ws.cuh"
 #include "ss_block.cuh"
 #include "ss_rq_m1.cuh"
+#include "ss_rq_big.cuh"
 #include "ss_far.cuh"
 
 using namespace ssd;
@@ -582,6 +583,14 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
     return SS_OK;
 }
 
+// m + 1 > 32 (config 5): the shared-memory Householder RQ (ss_rq_big.cuh) on
+// 96-column windows unless SS_BLOCK_RQ=givens asks for the reference's batch
+static bool rq_big(int m) {
+    const char* e = getenv("SS_BLOCK_RQ");
+    return m + 1 > 32 && m + 1 <= 64 && !(e && strcmp(e, "givens") == 0);
+}
+constexpr int kRqBigNb = 96;
+
 // m < 4: the per-window overhead 2m/nb is already < 13% at nb = 64 and the
 // one-level sweep measured faster (config 3, m = 1: 13.7 vs 19.3 ms)
 bool block_supported(int m) { return (m >= 4 && m <= 8) || m == 10 || m == 20; }
@@ -834,6 +843,27 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             else if (m + 1 <= 8) k_rq_house<8><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
             else if (m + 1 <= 16) k_rq_house<16><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
             else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
+        } else if (rq_big(m)) {
+            // m + 1 > 32: Householder RQ with the windows in shared memory
+            static bool configured = false;
+            if (!configured) {
+                SS_CUDA_TRY(h, allow_max_smem(h, k_rq_big));
+                configured = true;
+            }
+            RqDims rd;
+            rd.m = m;
+            rd.ptop = ptop;
+            rd.nb = s.nb;
+            rd.k = s.k;
+            rd.c0 = s.c0;
+            rd.r0 = s.r0;
+            rd.nc = s.nc;
+            rd.sb = sb;
+            rd.A = a.A;
+            rd.lda = a.lda;
+            rd.shifts = d.shifts;
+            rd.LDZ = LDZ;
+            k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(s.nb, m), st>>>(rd, B.Z, B.P);
         } else {
             // the reference's scheduled Givens batch: one warp per concurrent
             // rotation (<= 16 warps), rotation parameters in registers
@@ -1117,7 +1147,9 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const bool use_house = (m + 1 <= 32) && !(rqenv && strcmp(rqenv, "givens") == 0);
     const UpdTile tile = pick_tile(m);
     // the Householder block RQ maps one block row to one thread of two warps
-    const int nb0 = use_house ? std::min(nb0_req, 64) : nb0_req;
+    int nb_big = kRqBigNb;
+    if (const char* e = getenv("SS_BIG_NB")) nb_big = std::max(8, std::min(96, atoi(e)));
+    const int nb0 = use_house ? std::min(nb0_req, 64) : (rq_big(m) ? nb_big : nb0_req);
 
     // two-level sweep (ss_block.cuh) when the fused block kernel and the
     // warp-specialised far update cover m; SS_ONE_LEVEL=1 forces the
