@@ -98,23 +98,16 @@ class Clocks:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 r = get_r(h)
-                self.rows.append((float(sm), float(mx), int(r)))
+                self.rows.append((float(sm), float(mx), int(r), time.perf_counter()))
             except Exception:
                 pass
             if self.stop_ev.wait(0.005):
                 break
 
-    def _sample_now(self):
-        nv, h = self.nv, self.h
-        try:
-            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                nv.nvmlDeviceGetCurrentClocksThrottleReasons
-            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
-                              float(self.mx), int(get_r(h))))
-        except Exception:
-            pass
-
     def start(self):
+        """Start polling (call before the warm-up: the thread is then surely
+        running when the timed region opens); begin()/end() mark the region."""
+        self.t0 = self.t1 = None
         if self.nv is not None:
             import threading
             self.rows = []
@@ -130,23 +123,26 @@ class Clocks:
         except OSError:
             self.p = None
 
-    def mark(self):
-        """A synchronous sample (call while the GPU is busy with queued work)."""
-        if self.thread is not None:
-            self._sample_now()
+    def begin(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self) -> dict:
         if self.thread is not None:
             self.stop_ev.set()
             self.thread.join(timeout=5)
             nv = self.nv
+            if self.t0 is not None and self.t1 is not None:
+                self.rows = [r for r in self.rows if self.t0 <= r[3] <= self.t1]
             if not self.rows:
                 return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": "nvml"}
             bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                     "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
                     "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
-            reasons = sorted({k for _, _, r in self.rows for k, b in bits.items() if r & b})
+            reasons = sorted({k for _, _, r, _ in self.rows for k, b in bits.items() if r & b})
             sm = [r[0] for r in self.rows]
             mx = max(r[1] for r in self.rows)
             load = [v for v in sm if v >= 0.5 * mx] or sm
@@ -350,23 +346,24 @@ def main():
     D.check(h, L.ss_probe_dfma_peak(h.ptr, ctypes.byref(peak)))
     fp64_peak = peak.value  # measured TFLOP/s on this box
 
+    clk = Clocks(local)
+    clk.start()  # polling thread up before the timed region opens
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, no instrumentation ----
-    clk = Clocks(local)
-    clk.start()
     launches0 = h.launches()
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.begin()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
-        clk.mark()  # the queue holds this step's kernels: the GPU is under load
     ev1.record(stream)
     torch.cuda.synchronize()
+    clk.end()
     barrier()
     clocks = clk.stop()
     launches = h.launches() - launches0
