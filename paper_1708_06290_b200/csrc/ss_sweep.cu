@@ -374,6 +374,17 @@ UpdTile pick_tile(int m) {
 template <int G, int C, bool EXACT>
 int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStream_t st,
                     const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
+    if (threads > 256) {
+        // K-split with several column blocks per shift (m > 31): up to 10 warps
+        static bool configured_w = false;
+        if (!configured_w) {
+            SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320>));
+            configured_w = true;
+        }
+        k_update<G, C, EXACT, 320><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
+        SS_LAUNCH_CHECK(h);
+        return SS_OK;
+    }
     static bool configured = false;
     if (!configured) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT>));
@@ -911,7 +922,12 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         u.nws = nws;
         // a warp pair splits the panel K range of one (shift, column block) when
         // one block covers all m columns: twice the warps on the same staging
-        u.ksplit = (nws == 1 && tile.exact) ? 2 : 1;  // scratch = the shift's m x 64 Z2 stage
+        // (also for several column blocks per shift when the block RQ is the
+        // wide-window one: 2 nws warps per shift, SS_UPD_KSPLIT1=1 disables)
+        u.ksplit = ((nws == 1 && tile.exact) ||
+                    (nws > 1 && tile.exact && rq_big(m) && 64 * nws <= 320 && !getenv("SS_UPD_KSPLIT1")))
+                       ? 2
+                       : 1;  // scratch = the shift's m x 64 Z2 stage
         u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2));
         u.S = std::max(1, 8 / (nws * u.ksplit));
         const size_t two_per_sm = h->smem_optin / 2 - 1024;

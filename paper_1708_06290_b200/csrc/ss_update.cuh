@@ -82,8 +82,8 @@ __device__ __forceinline__ int pan_index(int row) {
     return p * (2 * RG) + rg * 2 + e;
 }
 
-template <int G, int C, bool EXACT>
-__global__ void __launch_bounds__(256)
+template <int G, int C, bool EXACT, int MAXT = 256>
+__global__ void __launch_bounds__(MAXT)
     k_update(UpdDims u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
              const double2* __restrict__ Pbuf) {
     constexpr int R = 2 * G, RG = 32 / G;
@@ -215,11 +215,15 @@ __global__ void __launch_bounds__(256)
         }
         if (u.ksplit == 2) {
             // half 1 hands its partial sums to half 0 through this shift's (now
-            // consumed) Z2 staging tile: [c][64 rows] per column block
-            const int bar = 1 + unit;
-            asm volatile("bar.sync %0, 64;\n" ::"r"(bar));   // half 0 done reading Zs
-            // scratch [(r*C + c)][lane]: conflict-free 16-byte stores / loads
-            double2* red = Zs + lane;
+            // consumed) Z2 staging tile: [c][64 rows] per column block.  With
+            // several column blocks every block's half 0 reads all m columns
+            // of Zs, so the whole shift group syncs (64 nws threads; one named
+            // barrier per shift of the CTA)
+            const int bar = u.nws == 1 ? 1 + unit : 1 + s_w;
+            const int cnt = 64 * u.nws;
+            asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(cnt));   // every half 0 done reading Zs
+            // scratch [(r*C + c)][lane] per column block: conflict-free 16-byte stores / loads
+            double2* red = Zs + blk * (R * C * 32) + lane;
             if (half == 1) {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(256)
                     for (int c = 0; c < C; ++c)
                         if (EXACT || c < ncol) red[(r * C + c) * 32] = acc[r][c];
             }
-            asm volatile("bar.sync %0, 64;\n" ::"r"(bar));   // partials visible
+            asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(cnt));   // partials visible
             if (half == 1) continue;
 #pragma unroll
             for (int r = 0; r < R; ++r)
