@@ -100,8 +100,18 @@ def main():
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    # parity spot check vs a dense solve of a few shifts
+    # parity spot check vs a dense solve of a few shifts (large n: complex128
+    # LU on the device through torch -- a checker, not the product path)
     if n > 4000:
+        Ad = A.to(torch.complex128)
+        for l in (0, s - 1):
+            sig = sh[l].item()
+            Ms = Ad - sig * torch.eye(n, dtype=torch.complex128, device=A.device)
+            X = torch.linalg.solve(Ms, B.to(torch.complex128))
+            Gr = -(C.to(torch.complex128) @ X)
+            err = float(torch.linalg.norm(G[:, l * m:(l + 1) * m] - Gr) / torch.linalg.norm(Gr))
+            print(f"  shift {l}: rel err vs dense solve {err:.2e}", flush=True)
+            del Ms, X
         return
     Ah, Bh, Ch = (x.cpu().numpy() for x in (A, B, C))
     Gh = G.cpu().numpy()
