@@ -459,7 +459,7 @@ def main():
                        "l2": "no flush: per-step working set (Ahat 128 MB + window state "
                              "~1.3 GB) exceeds the 126 MB L2",
                        "parallelism": f"shift-sharded x{world} (broadcast once, all-gather G)"},
-            "roofline": {"bound": "fp64", "kernel": "k_far (far-row update from the outer block's W; k_update_ws on the one-level path)",
+            "roofline": {"bound": "fp64", "kernel": "k_far4 (far-row update from the paired blocks' composite W, 128-column passes, four-way K split; k_far / k_update_ws on other paths)",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": achieved / fp64_peak if fp64_peak else None,
                          "traffic": traffic,

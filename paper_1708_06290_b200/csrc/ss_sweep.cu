@@ -44,6 +44,7 @@
 #include "ss_block.cuh"
 #include "ss_rq_m1.cuh"
 #include "ss_rq_big.cuh"
+#include "ss_far4.cuh"
 #include "ss_far.cuh"
 
 using namespace ssd;
@@ -463,6 +464,20 @@ int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStrea
     return SS_EARG;
 }
 
+// 128-column far passes with the four-way K split (ss_far4.cuh), m = 10
+template <bool ZID>
+int launch_far4_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
+                  const double2* pbuf) {
+    static bool configured = false;
+    if (!configured) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_far4<2, 5, 4, ZID>));
+        configured = true;
+    }
+    k_far4<2, 5, 4, ZID><<<grid, kFar4Threads, smem, st>>>(u, z, pbuf);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
 // Warp-specialised TMA/mbarrier update for tiles where one warp pair covers
 // all m columns (G*C == m); returns SS_EARG when the tile is not covered.
 int launch_update_ws(ss_handle* h, const UpdTile& t, dim3 grid, size_t smem, cudaStream_t st,
@@ -669,10 +684,15 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         const int64_t wstride = (int64_t)((pairing ? 2 : 1) * kBlkNB + m) * m;
         // far-row update of rows [rlo, r0) from the W rows [woff, woff + ncols
         // + m) of the buffer, panel columns [c0, c0 + ncols), in 64-column passes
+        // m = 10: 128-column passes on the four-way-split far kernel (SS_FAR4=0: 64-column k_far)
+        const bool far4 = m == 10 && tile.G == 2 && tile.C == 5 &&
+                          !(getenv("SS_FAR4") && atoi(getenv("SS_FAR4")) == 0) &&
+                          far4_smem_bytes<2, 5, 4>(128, m) + 1024 <= h->smem_optin;
+        const int pw = far4 ? 128 : 64;
         auto far_update = [&](int rlo, int r0, int c0, int ncols, int woff) -> int {
             const int rows = r0 - rlo;
-            for (int jb = 0; rows > 0 && jb < ncols; jb += 64) {
-                const int nbp = std::min(64, ncols - jb);
+            for (int jb = 0; rows > 0 && jb < ncols; jb += pw) {
+                const int nbp = std::min(pw, ncols - jb);
                 UpdDims u;
                 u.n = n;
                 u.m = m;
@@ -724,7 +744,24 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
                 cudaEvent_t ev = ss::timing_begin(h, st);
                 int rc;
-                if (getenv("SS_FAR_CLASSIC")) {
+                if (far4) {
+                    // role targets in panel-column equivalents: role 0 adds the
+                    // Z2 W22 part (2m) or the Z2 read and the epilogue, role 3
+                    // the read-add-write of the group buffer
+                    const int extra0 = (u.zid ? 1 : 2 * m) + 4;
+                    int T = (nbp + extra0 + 4 + 3) / 4;
+                    int j1 = std::max(0, T - extra0);
+                    if (const char* e = getenv("SS_FAR4_J")) j1 = std::max(0, j1 + atoi(e));
+                    const int rest = (nbp - j1);
+                    const int q = (rest - 2) / 3;
+                    u.jq[0] = std::min(nbp, j1);
+                    u.jq[1] = std::min(nbp, u.jq[0] + q + 1);
+                    u.jq[2] = std::min(nbp, u.jq[1] + q + 1);
+                    const int64_t units = (int64_t)((rows + 63) / 64) * sb;
+                    const int grid = (int)std::min<int64_t>(units, h->num_sms);
+                    rc = u.zid ? launch_far4_z<true>(h, grid, far4_smem_bytes<2, 5, 4>(nbp, m), st, u, B.Z, B.P)
+                               : launch_far4_z<false>(h, grid, far4_smem_bytes<2, 5, 4>(nbp, m), st, u, B.Z, B.P);
+                } else if (getenv("SS_FAR_CLASSIC")) {
                     rc = launch_update_ws(h, tile, gw, ws_smem_bytes(nbp, m), st, u, B.Z, B.Z, B.P);
                 } else {
                     const FarShape f = m == 20 ? FarShape{2, 5, 4, 4, 4, 2} : far_shape(tile);

@@ -59,6 +59,7 @@ struct UpdDims {
     int nws;     // column blocks per shift
     int ksplit;  // warps per (shift, column block): 1, or 2 = panel K range split
     int jh;      // ksplit == 2: warp half 0 takes panel columns [0, jh) + the Z2 part
+    int jq[3];   // k_far4: role boundaries of the four-way K split
     // P source (warp-specialised kernel): per shift, P12 = pstride*l + p12off
     // (nb x m, j-major), P22 = pstride*l + p22off (m x m) unless zid (P22 = I:
     // the far-row passes of the two-level sweep after the first)

@@ -7,13 +7,14 @@ Writes profiles/r1_far_traffic.json, which bench.py reports as roofline.traffic.
 import csv, json, sys
 from collections import defaultdict
 
-def far_launches(n=4000, m=10, p=10, s=1000, nb=128):
-    """(rows, ncols_of_pass, w22) per k_far launch, mirroring enqueue_part's
-    paired two-level loop (mode 0: far rows start at 0)."""
+def far_launches(n=4000, m=10, p=10, s=1000, nb=128, pw=128):
+    """(rows, ncols_of_pass, w22) per far-kernel launch, mirroring
+    enqueue_part's paired two-level loop (mode 0: far rows start at 0;
+    pw = pass width: 128 on k_far4 for m = 10, 64 on k_far)."""
     ptop, out = p, []
     def far(rlo, r0, ncols):
-        for jb in range(0, ncols, 64):
-            out.append((r0 - rlo, min(64, ncols - jb), jb == 0))
+        for jb in range(0, ncols, pw):
+            out.append((r0 - rlo, min(pw, ncols - jb), jb == 0))
     ko = n
     while ko >= m + 1:
         nba = min(nb, ko - m)
