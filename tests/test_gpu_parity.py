@@ -429,6 +429,26 @@ def test_paired_blocks_vs_unpaired(n, m, p, monkeypatch):
     assert max(rel(Xp[:, k], Xu[:, k]) for k in range(3)) <= 1e-12
 
 
+@pytest.mark.parametrize("n,p", [(1111, 10), (700, 3), (389, 10)])
+def test_far4_vs_far(n, p, monkeypatch):
+    """m = 10 far-row update: 128-column passes on the four-way-split kernel
+    (k_far4, default) against 64-column passes on k_far (SS_FAR4=0) --
+    ragged last blocks, odd pair counts, the near update, the reduced solve
+    (identity top, far rows from the block's first column)."""
+    m = 10
+    chf = _mhess_triple(n, m, p, seed=n * 7 + p)
+    shifts = np.concatenate([1j * np.logspace(-2, 2, 25) * np.sqrt(n) + 0.2,
+                             [0.4 * np.sqrt(n) + 0.9j * np.sqrt(n)]])
+    bd = np.exp(1j * np.arange(m * 3).reshape(m, 3))
+    G4 = ss.eval_transfer_function(chf, shifts, nb=64).G
+    X4 = ss.solve_shifted_reduced(chf, shifts[:3], bd, nb=64).x
+    monkeypatch.setenv("SS_FAR4", "0")
+    G2 = ss.eval_transfer_function(chf, shifts, nb=64).G
+    X2 = ss.solve_shifted_reduced(chf, shifts[:3], bd, nb=64).x
+    assert per_shift_rel(G4, G2, m, len(shifts)) <= 1e-12
+    assert max(rel(X4[:, k], X2[:, k]) for k in range(3)) <= 1e-12
+
+
 @pytest.mark.parametrize("n,nb", [(333, 64), (300, 32), (129, 7), (66, 64)])
 def test_m1_throughput_rq_vs_warp_rq(n, nb, monkeypatch):
     """m = 1 window RQ: the 8-lane-per-shift kernel (k_rq_m1, P rows beside
