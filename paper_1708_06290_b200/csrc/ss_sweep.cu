@@ -1202,6 +1202,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // the Householder block RQ maps one block row to one thread of two warps
     int nb_big = kRqBigNb;
     if (const char* e = getenv("SS_BIG_NB")) nb_big = std::max(8, std::min(96, atoi(e)));
+    // the generic update stages the whole (nb + m) x m P per shift: the
+    // widest window whose update and RQ fit one SM's shared memory
+    while (nb_big > 8 && (upd_smem_bytes(nb_big, m, 1) + 1024 > h->smem_optin ||
+                          rq_big_smem_bytes(nb_big, m) + 1024 > h->smem_optin))
+        nb_big -= 8;
     const int nb0 = use_house ? std::min(nb0_req, 64) : (rq_big(m) ? nb_big : nb0_req);
 
     // two-level sweep (ss_block.cuh) when the fused block kernel and the

@@ -470,7 +470,7 @@ def test_m1_throughput_rq_vs_warp_rq(n, nb, monkeypatch):
         assert rel(r1.G[:, l:l + 1], Go[:, k:k + 1]) <= 1e-10
 
 
-@pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4)])
+@pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4), (300, 63, 5)])
 def test_wide_m_paths_vs_oracle(n, m, p):
     """Block widths outside the two-level set: m + 1 > 32 takes the scheduled
     Givens block RQ (config 5: m = 50), m = 16 / 20 the one-level update with
