@@ -33,6 +33,22 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, sh[idx], nb=nb)
     err = max(np.linalg.norm(G[:, l * m:(l + 1) * m] - Go[:, k * m:(k + 1) * m]) /
               np.linalg.norm(Go[:, k * m:(k + 1) * m]) for k, l in enumerate(idx))
+    # reduced solve (identity top) and, for m + 1 <= 32, the transposed solve
+    k2 = [0, s - 1]
+    bd = rng.standard_normal((m, len(k2))) + 1j * rng.standard_normal((m, len(k2)))
+    try:
+        X = ss.solve_shifted_reduced(chf, sh[k2], bd, nb=nb, batch_size=bs).x
+        for k, l in enumerate(k2):
+            xo = O.lu_solve_shifted(chf.Ahat, sh[l], chf.Bhat @ bd[:, k])
+            err = max(err, np.linalg.norm(X[:, k] - xo) / np.linalg.norm(xo))
+        if m + 1 <= 32:
+            rhs = rng.standard_normal((n, len(k2))) + 1j * rng.standard_normal((n, len(k2)))
+            Xt = ss.solve_shifted_transposed(chf, sh[k2], rhs, nb=min(nb, 32), batch_size=bs).x
+            for k, l in enumerate(k2):
+                xo = O.lu_solve_shifted(chf.Ahat, sh[l], rhs[:, k], transpose=True)
+                err = max(err, np.linalg.norm(Xt[:, k] - xo) / np.linalg.norm(xo))
+    except Exception as e:
+        print(f"EXC(solve) n={n} m={m} p={p} nb={nb} bs={bs}: {e}"); bad += 1; continue
     worst = max(worst, err)
     flag = "FAIL" if err > 1e-10 else "ok"
     if err > 1e-10:
