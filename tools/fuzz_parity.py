@@ -18,7 +18,7 @@ ms = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 16, 20, 24, 31, 32, 40, 50, 63]
 worst, bad = 0.0, 0
 for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     m = int(rng.choice(ms))
-    n = int(rng.integers(m + 2, 900))
+    n = int(rng.integers(m + 2, int(os.environ.get("FUZZ_NMAX", "900"))))
     p = int(rng.integers(1, 12))
     nb = int(rng.choice([4, 7, 16, 32, 64]))
     bs = [None, 3, 17][int(rng.integers(0, 3))]
