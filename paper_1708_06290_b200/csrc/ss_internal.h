@@ -76,6 +76,10 @@ struct ss_handle {
 
 namespace ss {
 
+// cudaFuncSetAttribute acts on the current device: the launch helpers keep
+// one "configured" bit per device (handles on several devices in one process)
+inline unsigned dev_bit(const ss_handle* h) { return 1u << (h->device & 31); }
+
 int set_err(ss_handle* h, int code, const std::string& msg);
 int cuda_err(ss_handle* h, cudaError_t e, const char* what);
 // Ensure workspace of at least `bytes`; which=0 main, 1 secondary.

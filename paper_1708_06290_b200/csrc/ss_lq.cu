@@ -481,10 +481,10 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     double2* Sb = (double2*)h->ws;
     double2* Pb = Sb + (size_t)sb_max * mp * LDS;
     double* tolb = (double*)(Pb + (size_t)sb_max * (nb0 + mp) * mp);
-    static bool attrs = false;
-    if (!attrs) {
+    static unsigned attrs = 0;  // devices configured (bit per device)
+    if (!(attrs & ss::dev_bit(h))) {
         SS_CUDA_TRY(h, allow_smem(h, k_tupd));
-        attrs = true;
+        attrs |= ss::dev_bit(h);
     }
     for (int64_t lo = 0; lo < s; lo += sb_max) {
         const int sb = (int)std::min<int64_t>(sb_max, s - lo);

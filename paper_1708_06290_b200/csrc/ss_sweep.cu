@@ -377,19 +377,19 @@ int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStrea
                     const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
     if (threads > 256) {
         // K-split with several column blocks per shift (m > 31): up to 10 warps
-        static bool configured_w = false;
-        if (!configured_w) {
+        static unsigned configured_w = 0;  // devices configured (bit per device)
+        if (!(configured_w & ss::dev_bit(h))) {
             SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320>));
-            configured_w = true;
+            configured_w |= ss::dev_bit(h);
         }
         k_update<G, C, EXACT, 320><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
         SS_LAUNCH_CHECK(h);
         return SS_OK;
     }
-    static bool configured = false;
-    if (!configured) {
+    static unsigned configured = 0;  // devices configured (bit per device)
+    if (!(configured & ss::dev_bit(h))) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT>));
-        configured = true;
+        configured |= ss::dev_bit(h);
     }
     k_update<G, C, EXACT><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -399,10 +399,10 @@ int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStrea
 template <int G, int C, bool ZID>
 int launch_update_ws_z(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const UpdDims& u,
                        const double2* zin, double2* zout, const double2* pbuf) {
-    static bool configured = false;
-    if (!configured) {
+    static unsigned configured = 0;  // devices configured (bit per device)
+    if (!(configured & ss::dev_bit(h))) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_update_ws<G, C, ZID>));
-        configured = true;
+        configured |= ss::dev_bit(h);
     }
     k_update_ws<G, C, ZID><<<grid, kWsThreads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -419,10 +419,10 @@ int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, co
 template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB, bool MSH = false>
 int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                  const double2* pbuf) {
-    static bool configured = false;
-    if (!configured) {
+    static unsigned configured = 0;  // devices configured (bit per device)
+    if (!(configured & ss::dev_bit(h))) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID, NCB, MSH>));
-        configured = true;
+        configured |= ss::dev_bit(h);
     }
     k_far<G, C, R, NPAIR, NST, ZID, NCB, MSH><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -468,10 +468,10 @@ int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStrea
 template <bool ZID>
 int launch_far4_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                   const double2* pbuf) {
-    static bool configured = false;
-    if (!configured) {
+    static unsigned configured = 0;  // devices configured (bit per device)
+    if (!(configured & ss::dev_bit(h))) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_far4<2, 5, 4, ZID>));
-        configured = true;
+        configured |= ss::dev_bit(h);
     }
     k_far4<2, 5, 4, ZID><<<grid, kFar4Threads, smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -592,10 +592,10 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
     switch (m) {
 #define SS_CASE(K)                                                        \
     case K: {                                                             \
-        static bool configured = false;                                   \
-        if (!configured) {                                                \
+        static unsigned configured = 0;                                   \
+        if (!(configured & ss::dev_bit(h))) {                                                \
             SS_CUDA_TRY(h, allow_max_smem(h, k_block<K, kBlkShiftsPerWarp>)); \
-            configured = true;                                            \
+            configured |= ss::dev_bit(h);                                            \
         }                                                                 \
         k_block<K, kBlkShiftsPerWarp>                                     \
             <<<(sb + kBlkShiftsPerWarp - 1) / kBlkShiftsPerWarp, 32, smem, st>>>(bd, Z, W, sb); \
@@ -893,10 +893,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
         } else if (rq_big(m)) {
             // m + 1 > 32: Householder RQ with the windows in shared memory
-            static bool configured = false;
-            if (!configured) {
+            static unsigned configured = 0;  // devices configured (bit per device)
+            if (!(configured & ss::dev_bit(h))) {
                 SS_CUDA_TRY(h, allow_max_smem(h, k_rq_big));
-                configured = true;
+                configured |= ss::dev_bit(h);
             }
             RqDims rd;
             rd.m = m;
@@ -1176,8 +1176,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const int nb0_req = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
     const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
 
-    static bool attrs = false;
-    if (!attrs) {
+    static unsigned attrs = 0;  // devices configured (bit per device)
+    if (!(attrs & ss::dev_bit(h))) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<1>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<2>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<4>));
@@ -1192,7 +1192,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<11, 11>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<21, 21>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_head));
-        attrs = true;
+        attrs |= ss::dev_bit(h);
     }
     // block RQ flavour: row Householder (one warp per shift) unless m+1 > 32
     // or SS_BLOCK_RQ=givens selects the reference's scheduled Givens batch
