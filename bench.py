@@ -331,7 +331,7 @@ def main():
 
     def step():
         rc = L.ss_tf_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C), D.ld(C),
-                          D.ptr(sh_d), len(shifts_loc), args.nb, args.batch, 0.0, D.ptr(G), p,
+                          D.ptr(sh_d), len(shifts_loc), args.nb, args.batch, float("nan"), D.ptr(G), p,
                           D.ptr(fail), ctypes.c_void_p(stream.cuda_stream))
         D.check(h, rc)
         if world > 1:

@@ -61,8 +61,10 @@ int ss_greedy_schedule(int n_rows, int n_cols, int64_t* job_size, int64_t job_ca
  * Ahat n x n (m-Hessenberg, zeros below the m-th subdiagonal), Bhat: only
  * Bhat[0:m, 0:m] is read, Chat p x n.  shifts: s complex128.  nb: window
  * block (>= 1; clamped to what one SM's shared memory holds for this m).
- * batch: shifts per device pass (<= 0: sized from free memory).  rtol <= 0:
- * 1e3*n*eps (solvers.py:95-97).  G: p x (s*m) complex128, leading dim ldg.
+ * batch: shifts per device pass (<= 0: sized from free memory).  rtol: the
+ * relative pivot threshold, used as given (0: only exactly-zero pivots fail,
+ * solvers.py:227); NaN selects the reference default 1e3*n*eps
+ * (solvers.py:95-97).  G: p x (s*m) complex128, leading dim ldg.
  * fail_row[l]: -1, or the 0-based head pivot index that fell below
  * rtol*||Ahat - sigma_l I||_F (G slice is then NaN). */
 int ss_tf_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t lda,

@@ -108,7 +108,7 @@ def tf_eval(Ahat, Bhat, Chat, shifts, nb: int = 32, rtol: float | None = None,
     fail = np.zeros(s, dtype=np.int32)
     rc = lib().orc_tf_eval(n, m, p, _ptr(A), A.shape[0], _ptr(B), B.shape[0], _ptr(C),
                            max(C.shape[0], 1), _ptr(sh), s, nb,
-                           -1.0 if rtol is None else rtol, _ptr(G), max(p, 1), _ptr(fail),
+                           float("nan") if rtol is None else rtol, _ptr(G), max(p, 1), _ptr(fail),
                            threads)
     if rc:
         raise ValueError("bad tf_eval arguments")
@@ -126,7 +126,7 @@ def solve_reduced(Ahat, Bhat, shifts, b_dirs, nb: int = 32, rtol: float | None =
     X = np.zeros((n, s), dtype=np.complex128, order="F")
     fail = np.zeros(s, dtype=np.int32)
     rc = lib().orc_solve_reduced(n, m, _ptr(A), n, _ptr(B), B.shape[0], _ptr(sh), s, _ptr(bd),
-                                 m, nb, -1.0 if rtol is None else rtol, _ptr(X), n,
+                                 m, nb, float("nan") if rtol is None else rtol, _ptr(X), n,
                                  _ptr(fail), threads)
     if rc:
         raise ValueError("bad solve_reduced arguments")

@@ -355,7 +355,7 @@ int orc_tf_eval(int n, int m, int p, const double* A, long lda, const double* B,
                 const double* C, long ldc, const zc* shifts, int s, int nb, double rtol,
                 zc* G, long ldg, int* fail, int nthreads) {
     if (n < 1 || m < 1 || m > n || p < 0 || nb < 1 || s < 0) return -1;
-    if (rtol <= 0.0) rtol = 1e3 * n * ORC_EPS;
+    if (isnan(rtol)) rtol = 1e3 * n * ORC_EPS; /* NaN: reference default */
     double fro2, tr;
     orc_fro2_trace(n, A, lda, &fro2, &tr);
     zc* Bh = (zc*)malloc(sizeof(zc) * (size_t)m * m);
@@ -397,7 +397,7 @@ int orc_solve_reduced(int n, int m, const double* A, long lda, const double* B, 
                       const zc* shifts, int s, const zc* bdirs, long ldbd, int nb,
                       double rtol, zc* Xo, long ldx, int* fail, int nthreads) {
     if (n < 1 || m < 1 || m > n || nb < 1 || s < 0) return -1;
-    if (rtol <= 0.0) rtol = 1e3 * n * ORC_EPS;
+    if (isnan(rtol)) rtol = 1e3 * n * ORC_EPS; /* NaN: reference default */
     double fro2, tr;
     orc_fro2_trace(n, A, lda, &fro2, &tr);
     orc_set_threads(nthreads);

@@ -190,10 +190,12 @@ int ss_create(ss_handle** out, int device) {
     if (!out) return SS_EARG;
     *out = nullptr;
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev || device >= 64) {
         cudaGetLastError();
         return SS_ECUDA;
     }
+    int prev = 0;
+    cudaGetDevice(&prev);
     if (cudaSetDevice(device) != cudaSuccess) return SS_ECUDA;
     ss_handle* h = new ss_handle();
     h->device = device;
@@ -205,14 +207,18 @@ int ss_create(ss_handle** out, int device) {
         cudaEventCreate(&h->ev_a) != cudaSuccess || cudaEventCreate(&h->ev_b) != cudaSuccess) {
         cudaGetLastError();
         delete h;
+        cudaSetDevice(prev);
         return SS_ECUDA;
     }
+    cudaSetDevice(prev);  // the caller's current device is left as it was
     *out = h;
     return SS_OK;
 }
 
 void ss_destroy(ss_handle* h) {
     if (!h) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     for (auto& kv : h->sched) {
@@ -228,9 +234,12 @@ void ss_destroy(ss_handle* h) {
     }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    for (auto e : h->chunk_ev) cudaEventDestroy(e);
     if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->ev_b) cudaEventDestroy(h->ev_b);
     delete h;
+    cudaSetDevice(prev);
 }
 
 const char* ss_last_error(const ss_handle* h) { return h ? h->err.c_str() : "null handle"; }

@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cstdint>
 #include <map>
 #include <string>
@@ -77,8 +79,34 @@ struct ss_handle {
 namespace ss {
 
 // cudaFuncSetAttribute acts on the current device: the launch helpers keep
-// one "configured" bit per device (handles on several devices in one process)
-inline unsigned dev_bit(const ss_handle* h) { return 1u << (h->device & 31); }
+// one "configured" bit per device (handles on several devices in one
+// process; ss_create rejects device ids >= 64).  Atomic: handles are per
+// thread, so first calls may race; configuring twice is harmless.
+struct DevMask {
+    std::atomic<uint64_t> bits{0};
+    bool has(const ss_handle* h) const;
+    void set(const ss_handle* h);
+};
+inline bool DevMask::has(const ss_handle* h) const {
+    return (bits.load(std::memory_order_acquire) >> h->device) & 1u;
+}
+inline void DevMask::set(const ss_handle* h) {
+    bits.fetch_or(uint64_t(1) << h->device, std::memory_order_acq_rel);
+}
+
+// Makes the handle's device current for one entry point and restores the
+// caller's device on return.
+struct DevGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DevGuard(int device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        err = cudaSetDevice(device);
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 int set_err(ss_handle* h, int code, const std::string& msg);
 int cuda_err(ss_handle* h, cudaError_t e, const char* what);

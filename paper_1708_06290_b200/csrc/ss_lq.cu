@@ -455,8 +455,9 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     if (s == 0) return SS_OK;
     if (!Ahat || !shifts || !rhs || !X || !fail_row) return ss::set_err(h, SS_EARG, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    SS_CUDA_TRY(h, cudaSetDevice(h->device));
-    const double rt = rtol > 0.0 ? rtol : 1e3 * n * 2.220446049250313e-16;
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
+    const double rt = std::isnan(rtol) ? 1e3 * n * 2.220446049250313e-16 : rtol;  // NaN: default
     const int nb0 = std::max(1, std::min(std::min(nb, kLqMaxNb), std::max(n - m, 1)));
     const int mp = m + 1;
     const int64_t LDS = ((int64_t)2 * n + 7) & ~(int64_t)7;
@@ -481,10 +482,10 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     double2* Sb = (double2*)h->ws;
     double2* Pb = Sb + (size_t)sb_max * mp * LDS;
     double* tolb = (double*)(Pb + (size_t)sb_max * (nb0 + mp) * mp);
-    static unsigned attrs = 0;  // devices configured (bit per device)
-    if (!(attrs & ss::dev_bit(h))) {
+    static ss::DevMask attrs;  // devices configured
+    if (!attrs.has(h)) {
         SS_CUDA_TRY(h, allow_smem(h, k_tupd));
-        attrs |= ss::dev_bit(h);
+        attrs.set(h);
     }
     for (int64_t lo = 0; lo < s; lo += sb_max) {
         const int sb = (int)std::min<int64_t>(sb_max, s - lo);

@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(512) k_dfma_chain(int iters, double x, double 
 
 extern "C" int ss_probe_dfma_peak(ss_handle* h, double* tflops) {
     if (!h || !tflops) return SS_EARG;
-    SS_CUDA_TRY(h, cudaSetDevice(h->device));
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
     const int blocks = h->num_sms * 4, threads = 512, iters = 2048;
     cudaEvent_t a, b;
     SS_CUDA_TRY(h, cudaEventCreate(&a));

@@ -398,7 +398,8 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
         return ss::set_err(h, SS_EDIM, "leading dimension too small");
     if (block_size < 1) return ss::set_err(h, SS_EARG, "block_size must be positive");
     if (!A || !B || (p > 0 && !C)) return ss::set_err(h, SS_EARG, "null pointer");
-    SS_CUDA_TRY(h, cudaSetDevice(h->device));
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
     cudaStream_t st = (cudaStream_t)stream;
     Ctx x{h, st};
     cudaEvent_t e0 = ss::timing_begin(h, st);

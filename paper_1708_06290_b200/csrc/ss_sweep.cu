@@ -30,7 +30,6 @@
 // ss_tf_eval_stream additionally streams Ahat from pinned host memory in the
 // order the sweep consumes its columns (copy stream + one event per chunk).
 #include <algorithm>
-#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -377,19 +376,19 @@ int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStrea
                     const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
     if (threads > 256) {
         // K-split with several column blocks per shift (m > 31): up to 10 warps
-        static unsigned configured_w = 0;  // devices configured (bit per device)
-        if (!(configured_w & ss::dev_bit(h))) {
+        static ss::DevMask configured_w;  // devices configured
+        if (!configured_w.has(h)) {
             SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320>));
-            configured_w |= ss::dev_bit(h);
+            configured_w.set(h);
         }
         k_update<G, C, EXACT, 320><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
         SS_LAUNCH_CHECK(h);
         return SS_OK;
     }
-    static unsigned configured = 0;  // devices configured (bit per device)
-    if (!(configured & ss::dev_bit(h))) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT>));
-        configured |= ss::dev_bit(h);
+        configured.set(h);
     }
     k_update<G, C, EXACT><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -399,10 +398,10 @@ int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStrea
 template <int G, int C, bool ZID>
 int launch_update_ws_z(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, const UpdDims& u,
                        const double2* zin, double2* zout, const double2* pbuf) {
-    static unsigned configured = 0;  // devices configured (bit per device)
-    if (!(configured & ss::dev_bit(h))) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_update_ws<G, C, ZID>));
-        configured |= ss::dev_bit(h);
+        configured.set(h);
     }
     k_update_ws<G, C, ZID><<<grid, kWsThreads, smem, st>>>(u, zin, zout, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -419,10 +418,10 @@ int launch_update_ws_t(ss_handle* h, dim3 grid, size_t smem, cudaStream_t st, co
 template <int G, int C, int R, int NPAIR, int NST, bool ZID, int NCB, bool MSH = false>
 int launch_far_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                  const double2* pbuf) {
-    static unsigned configured = 0;  // devices configured (bit per device)
-    if (!(configured & ss::dev_bit(h))) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_far<G, C, R, NPAIR, NST, ZID, NCB, MSH>));
-        configured |= ss::dev_bit(h);
+        configured.set(h);
     }
     k_far<G, C, R, NPAIR, NST, ZID, NCB, MSH><<<grid, far_threads(NPAIR), smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -440,8 +439,8 @@ struct FarShape {
 
 FarShape far_shape(const UpdTile& t) {
     // measured on B200 (config 2): R = 8 rows per lane (3 pairs, 255
-    // registers, spills) was slower than R = 2G with 4 pairs / 8 stages
-    if (t.G == 2 && t.C == 5 && getenv("SS_FAR_P3")) return FarShape{2, 5, 4, 3, 6, 1};
+    // registers, spills) and 3 pairs x 6 stages were slower than R = 2G with
+    // 4 pairs / 8 stages
     return FarShape{t.G, t.C, 2 * t.G, 4, 8, 1};
 }
 
@@ -453,7 +452,7 @@ int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStrea
         f.NCB == KB)                                                                             \
         return u.zid ? launch_far_z<GG, CC, RR, NP, NS, true, KB>(h, grid, smem, st, u, z, pbuf)  \
                      : launch_far_z<GG, CC, RR, NP, NS, false, KB>(h, grid, smem, st, u, z, pbuf);
-    SS_FAR(2, 5, 4, 4, 8, 1) SS_FAR(2, 5, 4, 3, 6, 1) SS_FAR(2, 5, 4, 4, 4, 2)
+    SS_FAR(2, 5, 4, 4, 8, 1) SS_FAR(2, 5, 4, 4, 4, 2)
     SS_FAR(2, 4, 4, 4, 8, 1)
     SS_FAR(1, 1, 2, 4, 8, 1) SS_FAR(1, 2, 2, 4, 8, 1) SS_FAR(1, 3, 2, 4, 8, 1) SS_FAR(1, 4, 2, 4, 8, 1)
     SS_FAR(1, 5, 2, 4, 8, 1) SS_FAR(1, 6, 2, 4, 8, 1) SS_FAR(1, 7, 2, 4, 8, 1) SS_FAR(1, 8, 2, 4, 8, 1)
@@ -468,10 +467,10 @@ int launch_far(ss_handle* h, const FarShape& f, int grid, size_t smem, cudaStrea
 template <bool ZID>
 int launch_far4_z(ss_handle* h, int grid, size_t smem, cudaStream_t st, const UpdDims& u, double2* z,
                   const double2* pbuf) {
-    static unsigned configured = 0;  // devices configured (bit per device)
-    if (!(configured & ss::dev_bit(h))) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_far4<2, 5, 4, ZID>));
-        configured |= ss::dev_bit(h);
+        configured.set(h);
     }
     k_far4<2, 5, 4, ZID><<<grid, kFar4Threads, smem, st>>>(u, z, pbuf);
     SS_LAUNCH_CHECK(h);
@@ -592,10 +591,10 @@ int launch_block(ss_handle* h, int m, int sb, size_t smem, cudaStream_t st, cons
     switch (m) {
 #define SS_CASE(K)                                                        \
     case K: {                                                             \
-        static unsigned configured = 0;                                   \
-        if (!(configured & ss::dev_bit(h))) {                                                \
+        static ss::DevMask configured;                                   \
+        if (!configured.has(h)) {                                                \
             SS_CUDA_TRY(h, allow_max_smem(h, k_block<K, kBlkShiftsPerWarp>)); \
-            configured |= ss::dev_bit(h);                                            \
+            configured.set(h);                                            \
         }                                                                 \
         k_block<K, kBlkShiftsPerWarp>                                     \
             <<<(sb + kBlkShiftsPerWarp - 1) / kBlkShiftsPerWarp, 32, smem, st>>>(bd, Z, W, sb); \
@@ -723,9 +722,6 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 // DFMA per column of m unless it is the identity) and the epilogue
                 u.jh = u.zid ? nbp / 2 : std::max(0, std::min(nbp, (nbp - 2 * m) / 2 - 1));
                 u.flags = 0;
-                if (const char* e = getenv(u.zid ? "SS_FAR_JH1" : "SS_FAR_JH"))
-                    u.jh = std::max(0, std::min(nbp, u.jh + atoi(e)));
-                if (getenv("SS_FAR_SPIN")) u.flags |= 1;
                 // algorithmic flops: structurally nonzero panel entries of the
                 // far rows (Chat rows dense, identity rows one per column,
                 // Ahat rows above the band dense) x m complex columns
@@ -741,7 +737,6 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 }
                 if (r0 > std::max(rlo, ptop)) nnz += (double)(r0 - std::max(rlo, ptop)) * nbp;
                 const double fl_alg = 4.0 * m * nnz * sb;
-                dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
                 cudaEvent_t ev = ss::timing_begin(h, st);
                 int rc;
                 if (far4) {
@@ -751,7 +746,6 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                     const int extra0 = (u.zid ? 1 : 2 * m) + 4;
                     int T = (nbp + extra0 + 4 + 3) / 4;
                     int j1 = std::max(0, T - extra0);
-                    if (const char* e = getenv("SS_FAR4_J")) j1 = std::max(0, j1 + atoi(e));
                     const int rest = (nbp - j1);
                     const int q = (rest - 2) / 3;
                     u.jq[0] = std::min(nbp, j1);
@@ -761,8 +755,6 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                     const int grid = (int)std::min<int64_t>(units, h->num_sms);
                     rc = u.zid ? launch_far4_z<true>(h, grid, far4_smem_bytes<2, 5, 4>(nbp, m), st, u, B.Z, B.P)
                                : launch_far4_z<false>(h, grid, far4_smem_bytes<2, 5, 4>(nbp, m), st, u, B.Z, B.P);
-                } else if (getenv("SS_FAR_CLASSIC")) {
-                    rc = launch_update_ws(h, tile, gw, ws_smem_bytes(nbp, m), st, u, B.Z, B.Z, B.P);
                 } else {
                     const FarShape f = m == 20 ? FarShape{2, 5, 4, 4, 4, 2} : far_shape(tile);
                     const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * sb;
@@ -800,44 +792,25 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             ss::timing_end(h, st, ev, ss::PH_RQ);
             return SS_OK;
         };
-        const bool hprof = getenv("SS_HOST_PROF") != nullptr;
-        auto hnow = [] { return std::chrono::steady_clock::now(); };
-        auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
-            return std::chrono::duration<double, std::milli>(b - a).count();
-        };
-        auto block_p = block;
-        auto far_p = far_update;
-        auto block_t = [&](int ko, int NBo, int woff, int wprod) -> int {
-            auto t0 = hnow();
-            int rc = block_p(ko, NBo, woff, wprod);
-            if (hprof && hms(t0, hnow()) > 1.0) fprintf(stderr, "[host] block ko=%d %.2f ms\n", ko, hms(t0, hnow()));
-            return rc;
-        };
-        auto far_t = [&](int rlo, int r0, int c0, int ncols, int woff) -> int {
-            auto t0 = hnow();
-            int rc = far_p(rlo, r0, c0, ncols, woff);
-            if (hprof && hms(t0, hnow()) > 1.0) fprintf(stderr, "[host] far r0=%d %.2f ms\n", r0, hms(t0, hnow()));
-            return rc;
-        };
         for (int ko = n; ko >= m + 1;) {
             const int NBa = std::min(kBlkNB, ko - m);
             const int c0a = ko - m - NBa, r0a = ptop + ko - NBa;
             const int kb = ko - NBa;  // block B's k
             if (pairing && kb - m >= kBlkNB) {
                 const int c0b = c0a - kBlkNB, r0b = r0a - kBlkNB;
-                int rc = block_t(ko, NBa, kBlkNB, 0);
+                int rc = block(ko, NBa, kBlkNB, 0);
                 if (rc) return rc;
-                rc = far_t(r0b, r0a, c0a, NBa, kBlkNB);  // near: B's rows
+                rc = far_update(r0b, r0a, c0a, NBa, kBlkNB);  // near: B's rows
                 if (rc) return rc;
-                rc = block_t(kb, kBlkNB, 0, NBa + m);
+                rc = block(kb, kBlkNB, 0, NBa + m);
                 if (rc) return rc;
-                rc = far_t(a.mode == 1 ? c0b : 0, r0b, c0b, kBlkNB + NBa, 0);
+                rc = far_update(a.mode == 1 ? c0b : 0, r0b, c0b, kBlkNB + NBa, 0);
                 if (rc) return rc;
                 ko = kb - kBlkNB;
             } else {
-                int rc = block_t(ko, NBa, 0, 0);
+                int rc = block(ko, NBa, 0, 0);
                 if (rc) return rc;
-                rc = far_t(a.mode == 1 ? c0a : 0, r0a, c0a, NBa, 0);
+                rc = far_update(a.mode == 1 ? c0a : 0, r0a, c0a, NBa, 0);
                 if (rc) return rc;
                 ko = kb;
             }
@@ -893,10 +866,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             else k_rq_house<32><<<sb, 32, sm, st>>>(rd, B.Z, B.P);
         } else if (rq_big(m)) {
             // m + 1 > 32: Householder RQ with the windows in shared memory
-            static unsigned configured = 0;  // devices configured (bit per device)
-            if (!(configured & ss::dev_bit(h))) {
+            static ss::DevMask configured;  // devices configured
+            if (!configured.has(h)) {
                 SS_CUDA_TRY(h, allow_max_smem(h, k_rq_big));
-                configured |= ss::dev_bit(h);
+                configured.set(h);
             }
             RqDims rd;
             rd.m = m;
@@ -961,8 +934,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         // one block covers all m columns: twice the warps on the same staging
         // (also for several column blocks per shift when the block RQ is the
         // wide-window one: 2 nws warps per shift, SS_UPD_KSPLIT1=1 disables)
-        u.ksplit = ((nws == 1 && tile.exact) ||
-                    (nws > 1 && tile.exact && rq_big(m) && 64 * nws <= 320 && !getenv("SS_UPD_KSPLIT1")))
+        u.ksplit = ((nws == 1 && tile.exact) || (nws > 1 && tile.exact && rq_big(m) && 64 * nws <= 320))
                        ? 2
                        : 1;  // scratch = the shift's m x 64 Z2 stage
         u.jh = std::max(0, std::min(s.nb, (s.nb - 2 * m) / 2));
@@ -988,8 +960,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         const double fl_alg = 4.0 * m * nnz * sb;
         ev = ss::timing_begin(h, st);
         int rc;
-        const bool ws = nws == 1 && tile.exact && tile.G * tile.C == m && !getenv("SS_UPDATE_CLASSIC") &&
-                        !(m == 1 && !getenv("SS_NO_MSH")) &&
+        const bool ws = nws == 1 && tile.exact && tile.G * tile.C == m && m != 1 &&
                         ws_smem_bytes(s.nb, m) + 1024 <= h->smem_optin;
         if (ws) {
             // warp-specialised pipeline: 1 producer + 4 consumer pairs, SG shifts per CTA
@@ -1000,8 +971,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             dim3 gw((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
             rc = launch_update_ws(h, tile, gw, ws_smem_bytes(s.nb, m), st, u, B.Z, B.Z,
                                   B.P);
-        } else if (m == 1 && !getenv("SS_UPDATE_CLASSIC") && !getenv("SS_NO_MSH") &&
-                   far_smem_bytes(s.nb, 10, 64, 8) + 1024 <= h->smem_optin) {
+        } else if (m == 1 && far_smem_bytes(s.nb, 10, 64, 8) + 1024 <= h->smem_optin) {
             // m = 1: ten shifts per unit as the ten columns of the m = 10 tile
             FarShape f{2, 5, 4, 4, 8, 1};
             f.MSH = true;
@@ -1017,7 +987,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             UpdDims um = u;
             um.nc = s.nb + 1;
             rc = launch_far(h, f, grid, far_smem_bytes(s.nb, 10, f.tile(), f.NST), st, um, B.Z, B.P);
-        } else if (nws == 2 && tile.exact && tile.G == 2 && tile.C == 5 && !getenv("SS_UPDATE_CLASSIC") &&
+        } else if (nws == 2 && tile.exact && tile.G == 2 && tile.C == 5 &&
                    far_smem_bytes(s.nb, m, 64, 4) + 1024 <= h->smem_optin) {
             // m = 20: persistent far kernel with two column blocks per unit
             // (one group of two pairs shares the unit's stage)
@@ -1171,13 +1141,16 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : n;
     if (a.s == 0) return SS_OK;
-    SS_CUDA_TRY(h, cudaSetDevice(h->device));
-    const double rtol = a.rtol > 0.0 ? a.rtol : 1e3 * n * 2.220446049250313e-16;
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
+    // NaN selects the reference default 1e3 n eps (solvers.py:95-97); any other
+    // value is used as given (0: only exactly-zero pivots fail, solvers.py:227)
+    const double rtol = std::isnan(a.rtol) ? 1e3 * n * 2.220446049250313e-16 : a.rtol;
     const int nb0_req = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
     const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
 
-    static unsigned attrs = 0;  // devices configured (bit per device)
-    if (!(attrs & ss::dev_bit(h))) {
+    static ss::DevMask attrs;  // devices configured
+    if (!attrs.has(h)) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<1>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<2>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq<4>));
@@ -1192,7 +1165,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<11, 11>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_rq_house<21, 21>));
         SS_CUDA_TRY(h, allow_max_smem(h, k_head));
-        attrs |= ss::dev_bit(h);
+        attrs.set(h);
     }
     // block RQ flavour: row Householder (one warp per shift) unless m+1 > 32
     // or SS_BLOCK_RQ=givens selects the reference's scheduled Givens batch
@@ -1201,7 +1174,6 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     const UpdTile tile = pick_tile(m);
     // the Householder block RQ maps one block row to one thread of two warps
     int nb_big = kRqBigNb;
-    if (const char* e = getenv("SS_BIG_NB")) nb_big = std::max(8, std::min(96, atoi(e)));
     // the generic update stages the whole (nb + m) x m P per shift: the
     // widest window whose update and RQ fit one SM's shared memory
     while (nb_big > 8 && (upd_smem_bytes(nb_big, m, 1) + 1024 > h->smem_optin ||
@@ -1215,7 +1187,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // (m = 20: the far passes run k_far with two column blocks per unit)
     const bool two_level = use_house && block_supported(m) && tile.exact &&
                            (tile.G * tile.C == m || (m == 20 && tile.G == 2 && tile.C == 5)) &&
-                           !getenv("SS_ONE_LEVEL") && !getenv("SS_UPDATE_CLASSIC") &&
+                           !getenv("SS_ONE_LEVEL") &&
                            far_smem_bytes(64, m, 64, m == 20 ? 4 : 8) + 1024 <= h->smem_optin;
     // fro2 / trace for the per-shift singularity thresholds (streamed Ahat:
     // after the last chunk, just before the first head)
@@ -1279,11 +1251,10 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // (the persistent far-row kernel -- two-level sweep, and the one-level
     // m = 20 update -- owns every SM, so it runs on one stream; otherwise
     // two halves overlap)
-    const char* sv = getenv("SS_STREAMS");
     const bool far_m20 = !two_level && tile.exact && tile.G == 2 && tile.C == 5 &&
-                         (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2 && !getenv("SS_UPDATE_CLASSIC");
-    const bool far_m1 = !two_level && m == 1 && !getenv("SS_UPDATE_CLASSIC") && !getenv("SS_NO_MSH");
-    int NS = sv ? std::max(1, std::min(2, atoi(sv))) : ((two_level || far_m20 || far_m1) ? 1 : 2);
+                         (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2;
+    const bool far_m1 = !two_level && m == 1;
+    int NS = (two_level || far_m20 || far_m1) ? 1 : 2;
     if (sb_max < 64 || feed.on) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
@@ -1409,6 +1380,8 @@ int ss_pspec_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t
     int rc = ss_tf_eval(h, n, m, p, Ahat, lda, Bhat, ldb, Chat, ldc, shifts, s, nb, batch, rtol, G,
                         ldg, fail_row, stream);
     if (rc || s == 0) return rc;
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
     cudaStream_t st = (cudaStream_t)stream;
     cudaEvent_t ev = ss::timing_begin(h, st);
     k_pnorm<<<(unsigned)s, 32, 0, st>>>(p, m, (const double2*)G, ldg, fail_row, norms);

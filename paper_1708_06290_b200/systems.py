@@ -31,19 +31,19 @@ class SystemBundle:
 
 
 def random_stable_system(n: int, m: int, p: int, seed: int = 0, margin: float = 0.05,
-                         circular: bool | None = None) -> SystemBundle:
+                         circular: bool = False) -> SystemBundle:
     """Seeded Gaussian triple with A shifted to a negative spectral abscissa.
 
-    Same rng call order as the reference generator, so for ``circular=False``
-    the triple is identical to ``shiftsolve.random_stable_system``.  With
-    ``circular=True`` (default for n >= 4000) the O(n^3) eigenvalue
-    computation is replaced by the circular-law bound: a standard Gaussian
-    n x n matrix has spectral radius ~sqrt(n), so A - 1.1 sqrt(n) I is
-    stable with abscissa ~ -0.1 sqrt(n) (SURVEY.md 8(d), documented deviation;
-    the solve cost does not depend on the values).
+    Default: the reference generator (systems.py:71-86) -- same rng call
+    order and the eigenvalue-based shift, so the triple is identical to
+    ``shiftsolve.random_stable_system(n, m, p, seed)``.
+
+    ``circular=True`` replaces the O(n^3) eigenvalue computation by the
+    circular-law bound: a standard Gaussian n x n matrix has spectral radius
+    ~sqrt(n), so A - 1.1 sqrt(n) I is stable with abscissa ~ -0.1 sqrt(n).
+    SURVEY.md 8(d) uses it for n >= 10000 (eigvals takes ~20 min at
+    n = 20000); it is a documented deviation and carries a distinct name.
     """
-    if circular is None:
-        circular = n >= 4000
     rng = np.random.default_rng(seed)
     A = np.asfortranarray(rng.standard_normal((n, n)))
     if circular:
@@ -53,7 +53,8 @@ def random_stable_system(n: int, m: int, p: int, seed: int = 0, margin: float = 
         A -= (abscissa + margin * np.sqrt(n)) * np.eye(n)
     B = np.asfortranarray(rng.standard_normal((n, m)))
     C = np.asfortranarray(rng.standard_normal((p, n)))
-    return SystemBundle(A=A, B=B, C=C, name=f"random-n{n}-m{m}-p{p}-s{seed}")
+    tag = "circular" if circular else "random"
+    return SystemBundle(A=A, B=B, C=C, name=f"{tag}-n{n}-m{m}-p{p}-s{seed}")
 
 
 def config_shifts(cfg: int, n: int, seed: int | None = None) -> np.ndarray:

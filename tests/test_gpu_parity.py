@@ -140,6 +140,29 @@ def test_failure_isolation_bitwise():
     assert np.isnan(redm.x[:, 7]).all()
 
 
+def test_singular_rtol_is_used_as_given():
+    """singular_rtol=0.0 means only exactly-zero pivots fail (reference
+    solvers.py:227 ``abs(piv) <= rtol * scale``); it must not fall back to
+    the default 1e3 n eps.  A huge rtol flags every shift."""
+    sysb = ss.random_stable_system(16, 2, 2, seed=8, circular=False)
+    chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    ev = np.linalg.eigvals(chf.Ahat)[0]
+    shifts = np.array([ev * (1 + 1e-14), 1j, ev])
+    default = ss.eval_transfer_function(chf, shifts, nb=4, on_singular="mark")
+    assert 0 in default.failures and 2 in default.failures
+    zero = ss.eval_transfer_function(chf, shifts, nb=4, on_singular="mark", singular_rtol=0.0)
+    G_o, f_o = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts, nb=4, rtol=0.0)
+    assert zero.failures == {int(l): int(f_o[l]) for l in np.nonzero(f_o >= 0)[0]}
+    assert 1 not in zero.failures and 0 not in zero.failures
+    assert np.isfinite(zero.value(0)).all()
+    np.testing.assert_array_equal(zero.value(1), default.value(1))
+    red = ss.solve_shifted_reduced(chf, shifts[:2], np.ones((2, 2)), nb=4, on_singular="mark",
+                                   singular_rtol=0.0)
+    assert red.failures == {}
+    big = ss.eval_transfer_function(chf, shifts, nb=4, on_singular="mark", singular_rtol=1e6)
+    assert sorted(big.failures) == [0, 1, 2]
+
+
 def test_singular_shift_raises_by_default():
     sysb = ss.random_stable_system(16, 2, 2, seed=8, circular=False)
     chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)

@@ -51,7 +51,7 @@ def main():
 
     def call():
         rc = L.ss_tf_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C), D.ld(C),
-                          D.ptr(sh), s, args.nb, 0, 0.0, D.ptr(G), p, D.ptr(fail),
+                          D.ptr(sh), s, args.nb, 0, float("nan"), D.ptr(G), p, D.ptr(fail),
                           ctypes.c_void_p(st.cuda_stream))
         D.check(h, rc)
 

@@ -16,7 +16,7 @@ for cfg in (1, 3, 2):
     h = _lib.handle(0); L = _lib.load(); st = torch.cuda.current_stream(dev)
     def call():
         D.check(h, L.ss_tf_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C), D.ld(C),
-                                D.ptr(sh), s, 64, 0, 0.0, D.ptr(G), p, D.ptr(fail), ctypes.c_void_p(st.cuda_stream)))
+                                D.ptr(sh), s, 64, 0, float("nan"), D.ptr(G), p, D.ptr(fail), ctypes.c_void_p(st.cuda_stream)))
     for _ in range(3): call()
     torch.cuda.synchronize()
     enq, gpu = [], []

@@ -20,7 +20,7 @@ h = _lib.handle(0); L = _lib.load()
 stream = torch.cuda.current_stream(dev)
 def step():
     D.check(h, L.ss_tf_eval(h.ptr, n, m, p, D.ptr(A), D.ld(A), D.ptr(B), D.ld(B), D.ptr(C), D.ld(C),
-                            D.ptr(sh), s, 64, 0, 0.0, D.ptr(G), p, D.ptr(fail),
+                            D.ptr(sh), s, 64, 0, float("nan"), D.ptr(G), p, D.ptr(fail),
                             ctypes.c_void_p(stream.cuda_stream)))
 for _ in range(3): step()
 torch.cuda.synchronize()
