@@ -59,6 +59,10 @@ def lib():
         L.orc_tf_eval.restype = I
         L.orc_solve_reduced.argtypes = [I, I, P, Lg, P, Lg, P, I, P, Lg, I, D, P, Lg, P, I]
         L.orc_solve_reduced.restype = I
+        L.orc_tf_eval_diag.argtypes = L.orc_tf_eval.argtypes + [P]
+        L.orc_tf_eval_diag.restype = I
+        L.orc_solve_reduced_diag.argtypes = L.orc_solve_reduced.argtypes + [P]
+        L.orc_solve_reduced_diag.restype = I
         L.orc_reduce_chf.argtypes = [I, I, I, P, Lg, P, Lg, P, Lg, P, Lg]
         L.orc_reduce_chf.restype = I
         _lib = L
@@ -98,26 +102,32 @@ def _f64(a):
 
 
 def tf_eval(Ahat, Bhat, Chat, shifts, nb: int = 32, rtol: float | None = None,
-            threads: int = 0):
-    """solvers.py:234-271 -> (G p x s*m, fail int32[s] (-1 ok / head index))."""
+            threads: int = 0, diag: bool = False):
+    """solvers.py:234-271 -> (G p x s*m, fail int32[s] (-1 ok / head index)).
+
+    ``diag=True`` also returns an (s, 3) array per shift: kappa =
+    ||Ahat - sigma I||_F / min |R_ii| (SURVEY 8(d) condition estimate), the
+    smallest computed head pivot / ||Ahat - sigma I||_F (what the singular
+    test compares with rtol) and sum log |R_ii| (log |det(Ahat - sigma I)|)."""
     A, B, C = _f64(Ahat), _f64(Bhat), _f64(Chat)
     n, m, p = A.shape[0], B.shape[1], C.shape[0]
     sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.complex128).ravel())
     s = len(sh)
     G = np.zeros((p, s * m), dtype=np.complex128, order="F")
     fail = np.zeros(s, dtype=np.int32)
-    rc = lib().orc_tf_eval(n, m, p, _ptr(A), A.shape[0], _ptr(B), B.shape[0], _ptr(C),
-                           max(C.shape[0], 1), _ptr(sh), s, nb,
-                           float("nan") if rtol is None else rtol, _ptr(G), max(p, 1), _ptr(fail),
-                           threads)
+    dg = np.zeros((s, 3)) if diag else None
+    rc = lib().orc_tf_eval_diag(n, m, p, _ptr(A), A.shape[0], _ptr(B), B.shape[0], _ptr(C),
+                                max(C.shape[0], 1), _ptr(sh), s, nb,
+                                float("nan") if rtol is None else rtol, _ptr(G), max(p, 1),
+                                _ptr(fail), threads, _ptr(dg) if diag else None)
     if rc:
         raise ValueError("bad tf_eval arguments")
-    return G, fail
+    return (G, fail, dg) if diag else (G, fail)
 
 
 def solve_reduced(Ahat, Bhat, shifts, b_dirs, nb: int = 32, rtol: float | None = None,
-                  threads: int = 0):
-    """solvers.py:274-313 -> (X n x s, fail int32[s])."""
+                  threads: int = 0, diag: bool = False):
+    """solvers.py:274-313 -> (X n x s, fail int32[s]) (+ diag as in tf_eval)."""
     A, B = _f64(Ahat), _f64(Bhat)
     n, m = A.shape[0], B.shape[1]
     sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.complex128).ravel())
@@ -125,12 +135,14 @@ def solve_reduced(Ahat, Bhat, shifts, b_dirs, nb: int = 32, rtol: float | None =
     bd = np.asfortranarray(np.asarray(b_dirs, dtype=np.complex128).reshape(m, s))
     X = np.zeros((n, s), dtype=np.complex128, order="F")
     fail = np.zeros(s, dtype=np.int32)
-    rc = lib().orc_solve_reduced(n, m, _ptr(A), n, _ptr(B), B.shape[0], _ptr(sh), s, _ptr(bd),
-                                 m, nb, float("nan") if rtol is None else rtol, _ptr(X), n,
-                                 _ptr(fail), threads)
+    dg = np.zeros((s, 3)) if diag else None
+    rc = lib().orc_solve_reduced_diag(n, m, _ptr(A), n, _ptr(B), B.shape[0], _ptr(sh), s,
+                                      _ptr(bd), m, nb, float("nan") if rtol is None else rtol,
+                                      _ptr(X), n, _ptr(fail), threads,
+                                      _ptr(dg) if diag else None)
     if rc:
         raise ValueError("bad solve_reduced arguments")
-    return X, fail
+    return (X, fail, dg) if diag else (X, fail)
 
 
 def reduce_chf(A, B, C, accumulate: bool = False):

@@ -214,9 +214,14 @@ static inline double orc_panel(int i, int col, int ptop, const double* A, long l
     return A[(i - ptop) + (long)col * lda];
 }
 
+/* rdiag (nullable): rdiag[0] = min |R_ii|, rdiag[1] = sum log|R_ii| over the
+   window blocks' R diagonals (after the RQ a block is [0 | R] with R nb x nb
+   upper triangular in its last nb columns); the head pivots are added by
+   orc_head_solve.  These give the condition estimate of SURVEY 8(d)
+   (||Ahat - sigma I||_F / min |R_ii|) and a determinant check. */
 static void orc_sweep_one(int n, int m, int ptop, const double* A, long lda,
                           const double* top, long ldt, zc sigma, int nb0, zc* z2,
-                          orc_ws* ws) {
+                          orc_ws* ws, double* rdiag) {
     const long ld = ptop + n;
     /* seed: last m columns of the stack with the shift on A's diagonal */
     for (int c = 0; c < m; ++c) {
@@ -253,6 +258,12 @@ static void orc_sweep_one(int n, int m, int ptop, const double* A, long lda,
         memset(P, 0, sizeof(zc) * (size_t)nc * nc);
         for (int i = 0; i < nc; ++i) P[i + (long)i * nc] = 1.0;
         orc_factor_block(Zb, nb, P, nc, sc->steps, sc->job, sc->info);
+        if (rdiag)
+            for (int t = 0; t < nb; ++t) {
+                double a = cabs(Zb[t + (long)(m + t) * nb]);
+                if (a < rdiag[0]) rdiag[0] = a;
+                rdiag[1] += log(a);
+            }
         /* update_shift (solvers.py:187-191): z2[:r0] = z2[:r0] @ P[nb:nb+m] */
         zc* tmp = ws->tmp;
         for (int c = 0; c < m; ++c) {
@@ -296,7 +307,7 @@ static void orc_sweep_one(int n, int m, int ptop, const double* A, long lda,
 
 /* solvers.py:204-231  _head_solve_rq for one shift; returns -1 or pivot i */
 static int orc_head_solve(zc* z2, long ld, int ptop, int m, const zc* rhs, int q, double tol,
-                          zc* X /* m x q, ld m */) {
+                          zc* X /* m x q, ld m */, double* rdiag, double* pmin) {
     for (int i = 0; i < m * q; ++i) X[i] = 0.0;
     for (int i = m - 1; i >= 0; --i) {
         int row = ptop + i;
@@ -308,6 +319,12 @@ static int orc_head_solve(zc* z2, long ld, int ptop, int m, const zc* rhs, int q
             z2[row + i * ld] = rr;
         }
         zc piv = z2[row + i * ld];
+        if (rdiag) {
+            double a = cabs(piv);
+            if (a < rdiag[0]) rdiag[0] = a;
+            rdiag[1] += log(a);
+        }
+        if (pmin && cabs(piv) < *pmin) *pmin = cabs(piv);
         if (cabs(piv) <= tol) return i;
         for (int c = 0; c < q; ++c) {
             zc acc = 0.0;
@@ -351,9 +368,28 @@ static void orc_set_threads(int nthreads) {
 /* G: p x (s*m) complex, ld ldg; fail[l] = -1 or the failing head index. */
 /* Failed slices are NaN (solvers.py:256).                               */
 /* ------------------------------------------------------------------ */
+/* diag (nullable): per shift 3 doubles -- kappa = ||Ahat - sigma I||_F /
+   min |R_ii| (SURVEY 8(d) condition estimate), the smallest computed head
+   pivot relative to ||Ahat - sigma I||_F (the quantity the singular test
+   compares with rtol, solvers.py:226-228), and sum log |R_ii| (=
+   log |det(Ahat - sigma I)| when no pivot failed).  Test infrastructure. */
+int orc_tf_eval_diag(int n, int m, int p, const double* A, long lda, const double* B, long ldb,
+                     const double* C, long ldc, const zc* shifts, int s, int nb, double rtol,
+                     zc* G, long ldg, int* fail, int nthreads, double* diag);
+int orc_solve_reduced_diag(int n, int m, const double* A, long lda, const double* B, long ldb,
+                           const zc* shifts, int s, const zc* bdirs, long ldbd, int nb,
+                           double rtol, zc* Xo, long ldx, int* fail, int nthreads, double* diag);
+
 int orc_tf_eval(int n, int m, int p, const double* A, long lda, const double* B, long ldb,
                 const double* C, long ldc, const zc* shifts, int s, int nb, double rtol,
                 zc* G, long ldg, int* fail, int nthreads) {
+    return orc_tf_eval_diag(n, m, p, A, lda, B, ldb, C, ldc, shifts, s, nb, rtol, G, ldg, fail,
+                            nthreads, NULL);
+}
+
+int orc_tf_eval_diag(int n, int m, int p, const double* A, long lda, const double* B, long ldb,
+                     const double* C, long ldc, const zc* shifts, int s, int nb, double rtol,
+                     zc* G, long ldg, int* fail, int nthreads, double* diag) {
     if (n < 1 || m < 1 || m > n || p < 0 || nb < 1 || s < 0) return -1;
     if (isnan(rtol)) rtol = 1e3 * n * ORC_EPS; /* NaN: reference default */
     double fro2, tr;
@@ -371,10 +407,17 @@ int orc_tf_eval(int n, int m, int p, const double* A, long lda, const double* B,
         zc* X = (zc*)malloc(sizeof(zc) * (size_t)m * m);
 #pragma omp for schedule(dynamic, 1)
         for (int l = 0; l < s; ++l) {
-            orc_sweep_one(n, m, p, A, lda, C, ldc, shifts[l], nb, z2, &ws);
-            double tol = rtol * orc_shift_scale(fro2, tr, n, shifts[l]);
-            int bad = orc_head_solve(z2, p + n, p, m, Bh, m, tol, X);
+            double rd[2] = {INFINITY, 0.0}, pm = INFINITY;
+            orc_sweep_one(n, m, p, A, lda, C, ldc, shifts[l], nb, z2, &ws, diag ? rd : NULL);
+            double scale = orc_shift_scale(fro2, tr, n, shifts[l]);
+            double tol = rtol * scale;
+            int bad = orc_head_solve(z2, p + n, p, m, Bh, m, tol, X, diag ? rd : NULL, &pm);
             fail[l] = bad;
+            if (diag) {
+                diag[3 * l] = scale / rd[0];
+                diag[3 * l + 1] = pm / scale;
+                diag[3 * l + 2] = rd[1];
+            }
             for (int c = 0; c < m; ++c) {
                 zc* g = G + (long)(l * m + c) * ldg;
                 for (int i = 0; i < p; ++i) {
@@ -396,6 +439,13 @@ int orc_tf_eval(int n, int m, int p, const double* A, long lda, const double* B,
 int orc_solve_reduced(int n, int m, const double* A, long lda, const double* B, long ldb,
                       const zc* shifts, int s, const zc* bdirs, long ldbd, int nb,
                       double rtol, zc* Xo, long ldx, int* fail, int nthreads) {
+    return orc_solve_reduced_diag(n, m, A, lda, B, ldb, shifts, s, bdirs, ldbd, nb, rtol, Xo, ldx,
+                                  fail, nthreads, NULL);
+}
+
+int orc_solve_reduced_diag(int n, int m, const double* A, long lda, const double* B, long ldb,
+                           const zc* shifts, int s, const zc* bdirs, long ldbd, int nb,
+                           double rtol, zc* Xo, long ldx, int* fail, int nthreads, double* diag) {
     if (n < 1 || m < 1 || m > n || nb < 1 || s < 0) return -1;
     if (isnan(rtol)) rtol = 1e3 * n * ORC_EPS; /* NaN: reference default */
     double fro2, tr;
@@ -417,10 +467,17 @@ int orc_solve_reduced(int n, int m, const double* A, long lda, const double* B, 
                 for (int j = 0; j < m; ++j) acc += B[i + (long)j * ldb] * bdirs[j + (long)l * ldbd];
                 rhs[i] = acc;
             }
-            orc_sweep_one(n, m, n, A, lda, NULL, 0, shifts[l], nb, z2, &ws);
-            double tol = rtol * orc_shift_scale(fro2, tr, n, shifts[l]);
-            int bad = orc_head_solve(z2, 2 * n, n, m, rhs, 1, tol, Y);
+            double rd[2] = {INFINITY, 0.0}, pm = INFINITY;
+            orc_sweep_one(n, m, n, A, lda, NULL, 0, shifts[l], nb, z2, &ws, diag ? rd : NULL);
+            double scale = orc_shift_scale(fro2, tr, n, shifts[l]);
+            double tol = rtol * scale;
+            int bad = orc_head_solve(z2, 2 * n, n, m, rhs, 1, tol, Y, diag ? rd : NULL, &pm);
             fail[l] = bad;
+            if (diag) {
+                diag[3 * l] = scale / rd[0];
+                diag[3 * l + 1] = pm / scale;
+                diag[3 * l + 2] = rd[1];
+            }
             zc* x = Xo + (long)l * ldx;
             for (int i = 0; i < n; ++i) {
                 if (bad >= 0) { x[i] = CMPLX(qnan, qnan); continue; }

@@ -122,3 +122,45 @@ def test_config1_matches_reference():
     for k, l in enumerate(g["lu_idx"]):
         lu = g["Glu"][:, k * m:(k + 1) * m]
         assert np.linalg.norm(G[:, l * m:(l + 1) * m] - lu) <= 1e-10 * np.linalg.norm(lu)
+
+
+@pytest.mark.parametrize("n,m,p,nb", [(60, 3, 2, 8), (100, 5, 4, 16), (45, 1, 1, 7), (90, 12, 3, 32)])
+def test_oracle_diagnostics_pin_the_R_diagonal(n, m, p, nb):
+    """The condition estimate of the parity rule reads the R
+    diagonal of every window block plus the head pivots; their log-magnitudes
+    sum to log |det(Ahat - sigma I)| (the sweep is a unitary column
+    transformation), for both the transfer-function and the reduced sweep."""
+    rng = np.random.default_rng(n + m)
+    A = np.triu(rng.standard_normal((n, n)), -m) - 1.1 * np.sqrt(n) * np.eye(n)
+    B = np.zeros((n, m))
+    B[:m, :m] = np.triu(rng.standard_normal((m, m))) + 2 * np.eye(m)
+    C = rng.standard_normal((p, n))
+    sh = np.array([3j, 2 + 5j, -1 + 0.3j])
+    _, _, d = O.tf_eval(A, B, C, sh, nb=nb, diag=True)
+    _, _, dr = O.solve_reduced(A, B, sh, np.ones((m, 3)), nb=nb, diag=True)
+    for l, s in enumerate(sh):
+        M = A - s * np.eye(n)
+        ld = np.linalg.slogdet(M)[1]
+        assert abs(d[l, 2] - ld) <= 1e-10 * abs(ld) + 1e-10
+        assert abs(dr[l, 2] - ld) <= 1e-10 * abs(ld) + 1e-10
+        # min |R_ii| >= sigma_min: the estimate never exceeds the Frobenius condition number
+        kf = np.linalg.norm(M, "fro") * np.linalg.norm(np.linalg.inv(M), 2)
+        assert 1.0 <= d[l, 0] <= kf * (1 + 1e-12)
+
+
+def test_parity_rule_failure_flags():
+    """assert_shift_parity: flags may differ only within 2x of the threshold."""
+    from conftest import assert_shift_parity
+    n, rt = 100, 1e3 * 100 * np.finfo(float).eps
+    Y = np.ones((2, 2), complex)
+    diag = np.array([[5.0, 1.5 * rt, 0.0], [5.0, 1.0, 0.0]])
+    Yg = Y.copy()
+    Yg[:, 0] = np.nan
+    assert_shift_parity(Yg, np.array([0, -1]), Y, np.array([-1, -1]), diag, n, 1)
+    diag[0, 1] = 3 * rt
+    with pytest.raises(AssertionError):
+        assert_shift_parity(Yg, np.array([0, -1]), Y, np.array([-1, -1]), diag, n, 1)
+    Yb = Y.copy()
+    Yb[0, 1] += 1e-6
+    with pytest.raises(AssertionError):
+        assert_shift_parity(Yb, np.array([-1, -1]), Y, np.array([-1, -1]), diag, n, 1)
