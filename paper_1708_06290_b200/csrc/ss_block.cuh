@@ -47,10 +47,11 @@ struct BlkDims {
     int64_t LDZ;
     int64_t wstride;  // elements (complex) per shift in W
     int woff;         // first W row of this block in the per-shift buffer
-    // paired outer blocks: > 0 = rows [kBlkNB, kBlkNB + wprod) of the buffer
-    // hold the previous (lower) block's W; they are multiplied in place by
-    // this block's W22 (the composite over both blocks) and this block's
-    // W22 rows are not written (ss_sweep.cu, enqueue_part)
+    // grouped outer blocks: > 0 = the wprod rows after this block's 128 W rows
+    // hold the composite of the blocks below it in the group; they are
+    // multiplied in place by this block's W22 (the composite now covers this
+    // block too) and this block's W22 rows are not written (ss_sweep.cu,
+    // enqueue_part)
     int wprod;
 };
 
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
 #pragma unroll
         for (int q = 0; q < NSW; ++q) {
             if (!vq[q]) continue;
-            double2* Wp = Wl[q] + (int64_t)(kBlkNB - d.woff) * M;
+            double2* Wp = Wl[q] + (int64_t)kBlkNB * M;  // the composite rows below this block's
             for (int row = lane; row < d.wprod; row += 32) {
                 // keep the W22 loads inside the loop (hoisting all m^2 of them
                 // out of it spills)

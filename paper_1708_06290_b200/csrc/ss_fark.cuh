@@ -1,0 +1,279 @@
+// Far-row update in ONE pass per composite: the K-streamed far kernel.
+//
+// Math (reference solvers.py:186-199 with the outer blocks' composite W in
+// place of one window's P; same as k_far / k_far4):
+//   Z_l[i, :] <- Z_l[i, :] W22_l + Pan[i, :] W12_l - sigma_l W12_l[i - (r0 - m), :]
+// for the far rows i in [rlo, r0), Pan = [Chat; Ahat](:, c0 : c0 + K).
+//
+// k_far / k_far4 stream each (row tile, shift) unit's Z tile through HBM once
+// per 64- / 128-column pass: at config 4 (m = 20) four passes per 256-column
+// composite move ~25 GB of Z state per composite against ~0.5 ms of FP64
+// work per GB -- ncu showed the far kernel at 44% of HBM bandwidth beside
+// 55% FP64-pipe.  Here the unit's K range is streamed instead:
+//  * units run shift-group-major (all row tiles of one group of S shifts,
+//    then the next group), so each CTA keeps ONE group's W (S (K + m) m
+//    complex, ~350 KB at m = 20) hot in L2 while it walks the tiles: the
+//    148 CTAs' groups (~52 MB) plus the packed panel (~20 MB) stay L2
+//    resident (tile-major order had every CTA on a different shift and
+//    re-read W from HBM: 3.4x the Z traffic);
+//  * unit = (64-row tile, S shifts); NW = S * NCB consumer warps, warp w owns
+//    shift w / NCB and 10 state columns ((w % NCB) * 10 ..), its register tile
+//    is 4 rows x 5 complex columns per lane over the WHOLE K range -- no
+//    partial-sum hand-off, Z read once and written once per composite;
+//  * the unit is a sequence of chunks through an NST-stage ring filled by one
+//    producer lane with cp.async.bulk + mbarrier complete_tx:
+//      nz "Z chunks"   (jz state columns of the S Z tiles + the matching jz
+//                       rows of W22, for the Z W22 part), then
+//      nk panel chunks (KC = 32 panel columns of the packed 64-row panel tile
+//                       + the S shifts' KC rows of W12);
+//  * the panel tile is packed once per composite by k_pack_panel into the
+//    lane-interleaved layout (rows rg + 16 w, pairs adjacent: one LDS.128
+//    feeds two rows), Chat / identity / zero rows merged, so every chunk is
+//    one contiguous bulk copy regardless of ldA, p or row alignment.
+#pragma once
+
+#include "ss_far.cuh"
+
+namespace ssd {
+
+constexpr int kFkTile = 64;  // rows per unit
+constexpr int kFkKC = 32;    // panel columns per chunk
+
+struct FarKDims {
+    int m, ptop, ident_top;
+    const double* A;
+    int64_t lda;
+    const double* T;  // dense top rows (Chat), ptop x n
+    int64_t ldt;
+    const double2* shifts;
+    int sb;
+    int64_t LDZ;
+    int r0, rlo, c0, K;  // far rows [rlo, r0), panel columns [c0, c0 + K)
+    int mnb;             // lazy-shift rows: W12 rows [0, mnb) correct rows r0 - m + dd
+    int64_t wstride;     // W of shift l: W + l * wstride + woff * m; rows [0, K) W12, [K, K + m) W22
+    int woff;
+    int nk, jz, nz, ntiles;
+    const double* pan;  // packed panel [ntiles][nk][KC][64]
+};
+
+template <int NCB, int S>
+__host__ __device__ constexpr size_t fark_stage_bytes() {
+    return (size_t)kFkKC * kFkTile * 8 + (size_t)S * kFkKC * (10 * NCB) * 16;
+}
+template <int NCB, int S, int NST>
+__host__ __device__ constexpr size_t fark_smem_bytes() {
+    return 256 + NST * fark_stage_bytes<NCB, S>();
+}
+// state columns per Z chunk: the S Z tiles' jz columns + jz rows of W22 fit a stage
+template <int NCB, int S>
+__host__ __device__ constexpr int fark_jz() {
+    return (int)(fark_stage_bytes<NCB, S>() / ((size_t)S * (kFkTile + 10 * NCB) * 16));
+}
+
+// Packs Pan(:, c0 + kc*KC .. ) rows [rlo + 64 t, +64) of [top; A] into the
+// chunk (t, kc): [KC columns][64 rows, lane-interleaved]; zero outside
+// [rlo, r0) x [c0, c0 + K).
+__global__ void __launch_bounds__(256) k_pack_panel(FarKDims u, double* __restrict__ pan) {
+    const int tile = blockIdx.x / u.nk, kc = blockIdx.x - tile * u.nk;
+    double* dst = pan + (size_t)blockIdx.x * kFkKC * kFkTile;
+    for (int e = threadIdx.x; e < kFkKC * kFkTile; e += blockDim.x) {
+        const int j = e >> 6, rr = e & 63;
+        const int i = u.rlo + tile * kFkTile + rr, jc = kc * kFkKC + j, col = u.c0 + jc;
+        double v = 0.0;
+        if (i < u.r0 && jc < u.K) {
+            if (i >= u.ptop)
+                v = u.A[(i - u.ptop) + (int64_t)col * u.lda];
+            else if (u.ident_top)
+                v = (i == col) ? 1.0 : 0.0;
+            else
+                v = u.T[i + (int64_t)col * u.ldt];
+        }
+        dst[j * kFkTile + far_pan_index<2>(rr)] = v;
+    }
+}
+
+template <int NCB, int S, int NST>
+__global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
+    k_fark(FarKDims u, double2* Z, const double2* __restrict__ W) {
+    constexpr int NW = NCB * S, M = 10 * NCB, R = 4, C = 5, RG = 16, TILE = kFkTile, KC = kFkKC;
+    constexpr size_t SB = fark_stage_bytes<NCB, S>();
+    constexpr size_t PANB = (size_t)KC * TILE * 8;
+    static_assert(fark_jz<NCB, S>() >= 1, "k_fark: a Z chunk must fit a stage");
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NST]
+    uint64_t* empty = full + NST;                         // [NST] (count NW)
+    unsigned char* stages = smem + 256;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = u.r0, sb = u.sb, K = u.K, jz = u.jz, nz = u.nz, nk = u.nk;
+    const int nsu = (sb + S - 1) / S;  // shift groups per row tile
+    const int64_t units = (int64_t)u.ntiles * nsu;
+    const int64_t ua = units * blockIdx.x / gridDim.x, ub = units * (blockIdx.x + 1) / gridDim.x;
+    const int nun = (int)(ub - ua);
+    const int CH = nz + nk;
+
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (nun <= 0) return;
+
+    if (warp == 0) {
+        // ---------------- producer: one lane streams every chunk in order ----------------
+        if (lane == 0) {
+            int g = 0;
+            for (int k = 0; k < nun; ++k) {
+                const int64_t unit = ua + k;
+                const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles), l0 = grp * S;
+                const int ns = min(S, sb - l0);
+                const int i0 = u.rlo + tile * TILE;
+                const unsigned zb = (unsigned)(min(TILE, r0 - i0) * 16);
+                for (int ch = 0; ch < CH; ++ch, ++g) {
+                    const int s = g % NST, use = g / NST;
+                    if (use > 0) mbar_wait_sleep(empty + s, (use - 1) & 1);
+                    unsigned char* st = stages + (size_t)s * SB;
+                    if (ch < nz) {
+                        const int j0 = ch * jz, jn = min(jz, M - j0);
+                        mbar_expect_tx(full + s, (unsigned)ns * (jn * zb + (unsigned)(jn * M * 16)));
+                        for (int sh = 0; sh < ns; ++sh) {
+                            const int64_t l = l0 + sh;
+                            double2* zs = reinterpret_cast<double2*>(st) + (size_t)sh * jz * (TILE + M);
+                            for (int j = 0; j < jn; ++j)
+                                tma_bulk_g2s(zs + j * TILE, Z + (l * M + j0 + j) * u.LDZ + i0, zb, full + s);
+                            tma_bulk_g2s(zs + jz * TILE, W + l * u.wstride + (int64_t)(u.woff + K + j0) * M,
+                                         (unsigned)(jn * M * 16), full + s);
+                        }
+                    } else {
+                        const int kc = ch - nz, kcols = min(KC, K - kc * KC);
+                        mbar_expect_tx(full + s, (unsigned)PANB + (unsigned)(ns * kcols * M * 16));
+                        tma_bulk_g2s(st, u.pan + ((size_t)tile * nk + kc) * KC * TILE, (unsigned)PANB, full + s);
+                        double2* ws = reinterpret_cast<double2*>(st + PANB);
+                        for (int sh = 0; sh < ns; ++sh) {
+                            const int64_t l = l0 + sh;
+                            tma_bulk_g2s(ws + (size_t)sh * KC * M,
+                                         W + l * u.wstride + (int64_t)(u.woff + kc * KC) * M,
+                                         (unsigned)(kcols * M * 16), full + s);
+                        }
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const int cw = warp - 1, sw = cw / NCB, cbk = cw - sw * NCB;
+    const int rg = lane >> 1, q = lane & 1;
+    const int cb = cbk * 10 + q * C;  // first output column of this lane
+    const int dlo = r0 - M;
+    int g = 0;
+    for (int k = 0; k < nun; ++k) {
+        const int64_t unit = ua + k;
+        const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles), l0 = grp * S;
+        const bool valid = l0 + sw < sb;
+        const int64_t l = valid ? l0 + sw : 0;
+        const int i0 = u.rlo + tile * TILE;
+        // boundary tile: rows r0 - m + dd (dd < mnb) carry the lazy shift
+        const bool interior = i0 + TILE <= (u.mnb > 0 ? dlo : r0);
+        const double2 sig = interior ? cz() : u.shifts[l];
+        double2 acc[R][C];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[r][c] = cz();
+        for (int ch = 0; ch < CH; ++ch, ++g) {
+            const int s = g % NST, use = g / NST;
+            mbar_wait(full + s, use & 1);
+            const unsigned char* st = stages + (size_t)s * SB;
+            if (valid) {
+                if (ch < nz) {
+                    const int j0 = ch * jz, jn = min(jz, M - j0);
+                    const double2* zs = reinterpret_cast<const double2*>(st) + (size_t)sw * jz * (TILE + M);
+                    const double2* w22 = zs + jz * TILE + cb;
+                    for (int j = 0; j < jn; ++j) {
+                        double2 z[R];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) z[r] = zs[j * TILE + rg + RG * r];
+#pragma unroll
+                        for (int c = 0; c < C; ++c) {
+                            const double2 pv = w22[j * M + c];
+#pragma unroll
+                            for (int r = 0; r < R; ++r) acc[r][c] = cfma(z[r], pv, acc[r][c]);
+                        }
+                    }
+                } else {
+                    const int kc = ch - nz, kcols = min(KC, K - kc * KC);
+                    const double* pan = reinterpret_cast<const double*>(st) + rg * 2;
+                    const double2* ws = reinterpret_cast<const double2*>(st + PANB) + (size_t)sw * KC * M + cb;
+                    if (kc == 0 && !interior) {
+                        // acc -= sigma W12[dd, :] (mnb <= m <= KC: the rows are in this chunk)
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const int dd = i0 + rg + RG * r - dlo;
+                            if (dd >= 0 && dd < u.mnb) {
+#pragma unroll
+                                for (int c = 0; c < C; ++c) acc[r][c] = csub(acc[r][c], cmul(sig, ws[dd * M + c]));
+                            }
+                        }
+                    }
+                    if (kcols == KC) {
+#pragma unroll 4
+                        for (int j = 0; j < KC; ++j) {
+                            double a[R];
+#pragma unroll
+                            for (int p = 0; p < R / 2; ++p) {
+                                const double2 v = *reinterpret_cast<const double2*>(pan + j * TILE + p * (2 * RG));
+                                a[2 * p] = v.x;
+                                a[2 * p + 1] = v.y;
+                            }
+#pragma unroll
+                            for (int c = 0; c < C; ++c) {
+                                const double2 pv = ws[j * M + c];
+#pragma unroll
+                                for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
+                            }
+                        }
+                    } else {
+                        for (int j = 0; j < kcols; ++j) {
+                            double a[R];
+#pragma unroll
+                            for (int p = 0; p < R / 2; ++p) {
+                                const double2 v = *reinterpret_cast<const double2*>(pan + j * TILE + p * (2 * RG));
+                                a[2 * p] = v.x;
+                                a[2 * p + 1] = v.y;
+                            }
+#pragma unroll
+                            for (int c = 0; c < C; ++c) {
+                                const double2 pv = ws[j * M + c];
+#pragma unroll
+                                for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        if (!valid) continue;
+        double2* zo = Z + (l * M + cb) * u.LDZ + i0 + rg;
+        if (i0 + TILE <= r0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < C; ++c) zo[(int64_t)c * u.LDZ + RG * r] = acc[r][c];
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (i0 + rg + RG * r >= r0) continue;
+#pragma unroll
+                for (int c = 0; c < C; ++c) zo[(int64_t)c * u.LDZ + RG * r] = acc[r][c];
+            }
+        }
+    }
+}
+
+}  // namespace ssd

@@ -45,6 +45,7 @@
 #include "ss_rq_big.cuh"
 #include "ss_far4.cuh"
 #include "ss_far.cuh"
+#include "ss_fark.cuh"
 
 using namespace ssd;
 
@@ -582,7 +583,36 @@ static int feed_wait(ss_handle* h, Feed& f, cudaStream_t st) {
 struct PartBufs {
     double2* Z;  // window state, updated in place
     double2* P;
+    double* pan = nullptr;  // packed panel of the K-streamed far kernel (k_fark)
 };
+
+// K-streamed far kernel (ss_fark.cuh): one pass per composite for m = 10, 20
+// (transfer function); SS_FAR_PASSES=1 keeps the 64 / 128-column pass
+// kernels (k_far / k_far4) for comparison.
+constexpr int kFarkStages = 4;
+static bool fark_supported(ss_handle* h, int m, int mode) {
+    if (mode != 0 || getenv("SS_FAR_PASSES")) return false;
+    if (m == 10) return fark_smem_bytes<1, 8, kFarkStages>() <= h->smem_optin;
+    if (m == 20) return fark_smem_bytes<2, 4, kFarkStages>() <= h->smem_optin;
+    return false;
+}
+static size_t fark_pan_bytes(int n, int ptop) {
+    const size_t ntiles = (size_t)(ptop + n) / kFkTile + 2;
+    return ntiles * ((4 * kBlkNB + kFkKC - 1) / kFkKC) * kFkKC * kFkTile * 8;  // K <= 4 outer blocks
+}
+template <int NCB, int S>
+int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_fark<NCB, S, kFarkStages>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)fark_smem_bytes<NCB, S, kFarkStages>()));
+        configured.set(h);
+    }
+    k_fark<NCB, S, kFarkStages><<<grid, 32 * (1 + NCB * S), fark_smem_bytes<NCB, S, kFarkStages>(), st>>>(fk, Z, W);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
 
 // Enqueue the whole sweep (seed, window steps, head) for shifts
 // [lo, lo + sb) of the call on stream `st`.
@@ -622,11 +652,17 @@ bool block_supported(int m) { return (m >= 4 && m <= 8) || m == 10 || m == 20; }
 
 // Paired outer blocks (composite W over 256 columns for the far rows);
 // SS_NO_PAIR=1 keeps one far update per 128-column block.
-static bool two_level_pairing(int m) {
-    (void)m;
-    return !getenv("SS_NO_PAIR");
+static int two_level_group(ss_handle* h, int m, int mode) {
+    if (getenv("SS_NO_PAIR")) return 1;
+    if (const char* e = getenv("SS_GROUP")) {
+        const int g = atoi(e);
+        if (g == 1 || g == 2 || g == 4) return g;
+    }
+    // one pass per composite (k_fark): 4 outer blocks per composite halve
+    // the far rows' Z W22 share (2m / 512) and Z traffic; the pass kernels
+    // keep pairs
+    return fark_supported(h, m, mode) ? 4 : 2;
 }
-
 // Reference phase flops of the window sweep at block size nb0 (shape only:
 // batched.py:58-61, solvers.py:186-199), independent of how the device
 // schedules the work.
@@ -679,8 +715,8 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         // rows above B get ONE update from it -- the Z2 W22 part on the far
         // rows is paid once per 256 columns instead of once per 128.
         account_ref_flops(h, sb, n, m, ptop, nb0);
-        const bool pairing = two_level_pairing(m);
-        const int64_t wstride = (int64_t)((pairing ? 2 : 1) * kBlkNB + m) * m;
+        const int group = two_level_group(h, m, a.mode);
+        const int64_t wstride = (int64_t)(group * kBlkNB + m) * m;
         // far-row update of rows [rlo, r0) from the W rows [woff, woff + ncols
         // + m) of the buffer, panel columns [c0, c0 + ncols), in 64-column passes
         // m = 10: 128-column passes on the four-way-split far kernel (SS_FAR4=0: 64-column k_far)
@@ -688,8 +724,53 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                           !(getenv("SS_FAR4") && atoi(getenv("SS_FAR4")) == 0) &&
                           far4_smem_bytes<2, 5, 4>(128, m) + 1024 <= h->smem_optin;
         const int pw = far4 ? 128 : 64;
+        const bool fark = B.pan != nullptr && fark_supported(h, m, a.mode);
         auto far_update = [&](int rlo, int r0, int c0, int ncols, int woff) -> int {
             const int rows = r0 - rlo;
+            if (fark && rows > 0) {
+                // one pass over the whole composite (ss_fark.cuh)
+                FarKDims fk;
+                fk.m = m;
+                fk.ptop = ptop;
+                fk.ident_top = d.ident_top;
+                fk.A = a.A;
+                fk.lda = a.lda;
+                fk.T = a.C;
+                fk.ldt = a.ldc;
+                fk.shifts = d.shifts;
+                fk.sb = sb;
+                fk.LDZ = LDZ;
+                fk.r0 = r0;
+                fk.rlo = rlo;
+                fk.c0 = c0;
+                fk.K = ncols;
+                fk.mnb = std::min(m, ncols);
+                fk.wstride = wstride;
+                fk.woff = woff;
+                fk.nk = (ncols + kFkKC - 1) / kFkKC;
+                fk.jz = m == 10 ? fark_jz<1, 8>() : fark_jz<2, 4>();
+                fk.nz = (m + fk.jz - 1) / fk.jz;
+                fk.ntiles = (rows + kFkTile - 1) / kFkTile;
+                fk.pan = B.pan;
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                SS_LAUNCH_CHECK(h);
+                ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
+                const int S = m == 10 ? 8 : 4;
+                const int64_t units = (int64_t)fk.ntiles * ((sb + S - 1) / S);
+                const int grid = (int)std::min<int64_t>(units, h->num_sms);
+                double nnz = 0.0;  // algorithmic flops: structural nonzeros x m complex columns
+                const int top_hi = std::min(r0, ptop);
+                if (top_hi > rlo) nnz += (double)(top_hi - rlo) * ncols;
+                if (r0 > std::max(rlo, ptop)) nnz += (double)(r0 - std::max(rlo, ptop)) * ncols;
+                ev = ss::timing_begin(h, st);
+                int rc = m == 10 ? launch_fark<1, 8>(h, grid, st, fk, B.Z, B.P)
+                                 : launch_fark<2, 4>(h, grid, st, fk, B.Z, B.P);
+                if (rc) return rc;
+                ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
+                               8.0 * rows * (double)sb * m * ncols, 4.0 * m * nnz * sb);
+                return SS_OK;
+            }
             for (int jb = 0; rows > 0 && jb < ncols; jb += pw) {
                 const int nbp = std::min(pw, ncols - jb);
                 UpdDims u;
@@ -792,28 +873,35 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             ss::timing_end(h, st, ev, ss::PH_RQ);
             return SS_OK;
         };
+        // Groups of g <= group outer blocks (1 = bottom, the first processed;
+        // only block 1 of the whole sweep can be ragged).  Per shift the W
+        // buffer holds [W_g | ... | W_2 | W_1 | W22]: block b writes its W12 at
+        // rows (g - b) 128 and (b >= 2) folds the composite of blocks 1..b-1
+        // below it by its W22 (ss_block.cuh, wprod), so rows [(g - b) 128, end)
+        // are the composite of blocks 1..b.  Before block b + 1 its own rows
+        // get that composite ("near", untouched since the group began); after
+        // block g the rows above the group get ONE update over
+        // (g - 1) 128 + NB1 columns.
         for (int ko = n; ko >= m + 1;) {
-            const int NBa = std::min(kBlkNB, ko - m);
-            const int c0a = ko - m - NBa, r0a = ptop + ko - NBa;
-            const int kb = ko - NBa;  // block B's k
-            if (pairing && kb - m >= kBlkNB) {
-                const int c0b = c0a - kBlkNB, r0b = r0a - kBlkNB;
-                int rc = block(ko, NBa, kBlkNB, 0);
+            const int NB1 = std::min(kBlkNB, ko - m);
+            const int avail = (ko - NB1 - m) / kBlkNB;  // full blocks above block 1
+            const int g = 1 + std::min(group - 1, avail);
+            int kb = ko, NBb = NB1;
+            for (int b = 1; b <= g; ++b) {
+                const int woff = (g - b) * kBlkNB;
+                const int K = (b - 1) * kBlkNB + NB1;  // columns of the composite 1..b
+                int rc = block(kb, NBb, woff, b == 1 ? 0 : (b - 2) * kBlkNB + NB1 + m);
                 if (rc) return rc;
-                rc = far_update(r0b, r0a, c0a, NBa, kBlkNB);  // near: B's rows
+                const int c0 = kb - m - NBb, r0 = ptop + kb - NBb;
+                if (b < g)
+                    rc = far_update(r0 - kBlkNB, r0, c0, K, woff);  // near: block b + 1's rows
+                else
+                    rc = far_update(a.mode == 1 ? c0 : 0, r0, c0, K, 0);
                 if (rc) return rc;
-                rc = block(kb, kBlkNB, 0, NBa + m);
-                if (rc) return rc;
-                rc = far_update(a.mode == 1 ? c0b : 0, r0b, c0b, kBlkNB + NBa, 0);
-                if (rc) return rc;
-                ko = kb - kBlkNB;
-            } else {
-                int rc = block(ko, NBa, 0, 0);
-                if (rc) return rc;
-                rc = far_update(a.mode == 1 ? c0a : 0, r0a, c0a, NBa, 0);
-                if (rc) return rc;
-                ko = kb;
+                kb -= NBb;
+                NBb = kBlkNB;
             }
+            ko = kb;
         }
     }
     while (k >= m + 1) {
@@ -1224,7 +1312,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
-    const int64_t pst = two_level ? (int64_t)((two_level_pairing(m) ? 2 : 1) * kBlkNB + m) * m
+    const int64_t pst = two_level ? (int64_t)(two_level_group(h, m, a.mode) * kBlkNB + m) * m
                                   : (int64_t)ncmax * m;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64;
     int64_t sb_max = std::min<int64_t>(a.batch > 0 ? a.batch : a.s, a.s);
@@ -1245,6 +1333,12 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     }
     double2* Z0 = (double2*)h->ws;
     double2* P0 = Z0 + (size_t)sb_max * m * LDZ;
+    double* pan = nullptr;  // k_fark's packed panel, after the 1 MB scratch of fro2_trace
+    if (two_level && fark_supported(h, m, a.mode)) {
+        int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(n, ptop), 1);
+        if (rc) return rc;
+        pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
+    }
 
     // Independent halves of a batch on two streams: the latency-bound block
     // RQ of one half overlaps the FP64-bound window update of the other.
@@ -1272,6 +1366,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             PartBufs B;
             B.Z = Z0 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * pst;
+            B.pan = pan;
             int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, tile,
                                   two_level, streams[p], feed);
             if (rc) return rc;

@@ -459,6 +459,7 @@ def test_far4_vs_far(n, p, monkeypatch):
     ragged last blocks, odd pair counts, the near update, the reduced solve
     (identity top, far rows from the block's first column)."""
     m = 10
+    monkeypatch.setenv("SS_FAR_PASSES", "1")  # the pass kernels, not k_fark
     chf = _mhess_triple(n, m, p, seed=n * 7 + p)
     shifts = np.concatenate([1j * np.logspace(-2, 2, 25) * np.sqrt(n) + 0.2,
                              [0.4 * np.sqrt(n) + 0.9j * np.sqrt(n)]])
@@ -470,6 +471,52 @@ def test_far4_vs_far(n, p, monkeypatch):
     X2 = ss.solve_shifted_reduced(chf, shifts[:3], bd, nb=64).x
     assert per_shift_rel(G4, G2, m, len(shifts)) <= 1e-12
     assert max(rel(X4[:, k], X2[:, k]) for k in range(3)) <= 1e-12
+
+
+@pytest.mark.parametrize("group", ["1", "2", "4"])
+@pytest.mark.parametrize("n,m,p", [(1111, 10, 10), (700, 20, 3), (389, 20, 20), (1400, 5, 4),
+                                   (650, 20, 5)])
+def test_block_groups_vs_oracle(group, n, m, p, monkeypatch):
+    """Groups of 1, 2, 4 outer blocks per composite (SS_GROUP; default 4 on
+    the K-streamed far kernel, 2 on the pass kernels): composites over up to
+    512 columns with near updates inside the group, ragged first blocks and
+    partial last groups; transfer function and reduced solve vs the oracle."""
+    monkeypatch.setenv("SS_GROUP", group)
+    chf = _mhess_triple(n, m, p, seed=n * 3 + m)
+    shifts = np.concatenate([1j * np.logspace(-2, 2, 9) * np.sqrt(n) + 0.3,
+                             [0.5 * np.sqrt(n) - 0.2j, 0.2 * np.sqrt(n) + 1.1j * np.sqrt(n)]])
+    s = len(shifts)
+    G = ss.eval_transfer_function(chf, shifts, nb=64).G
+    Go, fo = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts, nb=64, threads=4)
+    assert (fo < 0).all()
+    assert per_shift_rel(G, Go, m, s) <= 1e-11
+    bd = np.exp(1j * np.arange(m * 3).reshape(m, 3))
+    X = ss.solve_shifted_reduced(chf, shifts[:3], bd, nb=64).x
+    Xo, _ = O.solve_reduced(chf.Ahat, chf.Bhat, shifts[:3], bd, nb=64, threads=4)
+    assert max(rel(X[:, k], Xo[:, k]) for k in range(3)) <= 1e-11
+
+
+@pytest.mark.parametrize("n,m,p,s", [(1111, 10, 10, 26), (700, 10, 3, 9), (389, 20, 7, 13),
+                                     (1500, 20, 20, 41), (260, 20, 1, 5), (1337, 10, 5, 17)])
+def test_fark_vs_passes_and_oracle(n, m, p, s, monkeypatch):
+    """K-streamed far kernel (k_fark: one pass per composite, default for
+    m = 10, 20) against the 64 / 128-column pass kernels (SS_FAR_PASSES=1)
+    and the C oracle: ragged last blocks, odd p (unaligned Chat rows in the
+    packed panel), shift counts that leave a partial last shift group."""
+    chf = _mhess_triple(n, m, p, seed=n * 11 + m)
+    rng = np.random.default_rng(n + s)
+    shifts = (rng.uniform(-0.5, 1.0, s) + 1j * rng.uniform(-1.5, 1.5, s)) * np.sqrt(n)
+    Gk = ss.eval_transfer_function(chf, shifts, nb=64).G
+    Gb3 = ss.eval_transfer_function(chf, shifts, nb=64, batch_size=3).G
+    assert np.array_equal(Gk, Gb3)  # shift groups never mix shifts
+    monkeypatch.setenv("SS_FAR_PASSES", "1")
+    Gp = ss.eval_transfer_function(chf, shifts, nb=64).G
+    assert per_shift_rel(Gk, Gp, m, s) <= 1e-12
+    idx = np.arange(0, s, max(1, s // 4))
+    Go, fo = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, shifts[idx], nb=64, threads=4)
+    assert (fo < 0).all()
+    Gs = np.concatenate([Gk[:, l * m:(l + 1) * m] for l in idx], axis=1)
+    assert per_shift_rel(Gs, Go, m, len(idx)) <= 1e-11
 
 
 @pytest.mark.parametrize("n,nb", [(333, 64), (300, 32), (129, 7), (66, 64)])
