@@ -53,8 +53,10 @@ WORKLOADS = {
     5: "config5: large-scale transfer function n=20000, m=p=50, 500 complex shifts per GPU",
 }
 # dominant (far-row update) kernel per m, as enqueue_part selects it
-FAR_KERNEL = {10: "k_far4<2,5,4> (far-row update, 128-column passes, four-way K split)",
-              20: "k_far<2,5,4,4,4,2> (far-row update, 64-column passes, two column blocks per unit)"}
+FAR_KERNEL = {10: "k_fark<1,8,4> (K-streamed far-row update: one pass per 4-block composite, "
+                  "8 shifts x 64 rows per unit)",
+              20: "k_fark<2,4,4> (K-streamed far-row update: one pass per 4-block composite, "
+                  "4 shifts x 64 rows per unit)"}
 
 
 def parse(argv=None):

@@ -16,6 +16,8 @@
 //    148 CTAs' groups (~52 MB) plus the packed panel (~20 MB) stay L2
 //    resident (tile-major order had every CTA on a different shift and
 //    re-read W from HBM: 3.4x the Z traffic);
+//    Teams of spl CTAs share each shift group (interleaved tiles), cutting
+//    the live W working set by spl;
 //  * unit = (64-row tile, S shifts); NW = S * NCB consumer warps, warp w owns
 //    shift w / NCB and 10 state columns ((w % NCB) * 10 ..), its register tile
 //    is 4 rows x 5 complex columns per lane over the WHOLE K range -- no
@@ -53,6 +55,7 @@ struct FarKDims {
     int64_t wstride;     // W of shift l: W + l * wstride + woff * m; rows [0, K) W12, [K, K + m) W22
     int woff;
     int nk, jz, nz, ntiles;
+    int spl;  // CTAs per team (grid is a multiple of spl)
     const double* pan;  // packed panel [ntiles][nk][KC][64]
 };
 
@@ -107,8 +110,12 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
     const int r0 = u.r0, sb = u.sb, K = u.K, jz = u.jz, nz = u.nz, nk = u.nk;
     const int nsu = (sb + S - 1) / S;  // shift groups per row tile
     const int64_t units = (int64_t)u.ntiles * nsu;
-    const int64_t ua = units * blockIdx.x / gridDim.x, ub = units * (blockIdx.x + 1) / gridDim.x;
-    const int nun = (int)(ub - ua);
+    // teams of u.spl CTAs share one unit range and take every spl-th unit:
+    // fewer shift groups are live at once (W working set / spl)
+    const int spl = u.spl, team = blockIdx.x / spl, h = blockIdx.x - team * spl, nteams = gridDim.x / spl;
+    const int64_t ua0 = units * team / nteams, ub = units * (team + 1) / nteams;
+    const int64_t ua = ua0 + h;
+    const int nun = ua < ub ? (int)((ub - ua + spl - 1) / spl) : 0;
     const int CH = nz + nk;
 
     if (tid == 0) {
@@ -126,7 +133,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
         if (lane == 0) {
             int g = 0;
             for (int k = 0; k < nun; ++k) {
-                const int64_t unit = ua + k;
+                const int64_t unit = ua + (int64_t)k * spl;
                 const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles), l0 = grp * S;
                 const int ns = min(S, sb - l0);
                 const int i0 = u.rlo + tile * TILE;
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
     const int dlo = r0 - M;
     int g = 0;
     for (int k = 0; k < nun; ++k) {
-        const int64_t unit = ua + k;
+        const int64_t unit = ua + (int64_t)k * spl;
         const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles), l0 = grp * S;
         const bool valid = l0 + sw < sb;
         const int64_t l = valid ? l0 + sw : 0;

@@ -758,7 +758,11 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
                 const int S = m == 10 ? 8 : 4;
                 const int64_t units = (int64_t)fk.ntiles * ((sb + S - 1) / S);
-                const int grid = (int)std::min<int64_t>(units, h->num_sms);
+                // teams of 4 CTAs per shift group: the live W set drops from ~100 MB
+                // (over L2) to ~25 MB, DRAM bytes per launch 8.5 -> 2.6 GB at config 4
+                fk.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
+                const int grid = (int)std::max<int64_t>(
+                    fk.spl, std::min<int64_t>(units, h->num_sms) / fk.spl * fk.spl);
                 double nnz = 0.0;  // algorithmic flops: structural nonzeros x m complex columns
                 const int top_hi = std::min(r0, ptop);
                 if (top_hi > rlo) nnz += (double)(top_hi - rlo) * ncols;
