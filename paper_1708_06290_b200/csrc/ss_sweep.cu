@@ -220,6 +220,7 @@ struct HeadOut {
     double2* out;        // tf: G (batch-local, column l*m); reduced: X (batch-local)
     int64_t ldo;
     int32_t* fail;       // batch-local
+    double2* ybuf;       // deferred reduced solve: y = Qh X (m per shift) for k_expand
 };
 
 __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
@@ -307,7 +308,7 @@ __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
                 const int c = u / d.ptop, i = u - c * d.ptop;
                 h.out[i + ((int64_t)l * m + c) * h.ldo] = make_double2(qn, qn);
             }
-        } else {
+        } else if (!h.ybuf) {
             for (int i = threadIdx.x; i < d.n; i += blockDim.x)
                 h.out[i + (int64_t)l * h.ldo] = make_double2(qn, qn);
         }
@@ -331,6 +332,8 @@ __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
             for (int j = 0; j < m; ++j) acc = cfma(zl[(int64_t)j * d.LDZ + i], V[j + c * m], acc);
             h.out[i + ((int64_t)l * m + c) * h.ldo] = make_double2(-acc.x, -acc.y);
         }
+    } else if (h.ybuf) {
+        for (int r = threadIdx.x; r < m; r += blockDim.x) h.ybuf[(int64_t)l * m + r] = V[r];
     } else {
         for (int i = threadIdx.x; i < d.n; i += blockDim.x) {
             double2 acc = cz();
@@ -339,6 +342,79 @@ __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
         }
     }
     if (threadIdx.x == 0) h.fail[l] = -1;
+}
+
+// ---------------------------------------------------------------------------
+// Deferred identity top of the reduced solve (solvers.py:274-313).  The
+// reference sweeps [I; Ahat - sigma I] and reads x = Z2[:n] y; the identity
+// rows only ever receive  T <- T W22_c + E_c W12_c  (composite c over panel
+// columns [c0_c, c0_c + K_c)), so with T_0 = the seed's identity columns
+//   x = sum_c E_c W12_c (W22_{c+1} ... W22_C y) + E_seed (W22_1 ... W22_C y),
+// one backward pass over the kept composites per shift (O(n m) instead of
+// sweeping n identity rows through every far update).  One CTA per shift.
+// ---------------------------------------------------------------------------
+struct ExpandArgs {
+    int n, m, group, ncomp;
+    const double2* Xh;    // per shift: n x m (row = panel column), stride xh_stride
+    int64_t xh_stride;
+    const double2* W22h;  // per shift: ncomp x m x m (j-major), stride w22h_stride
+    int64_t w22h_stride;
+    const double2* Y;     // per shift: m
+    const int32_t* fail;
+    double2* X;           // n x sb, ldx
+    int64_t ldx;
+};
+
+__global__ void __launch_bounds__(256) k_expand(ExpandArgs e) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* v = reinterpret_cast<double2*>(smem);  // [2][m]
+    int* cs = reinterpret_cast<int*>(v + 2 * e.m);  // [ncomp][2]: (c0, K)
+    const int l = blockIdx.x, m = e.m;
+    double2* x = e.X + (int64_t)l * e.ldx;
+    if (e.fail[l] >= 0) {
+        const double qn = __longlong_as_double(0x7ff8000000000000ULL);
+        for (int i = threadIdx.x; i < e.n; i += blockDim.x) x[i] = make_double2(qn, qn);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        // the composites in sweep order, as enqueue_part's group loop forms them
+        int c = 0;
+        for (int ko = e.n; ko >= m + 1;) {
+            const int NB1 = min(kBlkNB, ko - m);
+            const int g = 1 + min(e.group - 1, (ko - NB1 - m) / kBlkNB);
+            const int K = (g - 1) * kBlkNB + NB1;
+            cs[2 * c] = ko - m - K;
+            cs[2 * c + 1] = K;
+            ++c;
+            ko -= K;
+        }
+    }
+    for (int t = threadIdx.x; t < m; t += blockDim.x) v[t] = e.Y[(int64_t)l * m + t];
+    __syncthreads();
+    const double2* xh = e.Xh + (int64_t)l * e.xh_stride;
+    const double2* w22 = e.W22h + (int64_t)l * e.w22h_stride;
+    int cur = 0;
+    for (int c = e.ncomp - 1; c >= 0; --c) {
+        const double2* vc = v + cur * m;
+        const int c0 = cs[2 * c], K = cs[2 * c + 1];
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
+            const double2* wr = xh + (int64_t)(c0 + j) * m;
+            double2 acc = cz();
+            for (int t = 0; t < m; ++t) acc = cfma(wr[t], vc[t], acc);
+            x[c0 + j] = acc;
+        }
+        // v <- W22_c v
+        const double2* wc = w22 + (int64_t)c * m * m;
+        double2* vn = v + (cur ^ 1) * m;
+        for (int j = threadIdx.x; j < m; j += blockDim.x) {
+            double2 acc = cz();
+            for (int t = 0; t < m; ++t) acc = cfma(wc[(int64_t)j * m + t], vc[t], acc);
+            vn[j] = acc;
+        }
+        cur ^= 1;
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < m; t += blockDim.x) x[e.n - m + t] = v[cur * m + t];
 }
 
 // ---------------------------------------------------------------------------
@@ -548,6 +624,11 @@ struct SweepArgs {
     // destination, filled chunk by chunk in sweep order on h->copy_stream
     const double* A_host = nullptr;
     int64_t lda_host = 0;
+    // reduced solve with the identity top deferred (two-level sweep): the
+    // sweep runs on Ahat alone (no top rows), each composite's W12 / W22 are
+    // kept per shift and x = [I; 0]-part is expanded after the head (k_expand)
+    bool defer = false;
+    int group = 1;
 };
 
 // Streamed-Ahat bookkeeping for one call: chunk c's event is recorded on the
@@ -584,6 +665,12 @@ struct PartBufs {
     double2* Z;  // window state, updated in place
     double2* P;
     double* pan = nullptr;  // packed panel of the K-streamed far kernel (k_fark)
+    // deferred reduced solve: per shift W12 history (n x m, row = panel column,
+    // j-major) and the composites' W22 (ncomp x m x m), plus the head's y (m)
+    double2* Xh = nullptr;
+    double2* W22h = nullptr;
+    double2* Y = nullptr;
+    int64_t xh_stride = 0, w22h_stride = 0;
 };
 
 // K-streamed far kernel (ss_fark.cuh): one pass per composite for m = 10, 20
@@ -685,13 +772,14 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                  int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, bool two_level,
                  cudaStream_t st, Feed& feed) {
     const int n = a.n, m = a.m;
-    const int ptop = a.mode == 0 ? a.p : n;
+    const int ptop = a.mode == 0 ? a.p : (a.defer ? 0 : n);
+    const int mode_far = a.defer ? 0 : a.mode;  // deferred reduced solve: far rows as tf with p = 0
     const int nws = (m + tile.G * tile.C - 1) / (tile.G * tile.C);  // warps per shift
     Dims d;
     d.n = n;
     d.m = m;
     d.ptop = ptop;
-    d.ident_top = a.mode == 1;
+    d.ident_top = a.mode == 1 && !a.defer;
     d.A = a.A;
     d.lda = a.lda;
     d.T = a.C;
@@ -714,8 +802,8 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         // (B) then folds A's W into the composite over both blocks, and the
         // rows above B get ONE update from it -- the Z2 W22 part on the far
         // rows is paid once per 256 columns instead of once per 128.
-        account_ref_flops(h, sb, n, m, ptop, nb0);
-        const int group = two_level_group(h, m, a.mode);
+        account_ref_flops(h, sb, n, m, a.mode == 0 ? a.p : n, nb0);  // the reference's stack
+        const int group = a.group;
         const int64_t wstride = (int64_t)(group * kBlkNB + m) * m;
         // far-row update of rows [rlo, r0) from the W rows [woff, woff + ncols
         // + m) of the buffer, panel columns [c0, c0 + ncols), in 64-column passes
@@ -724,7 +812,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                           !(getenv("SS_FAR4") && atoi(getenv("SS_FAR4")) == 0) &&
                           far4_smem_bytes<2, 5, 4>(128, m) + 1024 <= h->smem_optin;
         const int pw = far4 ? 128 : 64;
-        const bool fark = B.pan != nullptr && fark_supported(h, m, a.mode);
+        const bool fark = B.pan != nullptr && fark_supported(h, m, mode_far);
         auto far_update = [&](int rlo, int r0, int c0, int ncols, int woff) -> int {
             const int rows = r0 - rlo;
             if (fark && rows > 0) {
@@ -886,6 +974,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         // get that composite ("near", untouched since the group began); after
         // block g the rows above the group get ONE update over
         // (g - 1) 128 + NB1 columns.
+        int ncomp = 0;  // composites so far (deferred reduced solve)
         for (int ko = n; ko >= m + 1;) {
             const int NB1 = std::min(kBlkNB, ko - m);
             const int avail = (ko - NB1 - m) / kBlkNB;  // full blocks above block 1
@@ -900,8 +989,20 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (b < g)
                     rc = far_update(r0 - kBlkNB, r0, c0, K, woff);  // near: block b + 1's rows
                 else
-                    rc = far_update(a.mode == 1 ? c0 : 0, r0, c0, K, 0);
+                    rc = far_update(mode_far == 1 ? c0 : 0, r0, c0, K, 0);
                 if (rc) return rc;
+                if (b == g && a.defer) {
+                    // keep the composite: W12 rows -> history rows [c0, c0 + K),
+                    // W22 -> composite slot
+                    SS_CUDA_TRY(h, cudaMemcpy2DAsync(B.Xh + (int64_t)c0 * m, (size_t)B.xh_stride * 16, B.P,
+                                                     (size_t)wstride * 16, (size_t)K * m * 16, (size_t)sb,
+                                                     cudaMemcpyDeviceToDevice, st));
+                    SS_CUDA_TRY(h, cudaMemcpy2DAsync(B.W22h + (int64_t)ncomp * m * m, (size_t)B.w22h_stride * 16,
+                                                     B.P + (int64_t)K * m, (size_t)wstride * 16,
+                                                     (size_t)m * m * 16, (size_t)sb, cudaMemcpyDeviceToDevice,
+                                                     st));
+                    ++ncomp;
+                }
                 kb -= NBb;
                 NBb = kBlkNB;
             }
@@ -1113,6 +1214,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     ho.out = a.mode == 0 ? a.out + lo * m * a.ldo : a.out + lo * a.ldo;
     ho.ldo = a.ldo;
     ho.fail = a.fail + lo;
+    ho.ybuf = a.defer ? B.Y : nullptr;
     if (feed.on && feed.fro2_pending) {
         // streamed Ahat: all chunks are in (the last wait came with the last
         // window); the pivot tolerances need ||A||_F and trace(A)
@@ -1124,6 +1226,29 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
     k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z);
     SS_LAUNCH_CHECK(h);
+    if (a.defer) {
+        ExpandArgs e;
+        e.n = n;
+        e.m = m;
+        e.group = a.group;
+        e.ncomp = 0;
+        for (int ko = n; ko >= m + 1;) {  // composite count (the group loop's)
+            const int NB1 = std::min(kBlkNB, ko - m);
+            const int g = 1 + std::min(a.group - 1, (ko - NB1 - m) / kBlkNB);
+            ko -= (g - 1) * kBlkNB + NB1;
+            ++e.ncomp;
+        }
+        e.Xh = B.Xh;
+        e.xh_stride = B.xh_stride;
+        e.W22h = B.W22h;
+        e.w22h_stride = B.w22h_stride;
+        e.Y = B.Y;
+        e.fail = ho.fail;
+        e.X = ho.out;
+        e.ldx = ho.ldo;
+        k_expand<<<sb, 256, (size_t)2 * m * 16 + (size_t)e.ncomp * 8, st>>>(e);
+        SS_LAUNCH_CHECK(h);
+    }
     ss::timing_end(h, st, evh, ss::PH_TAIL);
     h->flops[ss::PH_TAIL] += a.mode == 0 ? (double)sb * 8.0 * a.p * m * m : (double)sb * 8.0 * n * m;
     return SS_OK;
@@ -1229,9 +1354,9 @@ int fro2_trace(ss_handle* h, int n, const double* A, int64_t lda, cudaStream_t s
 
 namespace {
 
-int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
+int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
+    SweepArgs a = a_in;
     const int n = a.n, m = a.m;
-    const int ptop = a.mode == 0 ? a.p : n;
     if (a.s == 0) return SS_OK;
     ss::DevGuard dg(h->device);
     SS_CUDA_TRY(h, dg.err);
@@ -1239,7 +1364,6 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     // value is used as given (0: only exactly-zero pivots fail, solvers.py:227)
     const double rtol = std::isnan(a.rtol) ? 1e3 * n * 2.220446049250313e-16 : a.rtol;
     const int nb0_req = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
-    const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
 
     static ss::DevMask attrs;  // devices configured
     if (!attrs.has(h)) {
@@ -1281,6 +1405,21 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
                            (tile.G * tile.C == m || (m == 20 && tile.G == 2 && tile.C == 5)) &&
                            !getenv("SS_ONE_LEVEL") &&
                            far_smem_bytes(64, m, 64, m == 20 ? 4 : 8) + 1024 <= h->smem_optin;
+    // reduced solve on the two-level sweep: identity top deferred (k_expand);
+    // SS_NO_DEFER=1 sweeps the identity rows as the reference does
+    a.defer = a.mode == 1 && two_level && !getenv("SS_NO_DEFER");
+    const int mode_far = a.defer ? 0 : a.mode;
+    a.group = two_level ? two_level_group(h, m, mode_far) : 1;
+    const int ptop = a.mode == 0 ? a.p : (a.defer ? 0 : n);
+    const int64_t LDZ = ((int64_t)(ptop + n) + 7) & ~(int64_t)7;
+    int ncomp = 0;
+    for (int ko = n; a.defer && ko >= m + 1; ++ncomp) {
+        const int NB1 = std::min(kBlkNB, ko - m);
+        ko -= (1 + std::min(a.group - 1, (ko - NB1 - m) / kBlkNB) - 1) * kBlkNB + NB1;
+    }
+    const int64_t xh_stride = a.defer ? (int64_t)n * m : 0;
+    const int64_t w22h_stride = a.defer ? (int64_t)ncomp * m * m : 0;
+    const int64_t y_stride = a.defer ? m : 0;  // the head's y for k_expand
     // fro2 / trace for the per-shift singularity thresholds (streamed Ahat:
     // after the last chunk, just before the first head)
     Feed feed;
@@ -1316,9 +1455,9 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
 
     // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
-    const int64_t pst = two_level ? (int64_t)(two_level_group(h, m, a.mode) * kBlkNB + m) * m
-                                  : (int64_t)ncmax * m;
-    const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64;
+    const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)ncmax * m;
+    const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64 +
+                             (size_t)(xh_stride + w22h_stride + y_stride) * 16;
     int64_t sb_max = std::min<int64_t>(a.batch > 0 ? a.batch : a.s, a.s);
     if (per_shift * (size_t)sb_max + 256 > h->ws_bytes) {
         // only when the workspace has to grow: cudaMemGetInfo is a driver
@@ -1337,8 +1476,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
     }
     double2* Z0 = (double2*)h->ws;
     double2* P0 = Z0 + (size_t)sb_max * m * LDZ;
+    double2* Xh0 = P0 + (size_t)sb_max * pst;
+    double2* W22h0 = Xh0 + (size_t)sb_max * xh_stride;
+    double2* Y0 = W22h0 + (size_t)sb_max * w22h_stride;
     double* pan = nullptr;  // k_fark's packed panel, after the 1 MB scratch of fro2_trace
-    if (two_level && fark_supported(h, m, a.mode)) {
+    if (two_level && fark_supported(h, m, mode_far)) {
         int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(n, ptop), 1);
         if (rc) return rc;
         pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
@@ -1371,6 +1513,13 @@ int run_sweep(ss_handle* h, const SweepArgs& a, cudaStream_t st) {
             B.Z = Z0 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * pst;
             B.pan = pan;
+            if (a.defer) {
+                B.Xh = Xh0 + (size_t)off * xh_stride;
+                B.W22h = W22h0 + (size_t)off * w22h_stride;
+                B.Y = Y0 + (size_t)off * m;
+                B.xh_stride = xh_stride;
+                B.w22h_stride = w22h_stride;
+            }
             int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, tile,
                                   two_level, streams[p], feed);
             if (rc) return rc;

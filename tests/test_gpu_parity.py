@@ -496,6 +496,52 @@ def test_block_groups_vs_oracle(group, n, m, p, monkeypatch):
     assert max(rel(X[:, k], Xo[:, k]) for k in range(3)) <= 1e-11
 
 
+@pytest.mark.parametrize("n,m", [(1111, 10), (700, 20), (389, 20), (1400, 5), (650, 8), (130, 4)])
+def test_reduced_deferred_identity_vs_swept(n, m, monkeypatch):
+    """Reduced solve on the two-level sweep with the identity top deferred
+    (x expanded from the kept composites, k_expand) against the identity rows
+    swept as the reference does (SS_NO_DEFER=1) and the oracle; failure
+    isolation keeps NaN columns."""
+    chf = _mhess_triple(n, m, 3, seed=n + 5 * m)
+    rng = np.random.default_rng(n * m)
+    s = 11
+    shifts = (rng.uniform(-0.5, 1.0, s) + 1j * rng.uniform(-1.5, 1.5, s)) * np.sqrt(n)
+    bd = rng.standard_normal((m, s)) + 1j * rng.standard_normal((m, s))
+    X = ss.solve_shifted_reduced(chf, shifts, bd, nb=64).x
+    Xb = ss.solve_shifted_reduced(chf, shifts, bd, nb=64, batch_size=4).x
+    assert np.array_equal(X, Xb)
+    Xo, fo = O.solve_reduced(chf.Ahat, chf.Bhat, shifts, bd, nb=64, threads=4)
+    assert (fo < 0).all()
+    assert max(rel(X[:, k], Xo[:, k]) for k in range(s)) <= 1e-11
+    monkeypatch.setenv("SS_NO_DEFER", "1")
+    Xs = ss.solve_shifted_reduced(chf, shifts, bd, nb=64).x
+    assert max(rel(X[:, k], Xs[:, k]) for k in range(s)) <= 1e-12
+    for k in range(3):
+        cert = ss.solvers.residual_certificate(chf, shifts[k], X[:, k], chf.Bhat[:, :m] @ bd[:, k])
+        assert cert <= 1e-13
+
+
+def test_reduced_deferred_failure_isolation():
+    """A shift on the spectrum fails alone in the deferred reduced solve
+    (NaN column, the pivot index as the reference reports it), the other
+    columns are bitwise those of a run without it."""
+    n, m = 300, 5
+    chf = _mhess_triple(n, m, 2, seed=77)
+    # decouple the leading m columns: eig(A11) are eigenvalues of Ahat and a
+    # shift there leaves the HEAD singular (where the reference tests pivots)
+    chf.Ahat[m:2 * m, :m] = 0.0
+    ev = np.linalg.eigvals(chf.Ahat[:m, :m])
+    shifts = np.array([0.3 + 2j, ev[0], -1.0 + 0.5j, 4j])
+    bd = np.exp(1j * np.arange(m * 4).reshape(m, 4))
+    res = ss.solve_shifted_reduced(chf, shifts, bd, nb=64, on_singular="mark")
+    Xo, fo = O.solve_reduced(chf.Ahat, chf.Bhat, shifts, bd, nb=64, threads=4)
+    assert res.failures == {int(l): int(fo[l]) for l in np.nonzero(fo >= 0)[0]}
+    assert 1 in res.failures and np.isnan(res.x[:, 1]).all()
+    keep = [0, 2, 3]
+    clean = ss.solve_shifted_reduced(chf, shifts[keep], bd[:, keep], nb=64).x
+    assert np.array_equal(clean, res.x[:, keep])
+
+
 @pytest.mark.parametrize("n,m,p,s", [(1111, 10, 10, 26), (700, 10, 3, 9), (389, 20, 7, 13),
                                      (1500, 20, 20, 41), (260, 20, 1, 5), (1337, 10, 5, 17)])
 def test_fark_vs_passes_and_oracle(n, m, p, s, monkeypatch):
