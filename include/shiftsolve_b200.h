@@ -87,7 +87,7 @@ int ss_tf_eval_stream(ss_handle* h, int n, int m, int p, const double* Ahat_host
 /* Structured pseudospectrum: ss_tf_eval (G into the caller's scratch G)
  * followed by a device epilogue norms[l] = ||G_l||_2 (p x m block; +inf for
  * a singular shift).  Replaces solvers.py:501-530 (two_norm_small's numpy
- * SVD).  Requires min(p, m) <= 32. */
+ * SVD): Gram matrix + parallel Hermitian Jacobi per shift, any p >= 1, m. */
 int ss_pspec_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t lda,
                   const double* Bhat, int64_t ldb, const double* Chat, int64_t ldc,
                   const double* shifts, int64_t s, int nb, int64_t batch, double rtol, double* G,
@@ -106,8 +106,9 @@ int ss_solve_reduced(ss_handle* h, int n, int m, const double* Ahat, int64_t lda
  * (top-down LQ sweep with fused forward substitution, batched.py:125-182).
  * rhs: n x s complex128 (ldr); X: n x s complex128 (ldx), NaN column on
  * failure; fail_row[l]: -1 or the 0-based row of the first pivot that fell
- * below rtol*||Ahat - sigma_l I||_F.  Requires m + 1 <= 32; nb is clamped
- * to 32 (one warp per window). */
+ * below rtol*||Ahat - sigma_l I||_F.  Requires m + 1 <= 256; nb is clamped
+ * to 32 (one warp per window), and for m + 1 > 32 to what the shared-memory
+ * window of k_lq_big holds. */
 int ss_solve_transposed(ss_handle* h, int n, int m, const double* Ahat, int64_t lda,
                         const double* shifts, int64_t s, const double* rhs, int64_t ldr,
                         int nb, int64_t batch, double rtol, double* X, int64_t ldx,

@@ -130,9 +130,11 @@ int fro2_trace(ss_handle* h, int n, const double* A, int64_t lda, cudaStream_t s
         if (_e != cudaSuccess) return ss::cuda_err(h, _e, #expr); \
     } while (0)
 
+#define SS_STR2(x) #x
+#define SS_STR(x) SS_STR2(x)
 #define SS_LAUNCH_CHECK(h)                                     \
     do {                                                       \
         (h)->launches++;                                       \
         cudaError_t _e = cudaGetLastError();                   \
-        if (_e != cudaSuccess) return ss::cuda_err(h, _e, "kernel launch"); \
+        if (_e != cudaSuccess) return ss::cuda_err(h, _e, "kernel launch at " __FILE__ ":" SS_STR(__LINE__)); \
     } while (0)

@@ -253,20 +253,214 @@ __global__ void __launch_bounds__(32) k_lq(TDims d, LqStep st, const double2* __
 }
 
 // ---------------------------------------------------------------------------
+// wide windows (m + 1 > 32): the same per-window LQ, chain and forward
+// substitution, with the block rows in shared memory instead of registers.
+//   * chain (warp 0, lane = block row): R[i][e] holds block columns
+//     e = 0..nb+m-1 of row i (e < m: the state z2, e >= m: panel column
+//     e - m of A^T, lazy -sigma on the block diagonal); step t's window is
+//     columns t..t+m of every row >= t.  The reflector vector u_t (L
+//     entries) is written over row t's window once row t has retired (only
+//     its diagonal, the pivot, is still needed, and it has been broadcast).
+//   * reverse accumulation (all threads): G threads per vector (G = 4, 8, 16
+//     for L <= 64, 128, 256), each holding 16 consecutive window entries in
+//     registers; dot products reduce over the group with xor shuffles and
+//     the window slides across the group with shfl_up.  Vectors are taken in
+//     rounds of blockDim / G.
+// Output Pout as k_lq.
+// ---------------------------------------------------------------------------
+constexpr int kLqBigThreads = 128;
+constexpr int kLqBigHW = 16;  // window entries per thread of a group (64 registers)
+
+__host__ __device__ inline int lq_big_rs(int nb, int m) { return (nb + m) | 1; }  // odd: conflict-free
+__host__ __device__ inline size_t lq_big_smem(int nb, int m) {
+    return ((size_t)32 * lq_big_rs(nb, m) + (m + 1) + 32 + 32 + 1) * 16;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kLqBigThreads) k_lq_big(TDims d, LqStep st, const double2* __restrict__ S,
+                                                          double2* __restrict__ Pout) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int HW = kLqBigHW;
+    const int m = d.m, L = m + 1, nb = st.nb, mp = d.mp;
+    const int RS = lq_big_rs(nb, m);
+    double2* R = reinterpret_cast<double2*>(smem);  // [32][RS]
+    double2* Uu = R + 32 * RS;                      // [L] current reflector
+    double2* Tau = Uu + L;                          // [32]
+    double2* Y = Tau + 32;                          // [32]
+    int* sfail = reinterpret_cast<int*>(Y + 32);
+    const int l = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (d.fail[l] >= 0) return;  // failed in an earlier window: left as is (NaN at the end)
+    const double2 sig = d.shifts[l];
+    const double2* Sl = S + (int64_t)l * mp * d.LDS;
+    double2* Po = Pout + (int64_t)l * (nb + mp) * mp;
+    // stage the block rows: state columns (coalesced along rows), then the
+    // panel of A^T (coalesced along columns: A^T(row, c) = A[c + row lda])
+    for (int v = tid; v < nb * m; v += blockDim.x) {
+        const int e = v / nb, i = v - e * nb;
+        R[i * RS + e] = Sl[(int64_t)e * d.LDS + st.k0 + i];
+    }
+    for (int v = tid; v < nb * nb; v += blockDim.x) {
+        const int i = v / nb, j = v - i * nb;
+        double2 x = make_double2(d.A[st.c0 + j + (int64_t)(st.k0 + i) * d.lda], 0.0);
+        if (i == m + j) x = csub(x, sig);  // block diagonal (lazy shift), solvers.py:398-400
+        R[i * RS + m + j] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const bool mine = lane < nb;
+        const double tol = d.tol[l];
+        double2 y = mine ? Sl[(int64_t)m * d.LDS + st.k0 + lane] : cz();
+        int fail = -1;
+        for (int t = 0; t < nb; ++t) {
+            double2* Rt = R + t * RS + t;
+            // reflector of row t (pivot first): zlarfg on y = conj(row)
+            double s2 = 0.0;
+            for (int j = 1 + lane; j < L; j += 32) s2 = fma(Rt[j].x, Rt[j].x, fma(Rt[j].y, Rt[j].y, s2));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            const double2 alpha = make_double2(Rt[0].x, -Rt[0].y);
+            double2 tau = cz(), scale = cz();
+            if (!(s2 == 0.0 && alpha.y == 0.0)) {
+                const double nrm2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
+                const double rn = rsqrt(nrm2);
+                const double sg = alpha.x >= 0.0 ? -1.0 : 1.0;
+                const double beta = sg * nrm2 * rn;
+                const double ib = sg * rn;
+                tau = make_double2(1.0 - alpha.x * ib, -alpha.y * ib);
+                const double zx = alpha.x - beta, zy = alpha.y;
+                const double rz = rsqrt(fma(zx, zx, zy * zy));
+                const double iz = rz * rz;
+                scale = make_double2(zx * iz, -zy * iz);
+            }
+            for (int j = lane; j < L; j += 32) {
+                const double2 x = Rt[j];
+                Uu[j] = j == 0 ? make_double2(1.0, 0.0) : cmul(make_double2(x.x, -x.y), scale);
+            }
+            __syncwarp();
+            // rows t..nb-1 (row t included): r <- r - tau (r . u) conj(u)
+            double2 r0 = cz();
+            if (mine && lane >= t) {
+                double2* rr = R + lane * RS + t;
+                double2 d0 = cz(), d1 = cz();
+                for (int j = 0; j < L; ++j) {
+                    double2& dd = (j & 1) ? d1 : d0;
+                    dd = cfma(rr[j], Uu[j], dd);
+                }
+                const double2 tw = cmul(tau, cadd(d0, d1));
+                for (int j = 0; j < L; ++j) {
+                    const double2 u = Uu[j];
+                    double2 r = rr[j];
+                    r.x = fma(-tw.x, u.x, fma(-tw.y, u.y, r.x));
+                    r.y = fma(-tw.y, u.x, fma(tw.x, u.y, r.y));
+                    rr[j] = r;
+                }
+                r0 = rr[0];
+            }
+            // forward substitution on the window's w segment (batched.py:170-178)
+            const double2 piv = make_double2(__shfl_sync(0xffffffffu, r0.x, t), __shfl_sync(0xffffffffu, r0.y, t));
+            if (fail < 0 && hypot(piv.x, piv.y) <= tol) fail = st.k0 + t;
+            double2 yt = make_double2(__shfl_sync(0xffffffffu, y.x, t), __shfl_sync(0xffffffffu, y.y, t));
+            yt = cdiv(yt, piv);
+            if (lane == t) y = yt;
+            if (mine && lane > t) y = csub(y, cmul(r0, yt));
+            if (lane == 0) Tau[t] = tau;
+            __syncwarp();
+            for (int j = lane; j < L; j += 32) Rt[j] = Uu[j];  // row t retired: keep u_t
+            __syncwarp();
+        }
+        if (mine) Y[lane] = y;
+        if (lane == 0) *sfail = fail;
+    }
+    __syncthreads();
+    if (*sfail >= 0) {
+        if (tid == 0) d.fail[l] = *sfail;
+        return;
+    }
+    // reverse accumulation: vector q < m is e_{nb+q}, vector m is [y; 0];
+    // P = H_0 ... H_{nb-1}: H_{nb-1} first; window = block columns t..t+m
+    const int gi = tid % G, base = gi * HW;
+    const unsigned gmask = 0xffffffffu;
+    for (int q0 = 0; q0 <= m; q0 += kLqBigThreads / G) {
+        const int q = q0 + tid / G;
+        const bool act = q <= m;
+        double2 w[HW];
+#pragma unroll
+        for (int k = 0; k < HW; ++k)
+            w[k] = make_double2(q < m && base + k == q + 1 ? 1.0 : 0.0, 0.0);
+        if (q == m && gi == 0) w[0] = Y[nb - 1];
+        for (int t = nb - 1; t >= 0; --t) {
+            const double2* U = R + t * RS + t;
+            double2 d0 = cz(), d1 = cz();
+#pragma unroll
+            for (int k = 0; k < HW; ++k) {
+                if (base + k < L) {
+                    const double2 u = U[base + k];
+                    double2& dd = (k & 1) ? d1 : d0;
+                    dd = cfma(make_double2(u.x, -u.y), w[k], dd);
+                }
+            }
+            double2 dp = cadd(d0, d1);
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+                dp.x += __shfl_xor_sync(gmask, dp.x, o);
+                dp.y += __shfl_xor_sync(gmask, dp.y, o);
+            }
+            const double2 td = cmul(Tau[t], dp);
+            double2 fin = cz();
+#pragma unroll
+            for (int k = 0; k < HW; ++k) {
+                if (base + k < L) w[k] = csub(w[k], cmul(U[base + k], td));
+                if (base + k == m) fin = w[k];
+            }
+            // entry t + m (block column e = t + m >= m: Pout row t) is final
+            if (act && base <= m && m < base + HW) {
+                if (q == m) fin = make_double2(-fin.x, -fin.y);
+                Po[(int64_t)t * mp + q] = fin;
+            }
+            // slide right by one across the group
+            const double nx = __shfl_up_sync(gmask, w[HW - 1].x, 1);
+            const double ny = __shfl_up_sync(gmask, w[HW - 1].y, 1);
+#pragma unroll
+            for (int k = HW - 1; k > 0; --k) w[k] = w[k - 1];
+            w[0] = gi > 0 ? make_double2(nx, ny) : ((q == m && t > 0) ? Y[t - 1] : cz());
+        }
+        // remaining entries 1..m (block columns 0..m-1 = state rows)
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < HW; ++k) {
+                const int j = base + k;
+                if (j >= 1 && j <= m) {
+                    double2 v = w[k];
+                    if (q == m) v = make_double2(-v.x, -v.y);
+                    Po[(int64_t)(nb + j - 1) * mp + q] = v;
+                }
+            }
+            if (gi == 0) Po[(int64_t)(nb + m) * mp + q] = make_double2(q == m ? 1.0 : 0.0, 0.0);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // rows below the window (solvers.py:431-468): S <- S T + Pan U12, with
 //   Pan(i, j) = A^T(i, c0 + j) for i < n, -[i - n == c0 + j] for i >= n,
 // lazy-shift rows k0 + nb + (m - mnb) + dd: S -= sigma P12[nb - mnb + dd].
-// One thread per row, all mp columns; panel tile staged in shared memory.
+// One thread per row, all mp columns; panel tile staged in shared memory,
+// the shift's P in shared memory too when it fits (PSM), else read through
+// L1 (the same element for every thread: a broadcast).
 // ---------------------------------------------------------------------------
-constexpr int kTuRows = 128;
+__host__ inline size_t tupd_smem(int rows, bool psm, int nb, int mp) {
+    return (size_t)nb * rows * 8 + (psm ? (size_t)(nb + mp) * mp * 16 : 0) + (size_t)mp * rows * 16;
+}
 
-__global__ void __launch_bounds__(kTuRows) k_tupd(TDims d, LqStep st, double2* __restrict__ S,
-                                                  const double2* __restrict__ Pbuf, int sg_size) {
+template <int ROWS, bool PSM>
+__global__ void __launch_bounds__(ROWS) k_tupd(TDims d, LqStep st, double2* __restrict__ S,
+                                               const double2* __restrict__ Pbuf, int sg_size) {
+    constexpr int kTuRows = ROWS;
     extern __shared__ __align__(16) unsigned char smem[];
     const int m = d.m, mp = d.mp, nb = st.nb;
     double* Pan = reinterpret_cast<double*>(smem);                                // [nb][kTuRows]
-    double2* Ps = reinterpret_cast<double2*>(smem + (size_t)nb * kTuRows * 8);   // (nb+mp) x mp
-    double2* Rb = Ps + (nb + mp) * mp;                                            // [mp][kTuRows] row copy
+    double2* Psm = reinterpret_cast<double2*>(smem + (size_t)nb * kTuRows * 8);  // (nb+mp) x mp
+    double2* Rb = Psm + (PSM ? (nb + mp) * mp : 0);                               // [mp][kTuRows] row copy
     const int rlo = st.k0 + nb;
     const int i = rlo + blockIdx.x * kTuRows + threadIdx.x;
     const int ihi = 2 * d.n;
@@ -285,7 +479,9 @@ __global__ void __launch_bounds__(kTuRows) k_tupd(TDims d, LqStep st, double2* _
         __syncthreads();
         if (d.fail[l] >= 0) continue;
         const double2* pl = Pbuf + (int64_t)l * (nb + mp) * mp;
-        for (int v = threadIdx.x; v < (nb + mp) * mp; v += blockDim.x) Ps[v] = pl[v];
+        if (PSM)
+            for (int v = threadIdx.x; v < (nb + mp) * mp; v += blockDim.x) Psm[v] = pl[v];
+        const double2* Ps = PSM ? Psm : pl;
         __syncthreads();
         if (i >= ihi) continue;
         double2* Sl = S + (int64_t)l * mp * d.LDS;
@@ -425,9 +621,12 @@ cudaError_t allow_smem(ss_handle* h, F* fn) {
                                 (int)(h->smem_optin - fa.sharedSizeBytes));
 }
 
+constexpr int kLqMaxL = 256;  // widest window (k_lq_big with 16 threads per vector)
+
 int launch_lq(ss_handle* h, int m, int sb, cudaStream_t st, const TDims& d, const LqStep& s,
               const double2* S, double2* P) {
     const int L = m + 1;
+    const size_t big = lq_big_smem(s.nb, m);
     if (L <= 2) k_lq<2><<<sb, 32, 0, st>>>(d, s, S, P);
     else if (L <= 4) k_lq<4><<<sb, 32, 0, st>>>(d, s, S, P);
     else if (L <= 8) k_lq<8><<<sb, 32, 0, st>>>(d, s, S, P);
@@ -435,7 +634,32 @@ int launch_lq(ss_handle* h, int m, int sb, cudaStream_t st, const TDims& d, cons
     else if (L <= 16) k_lq<16><<<sb, 32, 0, st>>>(d, s, S, P);
     else if (L <= 24) k_lq<24><<<sb, 32, 0, st>>>(d, s, S, P);
     else if (L <= 32) k_lq<32><<<sb, 32, 0, st>>>(d, s, S, P);
-    else return ss::set_err(h, SS_EARG, "transposed solve: m + 1 must be <= 32");
+    else if (L <= 4 * kLqBigHW) k_lq_big<4><<<sb, kLqBigThreads, big, st>>>(d, s, S, P);
+    else if (L <= 8 * kLqBigHW) k_lq_big<8><<<sb, kLqBigThreads, big, st>>>(d, s, S, P);
+    else if (L <= 16 * kLqBigHW) k_lq_big<16><<<sb, kLqBigThreads, big, st>>>(d, s, S, P);
+    else return ss::set_err(h, SS_EARG, "transposed solve: m + 1 must be <= 256");
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+// rows-below update: the widest variant whose shared memory fits
+int launch_tupd(ss_handle* h, cudaStream_t st, const TDims& d, const LqStep& s, double2* S,
+                const double2* P, int rows_total) {
+    const int sg = 8, nb = s.nb, mp = d.mp;
+    const size_t cap = h->smem_optin;
+    const unsigned gy = (unsigned)((d.sb + sg - 1) / sg);
+    auto grid = [&](int r) { return dim3((unsigned)((rows_total + r - 1) / r), gy); };
+    size_t sm;
+    if ((sm = tupd_smem(128, true, nb, mp)) <= cap)
+        k_tupd<128, true><<<grid(128), 128, sm, st>>>(d, s, S, P, sg);
+    else if ((sm = tupd_smem(64, true, nb, mp)) <= cap)
+        k_tupd<64, true><<<grid(64), 64, sm, st>>>(d, s, S, P, sg);
+    else if ((sm = tupd_smem(64, false, nb, mp)) <= cap)
+        k_tupd<64, false><<<grid(64), 64, sm, st>>>(d, s, S, P, sg);
+    else if ((sm = tupd_smem(32, false, nb, mp)) <= cap)
+        k_tupd<32, false><<<grid(32), 32, sm, st>>>(d, s, S, P, sg);
+    else
+        return ss::set_err(h, SS_EARG, "transposed solve: m too large for the row update");
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -451,14 +675,16 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
         return ss::set_err(h, SS_EDIM, "inconsistent controller-Hessenberg form");
     if (lda < n || ldr < n || ldx < n) return ss::set_err(h, SS_EDIM, "leading dimension too small");
     if (nb < 1) return ss::set_err(h, SS_EARG, "window block size must be >= 1");
-    if (m + 1 > 32) return ss::set_err(h, SS_EARG, "transposed solve: m + 1 must be <= 32");
+    if (m + 1 > kLqMaxL) return ss::set_err(h, SS_EARG, "transposed solve: m + 1 must be <= 256");
     if (s == 0) return SS_OK;
     if (!Ahat || !shifts || !rhs || !X || !fail_row) return ss::set_err(h, SS_EARG, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
     ss::DevGuard dg(h->device);
     SS_CUDA_TRY(h, dg.err);
     const double rt = std::isnan(rtol) ? 1e3 * n * 2.220446049250313e-16 : rtol;  // NaN: default
-    const int nb0 = std::max(1, std::min(std::min(nb, kLqMaxNb), std::max(n - m, 1)));
+    int nb0 = std::max(1, std::min(std::min(nb, kLqMaxNb), std::max(n - m, 1)));
+    // wide windows keep the block rows in shared memory: shrink the window to fit
+    while (m + 1 > 32 && nb0 > 1 && lq_big_smem(nb0, m) > h->smem_optin) --nb0;
     const int mp = m + 1;
     const int64_t LDS = ((int64_t)2 * n + 7) & ~(int64_t)7;
     // ||A||_F^2 and trace(A) for the per-shift pivot tolerances
@@ -484,7 +710,13 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     double* tolb = (double*)(Pb + (size_t)sb_max * (nb0 + mp) * mp);
     static ss::DevMask attrs;  // devices configured
     if (!attrs.has(h)) {
-        SS_CUDA_TRY(h, allow_smem(h, k_tupd));
+        SS_CUDA_TRY(h, allow_smem(h, k_tupd<128, true>));
+        SS_CUDA_TRY(h, allow_smem(h, k_tupd<64, true>));
+        SS_CUDA_TRY(h, allow_smem(h, k_tupd<64, false>));
+        SS_CUDA_TRY(h, allow_smem(h, k_tupd<32, false>));
+        SS_CUDA_TRY(h, allow_smem(h, k_lq_big<4>));
+        SS_CUDA_TRY(h, allow_smem(h, k_lq_big<8>));
+        SS_CUDA_TRY(h, allow_smem(h, k_lq_big<16>));
         attrs.set(h);
     }
     for (int64_t lo = 0; lo < s; lo += sb_max) {
@@ -517,13 +749,9 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
             if (rc) return rc;
             ss::timing_end(h, st, ev, ss::PH_RQ);
             const int rows = 2 * n - (k0 + ls.nb);
-            const int sg = 8;
-            dim3 g((unsigned)((rows + kTuRows - 1) / kTuRows), (unsigned)((sb + sg - 1) / sg));
-            const size_t sm = (size_t)ls.nb * kTuRows * 8 + (size_t)(ls.nb + mp) * mp * 16 +
-                              (size_t)mp * kTuRows * 16;
             ev = ss::timing_begin(h, st);
-            k_tupd<<<g, kTuRows, sm, st>>>(d, ls, Sb, Pb, sg);
-            SS_LAUNCH_CHECK(h);
+            rc = launch_tupd(h, st, d, ls, Sb, Pb, rows);
+            if (rc) return rc;
             const double fl_b = (double)sb * 8.0 * rows * mp * mp;
             const double fl_o = (double)sb * 8.0 * rows * mp * ls.nb;
             h->flops[ss::PH_BATCHED_GEMM] += fl_b;

@@ -221,13 +221,15 @@ struct HeadOut {
     int64_t ldo;
     int32_t* fail;       // batch-local
     double2* ybuf;       // deferred reduced solve: y = Qh X (m per shift) for k_expand
+    int l0;              // first batch-local shift of this launch
+    double2* gscr;       // non-null: Hh / Qh / X in global scratch (3 m^2 per CTA; wide m)
 };
 
 __global__ void k_head(Dims d, HeadOut h, const double2* __restrict__ Z2) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int m = d.m, l = blockIdx.x;
+    const int m = d.m, l = h.l0 + blockIdx.x;
     const int q = h.mode == 0 ? m : 1;
-    double2* Hh = (double2*)smem;  // m x m, col-major
+    double2* Hh = h.gscr ? h.gscr + (int64_t)blockIdx.x * 3 * m * m : (double2*)smem;  // m x m, col-major
     double2* Qh = Hh + m * m;      // m x m
     double2* X = Qh + m * m;       // m x q
     __shared__ int s_fail;
@@ -451,14 +453,19 @@ UpdTile pick_tile(int m) {
 template <int G, int C, bool EXACT>
 int launch_update_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStream_t st,
                     const UpdDims& u, const double2* zin, double2* zout, const double2* pbuf) {
-    if (threads > 256) {
+    if (threads > 256 || smem > h->smem_optin) {
         // K-split with several column blocks per shift (m > 31): up to 10 warps
         static ss::DevMask configured_w;  // devices configured
         if (!configured_w.has(h)) {
             SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320>));
+            SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320, true>));
             configured_w.set(h);
         }
-        k_update<G, C, EXACT, 320><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
+        if (smem > h->smem_optin)  // staged P does not fit: read it from global memory
+            k_update<G, C, EXACT, 320, true><<<grid, threads, upd_smem_bytes(u.nb, u.m, u.S, true), st>>>(
+                u, zin, zout, pbuf);
+        else
+            k_update<G, C, EXACT, 320><<<grid, threads, smem, st>>>(u, zin, zout, pbuf);
         SS_LAUNCH_CHECK(h);
         return SS_OK;
     }
@@ -590,15 +597,19 @@ int launch_update(ss_handle* h, const UpdTile& t, dim3 grid, int threads, size_t
     return ss::set_err(h, SS_EARG, "unsupported update tile");
 }
 
+// widest window <= nb_req whose block RQ and update fit one SM's shared
+// memory (the update may read P from global memory, k_update<..., PG>);
+// 0 if none does (m too wide for this device)
 int max_nb_for(ss_handle* h, int m, int nb_req) {
-    int nb = nb_req;
-    while (nb > 1) {
+    for (int nb = nb_req; nb >= 1; nb = nb > 8 ? nb - 8 : nb - 1) {
         const size_t need = rq_smem_bytes(nb, m, nb * m, nb * m);
-        const size_t upd = upd_smem_bytes(nb, m, 1);
-        if (need <= h->smem_optin && upd <= h->smem_optin && nb + m <= 255) break;
-        nb = nb > 8 ? nb - 8 : nb - 1;
+        const size_t upd = upd_smem_bytes(nb, m, 1, true);
+        // m + 1 > 64 runs the scheduled Givens batch (k_rq): <= 16 warps keep
+        // at most 8 x 32 rotations each in registers (~ nb m / 16 + nb + m)
+        const bool rots_ok = m + 1 <= 64 || nb * m / 16 + nb + m <= 256;
+        if (need <= h->smem_optin && upd <= h->smem_optin && nb + m <= 255 && rots_ok) return nb;
     }
-    return nb < 1 ? 1 : nb;
+    return 0;
 }
 
 struct SweepArgs {
@@ -1224,8 +1235,25 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     }
     cudaEvent_t evh = ss::timing_begin(h, st);
     const size_t smem_h = (size_t)(2 * m * m + m * (a.mode == 0 ? m : 1)) * 16;
-    k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z);
-    SS_LAUNCH_CHECK(h);
+    if (smem_h <= h->smem_optin) {
+        ho.l0 = 0;
+        ho.gscr = nullptr;
+        k_head<<<sb, 128, smem_h, st>>>(d, ho, B.Z);
+        SS_LAUNCH_CHECK(h);
+    } else {
+        // wide m (3 m^2 complex > shared memory): the head matrices of up to
+        // `chunk` shifts at a time in global scratch (L2-resident for one wave)
+        const size_t per = (size_t)3 * m * m * 16;
+        const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)sb, ((size_t)256 << 20) / per));
+        int rc = ss::ensure_ws(h, per * chunk, 1);
+        if (rc) return rc;
+        ho.gscr = (double2*)h->ws2;
+        for (int l0 = 0; l0 < sb; l0 += chunk) {
+            ho.l0 = l0;
+            k_head<<<std::min(chunk, sb - l0), 128, 0, st>>>(d, ho, B.Z);
+            SS_LAUNCH_CHECK(h);
+        }
+    }
     if (a.defer) {
         ExpandArgs e;
         e.n = n;
@@ -1258,79 +1286,166 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
 // ---------------------------------------------------------------------------
 // Pseudospectrum epilogue (solvers.py:501-530 structured_pseudospectrum_grid
 // with two_norm_small): ||G_l||_2 of every p x m block on the device.  One
-// 32-thread CTA per shift forms the k x k Gram matrix (k = min(p, m)) in
-// shared memory and thread 0 runs cyclic complex Hermitian Jacobi to
-// convergence; ||G||_2 = sqrt(lambda_max).  Failed shifts give +inf.
+// 128-thread CTA per shift (persistent over shifts) forms the k x k Gram
+// matrix H (k = min(p, m)) and runs parallel two-sided Hermitian Jacobi to
+// convergence: per round the k/2 disjoint pairs of a round-robin ordering
+// (Brent-Luk) get their rotations from the 2x2 blocks of H, then all
+// column updates (disjoint columns), then all row updates (disjoint rows),
+// each spread over the CTA; ||G||_2 = sqrt(lambda_max).  H lives in shared
+// memory for k <= kPnSmem, else in a per-CTA slot of global scratch (L2).
+// Failed shifts give +inf.
 // ---------------------------------------------------------------------------
-constexpr int kPnMax = 32;
+constexpr int kPnThreads = 128;
+constexpr int kPnSmem = 96;  // 96 x 97 x 16 B = 149 KB
 
-__global__ void __launch_bounds__(32) k_pnorm(int p, int m, const double2* __restrict__ G,
-                                              int64_t ldg, const int32_t* __restrict__ fail,
-                                              double* __restrict__ norms) {
-    __shared__ double2 H[kPnMax][kPnMax + 1];
-    const int l = blockIdx.x, tid = threadIdx.x;
-    const double2* Gl = G + (int64_t)l * m * ldg;  // G_l(i, j) = Gl[i + j * ldg]
-    if (fail[l] >= 0) {
-        if (tid == 0) norms[l] = __longlong_as_double(0x7ff0000000000000ULL);
-        return;
-    }
+__host__ __device__ inline int pn_ld(int k) { return k + 1; }
+// per-pair arrays (k/2 + 1 pairs) + reduction slots, rounded up so H
+// (double2) is 16-byte aligned
+__host__ __device__ inline int pn_pairs(int k) { return k / 2 + 1; }
+__host__ __device__ inline size_t pnorm_hdr_bytes(int k) {
+    return (((size_t)pn_pairs(k) * (16 + 8 + 8 + 4 + 4) + (kPnThreads / 32 + 2) * 8) + 15) & ~(size_t)15;
+}
+
+template <bool GLOBAL_H>
+__global__ void __launch_bounds__(kPnThreads) k_pnorm(int p, int m, int64_t s, const double2* __restrict__ G,
+                                                      int64_t ldg, const int32_t* __restrict__ fail,
+                                                      double* __restrict__ norms, double2* __restrict__ scratch) {
+    extern __shared__ __align__(16) unsigned char smem[];
     const bool gram_cols = p >= m;  // H = G^H G (m x m) or G G^H (p x p)
     const int k = gram_cols ? m : p, r = gram_cols ? p : m;
-    for (int u = tid; u < k * k; u += 32) {
-        const int i = u % k, j = u / k;
-        double2 acc = cz();
-        for (int t = 0; t < r; ++t) {
-            const double2 a = gram_cols ? Gl[t + (int64_t)i * ldg] : Gl[i + (int64_t)t * ldg];
-            const double2 b = gram_cols ? Gl[t + (int64_t)j * ldg] : Gl[j + (int64_t)t * ldg];
-            // gram_cols: conj(G_ti) G_tj ; else G_it conj(G_jt)
-            const double2 x = gram_cols ? make_double2(a.x, -a.y) : a;
-            const double2 y = gram_cols ? b : make_double2(b.x, -b.y);
-            acc = cfma(x, y, acc);
+    const int kp = k + (k & 1);  // padded with a dummy index when k is odd
+    const int np = kp / 2, ld = pn_ld(k);
+    const int tid = threadIdx.x;
+    // per-pair rotation: e (phase of H[a][b]), cs, sn, the pair (a, b)
+    const int npk = pn_pairs(k);
+    double2* e_ = reinterpret_cast<double2*>(smem);
+    double* cs_ = reinterpret_cast<double*>(e_ + npk);
+    double* sn_ = cs_ + npk;
+    double* red = sn_ + npk;  // [kPnThreads / 32 + 2]
+    int* pa = reinterpret_cast<int*>(red + kPnThreads / 32 + 2);
+    int* pb = pa + npk;
+    double2* H = GLOBAL_H ? scratch + (int64_t)blockIdx.x * k * ld
+                          : reinterpret_cast<double2*>(smem + pnorm_hdr_bytes(k));
+    for (int64_t l = blockIdx.x; l < s; l += gridDim.x) {
+        __syncthreads();  // H of the previous shift is dead
+        if (fail[l] >= 0) {
+            if (tid == 0) norms[l] = __longlong_as_double(0x7ff0000000000000ULL);
+            continue;
         }
-        H[i][j] = acc;
-    }
-    __syncthreads();
-    if (tid != 0) return;
-    double fro2 = 0.0;
-    for (int i = 0; i < k; ++i)
-        for (int j = 0; j < k; ++j) fro2 += H[i][j].x * H[i][j].x + H[i][j].y * H[i][j].y;
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        double off = 0.0;
-        for (int i = 0; i < k; ++i)
-            for (int j = i + 1; j < k; ++j) off += H[i][j].x * H[i][j].x + H[i][j].y * H[i][j].y;
-        if (off <= 1e-32 * fro2 || off == 0.0) break;
-        for (int a = 0; a < k; ++a) {
-            for (int b = a + 1; b < k; ++b) {
-                const double2 c = H[a][b];
-                const double ac = hypot(c.x, c.y);
-                if (ac == 0.0) continue;
-                const double2 e = make_double2(c.x / ac, c.y / ac);
-                const double ha = H[a][a].x, hb = H[b][b].x;
-                const double tau = (hb - ha) / (2.0 * ac);
-                const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
-                const double2 ce = make_double2(e.x, -e.y);
+        const double2* Gl = G + l * m * ldg;  // G_l(i, j) = Gl[i + j * ldg]
+        double f2 = 0.0;
+        for (int u = tid; u < k * k; u += blockDim.x) {
+            const int i = u % k, j = u / k;
+            double2 acc = cz();
+            for (int t = 0; t < r; ++t) {
+                const double2 a = gram_cols ? Gl[t + (int64_t)i * ldg] : Gl[i + (int64_t)t * ldg];
+                const double2 b = gram_cols ? Gl[t + (int64_t)j * ldg] : Gl[j + (int64_t)t * ldg];
+                // gram_cols: conj(G_ti) G_tj ; else G_it conj(G_jt)
+                const double2 x = gram_cols ? make_double2(a.x, -a.y) : a;
+                const double2 y = gram_cols ? b : make_double2(b.x, -b.y);
+                acc = cfma(x, y, acc);
+            }
+            H[i * ld + j] = acc;
+            f2 = fma(acc.x, acc.x, fma(acc.y, acc.y, f2));
+        }
+        // block sum helper (deterministic order)
+        auto bsum = [&](double v) -> double {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            __syncthreads();
+            if ((tid & 31) == 0) red[tid >> 5] = v;
+            __syncthreads();
+            double t = 0.0;
+            for (int w = 0; w < kPnThreads / 32; ++w) t += red[w];
+            return t;
+        };
+        const double fro2 = bsum(f2);
+        for (int sweep = 0; sweep < 40 && k > 1; ++sweep) {
+            double o = 0.0;
+            for (int u = tid; u < k * k; u += blockDim.x) {
+                const int i = u % k, j = u / k;
+                if (i < j) o = fma(H[i * ld + j].x, H[i * ld + j].x, fma(H[i * ld + j].y, H[i * ld + j].y, o));
+            }
+            const double off = bsum(o);
+            if (off <= 1e-32 * fro2 || off == 0.0) break;
+            for (int rd = 0; rd < kp - 1; ++rd) {
+                // round-robin pairs: (rd, kp - 1) and ((rd + i), (rd - i)) mod (kp - 1)
+                for (int i = tid; i < np; i += blockDim.x) {
+                    int a = i == 0 ? rd : (rd + i) % (kp - 1);
+                    int b = i == 0 ? kp - 1 : (rd - i + kp - 1) % (kp - 1);
+                    if (a > b) { const int t = a; a = b; b = t; }
+                    double cs = 1.0, sn = 0.0;
+                    double2 e = make_double2(1.0, 0.0);
+                    if (b < k) {
+                        const double2 c = H[a * ld + b];
+                        const double ac = hypot(c.x, c.y);
+                        if (ac != 0.0) {
+                            e = make_double2(c.x / ac, c.y / ac);
+                            const double ha = H[a * ld + a].x, hb = H[b * ld + b].x;
+                            const double tau = (hb - ha) / (2.0 * ac);
+                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                            cs = 1.0 / sqrt(1.0 + t * t);
+                            sn = t * cs;
+                        }
+                    }
+                    cs_[i] = cs;
+                    sn_[i] = sn;
+                    e_[i] = e;
+                    pa[i] = a;
+                    pb[i] = (b < k && sn != 0.0) ? b : -1;  // -1: no rotation
+                }
+                __syncthreads();
                 // columns: H V with V_aa = cs, V_ab = sn, V_ba = -sn conj(e), V_bb = cs conj(e)
-                for (int i = 0; i < k; ++i) {
-                    const double2 x = H[i][a], y = cmul(H[i][b], ce);
-                    H[i][a] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
-                    H[i][b] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+                for (int u = tid; u < np * k; u += blockDim.x) {
+                    const int i = u / k, row = u - i * k;
+                    const int b = pb[i];
+                    if (b < 0) continue;
+                    const int a = pa[i];
+                    const double cs = cs_[i], sn = sn_[i];
+                    const double2 ce = make_double2(e_[i].x, -e_[i].y);
+                    const double2 x = H[row * ld + a], y = cmul(H[row * ld + b], ce);
+                    H[row * ld + a] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+                    H[row * ld + b] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
                 }
+                __syncthreads();
                 // rows: V^H (H V)
-                for (int j = 0; j < k; ++j) {
-                    const double2 x = H[a][j], y = cmul(H[b][j], e);
-                    H[a][j] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
-                    H[b][j] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+                for (int u = tid; u < np * k; u += blockDim.x) {
+                    const int i = u / k, col = u - i * k;
+                    const int b = pb[i];
+                    if (b < 0) continue;
+                    const int a = pa[i];
+                    const double cs = cs_[i], sn = sn_[i];
+                    const double2 e = e_[i];
+                    const double2 x = H[a * ld + col], y = cmul(H[b * ld + col], e);
+                    H[a * ld + col] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+                    H[b * ld + col] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
                 }
-                H[a][b] = H[b][a] = cz();
-                H[a][a] = make_double2(ha - t * ac, 0.0);
-                H[b][b] = make_double2(hb + t * ac, 0.0);
+                __syncthreads();
+                // the 2x2 blocks are diagonal now: exact zeros, real diagonals
+                for (int i = tid; i < np; i += blockDim.x) {
+                    const int b = pb[i];
+                    if (b < 0) continue;
+                    const int a = pa[i];
+                    H[a * ld + b] = H[b * ld + a] = cz();
+                    H[a * ld + a].y = 0.0;
+                    H[b * ld + b].y = 0.0;
+                }
+                __syncthreads();
             }
         }
+        __syncthreads();
+        if (tid == 0) {
+            double lmax = 0.0;
+            for (int i = 0; i < k; ++i) lmax = fmax(lmax, H[i * ld + i].x);
+            norms[l] = sqrt(lmax);
+        }
     }
-    double lmax = 0.0;
-    for (int i = 0; i < k; ++i) lmax = fmax(lmax, H[i][i].x);
-    norms[l] = sqrt(lmax);
+}
+
+__host__ inline size_t pnorm_smem(int k, bool global_h) {
+    size_t b = pnorm_hdr_bytes(k);
+    if (!global_h) b += (size_t)k * pn_ld(k) * 16;
+    return b;
 }
 
 }  // namespace
@@ -1364,6 +1479,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     // value is used as given (0: only exactly-zero pivots fail, solvers.py:227)
     const double rtol = std::isnan(a.rtol) ? 1e3 * n * 2.220446049250313e-16 : a.rtol;
     const int nb0_req = max_nb_for(h, m, std::max(1, std::min(a.nb, std::max(n - m, 1))));
+    if (nb0_req < 1) return ss::set_err(h, SS_EARG, "m too large: the window does not fit shared memory");
 
     static ss::DevMask attrs;  // devices configured
     if (!attrs.has(h)) {
@@ -1622,8 +1738,7 @@ int ss_pspec_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t
                   const double* shifts, int64_t s, int nb, int64_t batch, double rtol, double* G,
                   int64_t ldg, double* norms, int32_t* fail_row, void* stream) {
     if (!h) return SS_EARG;
-    if (p < 1 || std::min(p, m) > kPnMax)
-        return ss::set_err(h, SS_EARG, "pseudospectrum epilogue: min(p, m) must be <= 32");
+    if (p < 1) return ss::set_err(h, SS_EARG, "pseudospectrum: p must be >= 1");
     if (s > 0 && !norms) return ss::set_err(h, SS_EARG, "null pointer");
     int rc = ss_tf_eval(h, n, m, p, Ahat, lda, Bhat, ldb, Chat, ldc, shifts, s, nb, batch, rtol, G,
                         ldg, fail_row, stream);
@@ -1631,8 +1746,28 @@ int ss_pspec_eval(ss_handle* h, int n, int m, int p, const double* Ahat, int64_t
     ss::DevGuard dg(h->device);
     SS_CUDA_TRY(h, dg.err);
     cudaStream_t st = (cudaStream_t)stream;
+    const int k = std::min(p, m);
+    const bool gh = k > kPnSmem;
+    const unsigned grid = (unsigned)std::min<int64_t>(s, (int64_t)h->num_sms * 4);
+    double2* scratch = nullptr;
+    if (gh) {  // one k x (k + 1) slot per CTA (the sweep's workspace is free again)
+        rc = ss::ensure_ws(h, (size_t)grid * k * pn_ld(k) * 16, 0);
+        if (rc) return rc;
+        scratch = (double2*)h->ws;
+    }
+    static ss::DevMask attrs;
+    if (!attrs.has(h)) {
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_pnorm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)pnorm_smem(kPnSmem, false)));
+        attrs.set(h);
+    }
     cudaEvent_t ev = ss::timing_begin(h, st);
-    k_pnorm<<<(unsigned)s, 32, 0, st>>>(p, m, (const double2*)G, ldg, fail_row, norms);
+    if (gh)
+        k_pnorm<true><<<grid, kPnThreads, pnorm_smem(k, true), st>>>(p, m, s, (const double2*)G, ldg,
+                                                                     fail_row, norms, scratch);
+    else
+        k_pnorm<false><<<grid, kPnThreads, pnorm_smem(k, false), st>>>(p, m, s, (const double2*)G, ldg,
+                                                                       fail_row, norms, nullptr);
     SS_LAUNCH_CHECK(h);
     ss::timing_end(h, st, ev, ss::PH_TAIL);
     return SS_OK;

@@ -68,9 +68,9 @@ struct UpdDims {
     int flags;  // experiment knobs (bit 0: producer spins instead of parking)
 };
 
-__host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S) {
+__host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S, bool pg = false) {
     const int nc = nb + m;
-    return (size_t)nb * kUpdRows * 8 + (size_t)S * nc * m * 16 + (size_t)S * m * kUpdRows * 16;
+    return (size_t)nb * kUpdRows * 8 + (pg ? 0 : (size_t)S * nc * m * 16) + (size_t)S * m * kUpdRows * 16;
 }
 
 // panel position of tile row `row` (0..63) inside one panel column: rows of
@@ -83,7 +83,10 @@ __device__ __forceinline__ int pan_index(int row) {
     return p * (2 * RG) + rg * 2 + e;
 }
 
-template <int G, int C, bool EXACT, int MAXT = 256>
+// PG: P_l is read from global memory (L1 / L2; every lane of a row group
+// reads the same entries) instead of being staged -- windows so wide
+// (m >~ 90) that the staged P does not fit shared memory.
+template <int G, int C, bool EXACT, int MAXT = 256, bool PG = false>
 __global__ void __launch_bounds__(MAXT)
     k_update(UpdDims u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
              const double2* __restrict__ Pbuf) {
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(MAXT)
     const int nb = u.nb, m = u.m, nc = u.nc, r0 = u.r0;
     double* Pan = (double*)smem;                                        // [nb][64] (pair-interleaved)
     double2* Pst = (double2*)(smem + (size_t)nb * kUpdRows * 8);        // [S][nc*m], j-major
-    double2* Zst = Pst + (size_t)u.S * nc * m;                          // [S][m][64]
+    double2* Zst = Pst + (PG ? 0 : (size_t)u.S * nc * m);               // [S][m][64]
     const int i0 = u.rlo + blockIdx.x * kUpdRows;
     const int l0 = blockIdx.y * u.SG;
     const int lend = min(l0 + u.SG, u.sb);
@@ -133,7 +136,8 @@ __global__ void __launch_bounds__(MAXT)
         {
             const double2* src = Pbuf + (int64_t)lc * nc * m;
             const int tot = nsc * nc * m;
-            for (int v = tid; v < tot; v += blockDim.x) cp_async16(Pst + v, src + v, true);
+            if (!PG)
+                for (int v = tid; v < tot; v += blockDim.x) cp_async16(Pst + v, src + v, true);
             const int ztot = nsc * m * kUpdRows;
             for (int v = tid; v < ztot; v += blockDim.x) {
                 const int ii = v & 63, sc = v >> 6;  // sc = s*m + c
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(MAXT)
         }
         if (s_w >= nsc) continue;
         const int l = lc + s_w;
-        const double2* Pl = Pst + (size_t)s_w * nc * m + cb;
+        const double2* Pl = PG ? Pbuf + (int64_t)l * nc * m + cb : Pst + (size_t)s_w * nc * m + cb;
         double2* Zs = Zst + (size_t)s_w * m * kUpdRows;
         const double2* Zl = Zs + rg;
         double2 acc[R][C];

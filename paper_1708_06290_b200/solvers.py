@@ -197,7 +197,8 @@ def solve_shifted_transposed(chf: ControllerHessForm, shifts, rhs, nb: int = 32,
     forward substitution fused into the sweep (csrc/ss_lq.cu).  Every pivot
     of the LQ factor is checked against ``rtol * ||Ahat - sigma I||_F``; a
     failing shift gets a NaN column and its first failing row in
-    ``failures``.  Requires m + 1 <= 32; ``nb`` is clamped to 32."""
+    ``failures``.  ``nb`` is clamped to 32 (and, for m + 1 > 32, to what the
+    shared-memory window of csrc/ss_lq.cu:k_lq_big holds); m + 1 <= 256."""
     del pool
     _check_chf(chf)
     shifts = _shifts_in(shifts)
@@ -256,19 +257,13 @@ def structured_pseudospectrum_grid(chf: ControllerHessForm, grid, nb: int = 32,
     rtol = default_singular_rtol(n) if singular_rtol is None else float(singular_rtol)
     host = all(D.is_host(a) for a in (chf.Ahat, chf.Bhat, chf.Chat, grid))
     dev = D.device_of(chf.Ahat, chf.Bhat, chf.Chat, grid)
-    if s == 0 or p == 0 or min(p, m) > 32:
-        # degenerate sizes or blocks beyond the epilogue: G on the device, norms by torch
+    if s == 0 or p == 0:
+        # empty values: ||.||_2 = 0 (two_norm_small), +inf where the shift is singular
         res = eval_transfer_function(chf, grid, nb=nb, batch_size=batch_size, counter=counter,
                                      on_singular="mark", singular_rtol=singular_rtol)
-        G = res.G if isinstance(res.G, torch.Tensor) else torch.from_numpy(
-            np.asfortranarray(res.G)).to(dev)
-        if s == 0 or p == 0:
-            out = torch.zeros(s, dtype=torch.float64, device=G.device)
-        else:
-            out = torch.linalg.matrix_norm(G.reshape(p, s, m).permute(1, 0, 2), ord=2)
-            if res.failures:
-                out = out.clone()
-                out[torch.tensor(sorted(res.failures), device=G.device)] = float("inf")
+        out = torch.zeros(s, dtype=torch.float64, device=dev)
+        if res.failures:
+            out[torch.tensor(sorted(res.failures), device=dev)] = float("inf")
         return out.cpu().numpy() if host else out
     with torch.cuda.device(dev):
         A = D.fmat(chf.Ahat, torch.float64, dev)

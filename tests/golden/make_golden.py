@@ -29,6 +29,7 @@ Cases (each cites the reference test it mirrors):
                      right-hand sides), the scalar known answer, a failure
                      case, and mirrored_schedule plans (test_solvers.py:139-189,
                      test_schedule.py:106-120)
+  transposed_wide.npz  the same for m + 1 > 32 (m = 33..100) and one IRKA run at m = 40
 """
 
 from __future__ import annotations
@@ -236,6 +237,39 @@ def transposed():
         d[f"ms_{nr}_{nc}_job"] = np.asarray(sch.job_size, dtype=np.int64)
         d[f"ms_{nr}_{nc}_info"] = np.asarray(sch.rot_info, dtype=np.int64)
     np.savez_compressed(os.path.join(OUT, "transposed.npz"), **d)
+
+
+def transposed_wide():
+    """Windows wider than one warp (m + 1 > 32): the shared-memory LQ path,
+    and IRKA on such a system (solve_shifted_transposed every iteration)."""
+    from shiftsolve.irka import default_initial_data, irka_iterate
+    rng = np.random.default_rng(23)
+    d = {}
+    specs = [(90, 33, 2, 60, 8), (120, 40, 3, 61, 16), (160, 50, 5, 62, 32), (200, 63, 4, 63, 32),
+             (260, 100, 3, 64, 16)]
+    for idx, (n, m, p, seed, nb) in enumerate(specs):
+        sysb = random_stable_system(n, m, p, seed=seed)
+        chf = reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+        shifts = bounded_shifts(rng, chf.Ahat, 4)
+        rhs = rng.standard_normal((n, 4)) + 1j * rng.standard_normal((n, 4))
+        res = solve_shifted_transposed(chf, shifts, rhs, nb=nb)
+        xlu = np.stack([lu_solve_shifted(chf.Ahat, s_, rhs[:, l], transpose=True)
+                        for l, s_ in enumerate(shifts)], axis=1)
+        pre = f"t{idx}_"
+        d[pre + "dims"] = np.asarray([n, m, p, seed, nb])
+        d[pre + "Ahat"], d[pre + "Bhat"], d[pre + "Chat"] = chf.Ahat, chf.Bhat, chf.Chat
+        d[pre + "shifts"], d[pre + "rhs"], d[pre + "x"], d[pre + "xlu"] = shifts, rhs, res.x, xlu
+    d["count"] = np.asarray(len(specs))
+    n, m, p, seed, r, iters = 120, 40, 3, 66, 6, 4
+    sysb = random_stable_system(n, m, p, seed=seed)
+    chf = reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=8)
+    s0, b0, c0 = default_initial_data(chf, r)
+    model, state = irka_iterate(chf, r, s0, b0, c0, maxiter=iters, fixed_iters=True, nb=8)
+    d["irka_dims"] = np.asarray([n, m, p, seed, r, iters])
+    d["irka_Ahat"], d["irka_Bhat"], d["irka_Chat"] = chf.Ahat, chf.Bhat, chf.Chat
+    d["irka_hist"] = np.stack([rec.shifts for rec in state.history])
+    d["irka_Ar"], d["irka_Br"], d["irka_Cr"] = model.Ar, model.Br, model.Cr
+    np.savez_compressed(os.path.join(OUT, "transposed_wide.npz"), **d)
 
 
 def cli():

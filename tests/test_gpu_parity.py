@@ -586,10 +586,12 @@ def test_m1_throughput_rq_vs_warp_rq(n, nb, monkeypatch):
         assert rel(r1.G[:, l:l + 1], Go[:, k:k + 1]) <= 1e-10
 
 
-@pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4), (300, 63, 5)])
+@pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4), (300, 63, 5),
+                                   (420, 100, 90), (380, 70, 3)])
 def test_wide_m_paths_vs_oracle(n, m, p):
     """Block widths outside the two-level set: m + 1 > 32 takes the scheduled
-    Givens block RQ (config 5: m = 50), m = 16 / 20 the one-level update with
+    Givens block RQ (config 5: m = 50; m = 100: head matrices in global
+    scratch), m = 16 / 20 the one-level update with
     several column blocks per shift (config 4: m = 20).  Transfer function and
     reduced solve vs the C oracle, conjugate pairs of complex shifts as in
     config 4 / 5."""
@@ -614,11 +616,13 @@ def test_wide_m_paths_vs_oracle(n, m, p):
         assert cert <= 1e3 * n * EPS
 
 
-@pytest.mark.parametrize("n,m,p", [(120, 7, 3), (90, 2, 6), (300, 10, 10), (64, 4, 1)])
+@pytest.mark.parametrize("n,m,p", [(120, 7, 3), (90, 2, 6), (300, 10, 10), (64, 4, 1),
+                                   (200, 33, 40), (260, 50, 50), (400, 100, 110)])
 def test_pseudospectrum_epilogue_vs_svd(n, m, p):
-    """The device ||G||_2 epilogue (Gram matrix + Hermitian Jacobi) against
-    numpy's SVD of the same G blocks (solvers.py:501-505), wide and tall
-    blocks; singular points -> +inf."""
+    """The device ||G||_2 epilogue (Gram matrix + parallel Hermitian Jacobi)
+    against numpy's SVD of the same G blocks (solvers.py:501-505), wide and
+    tall blocks, odd k, k = 50 (config 5's block) and k = 100 (Gram matrix in
+    global scratch); singular points -> +inf."""
     chf = _mhess_triple(n, m, p, seed=n + m + p)
     rng = np.random.default_rng(n)
     grid = (rng.uniform(-1, 1, 40) + 1j * rng.uniform(-1, 1, 40)) * np.sqrt(n)
