@@ -215,14 +215,17 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                     const int kc = ch - nz, kcols = min(KC, K - kc * KC);
                     const double* pan = reinterpret_cast<const double*>(st) + rg * 2;
                     const double2* ws = reinterpret_cast<const double2*>(st + PANB) + (size_t)sw * KC * M + cb;
-                    if (kc == 0 && !interior) {
-                        // acc -= sigma W12[dd, :] (mnb <= m <= KC: the rows are in this chunk)
+                    if (!interior && kc * KC < u.mnb) {
+                        // acc -= sigma W12[dd, :] for the lazy rows whose W12 row is
+                        // in this chunk (m > KC: they span two chunks)
+                        const int dhi = min(u.mnb, kc * KC + kcols);
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
                             const int dd = i0 + rg + RG * r - dlo;
-                            if (dd >= 0 && dd < u.mnb) {
+                            if (dd >= kc * KC && dd < dhi) {
 #pragma unroll
-                                for (int c = 0; c < C; ++c) acc[r][c] = csub(acc[r][c], cmul(sig, ws[dd * M + c]));
+                                for (int c = 0; c < C; ++c)
+                                    acc[r][c] = csub(acc[r][c], cmul(sig, ws[(dd - kc * KC) * M + c]));
                             }
                         }
                     }

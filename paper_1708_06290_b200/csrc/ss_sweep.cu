@@ -676,6 +676,7 @@ struct PartBufs {
     double2* Z;  // window state, updated in place
     double2* P;
     double* pan = nullptr;  // packed panel of the K-streamed far kernel (k_fark)
+    double2* W = nullptr;   // window composites: per shift (kWcWin nb0 + m) x m
     // deferred reduced solve: per shift W12 history (n x m, row = panel column,
     // j-major) and the composites' W22 (ncomp x m x m), plus the head's y (m)
     double2* Xh = nullptr;
@@ -698,18 +699,108 @@ static size_t fark_pan_bytes(int n, int ptop) {
     const size_t ntiles = (size_t)(ptop + n) / kFkTile + 2;
     return ntiles * ((4 * kBlkNB + kFkKC - 1) / kFkKC) * kFkKC * kFkTile * 8;  // K <= 4 outer blocks
 }
-template <int NCB, int S>
+template <int NCB, int S, int NST = kFarkStages>
 int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
     static ss::DevMask configured;  // devices configured
     if (!configured.has(h)) {
-        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_fark<NCB, S, kFarkStages>,
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_fark<NCB, S, NST>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)fark_smem_bytes<NCB, S, kFarkStages>()));
+                                            (int)fark_smem_bytes<NCB, S, NST>()));
         configured.set(h);
     }
-    k_fark<NCB, S, kFarkStages><<<grid, 32 * (1 + NCB * S), fark_smem_bytes<NCB, S, kFarkStages>(), st>>>(fk, Z, W);
+    k_fark<NCB, S, NST><<<grid, 32 * (1 + NCB * S), fark_smem_bytes<NCB, S, NST>(), st>>>(fk, Z, W);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Window composites for wide windows (m = 40, 50, 60 on the shared-memory
+// RQ, k_rq_big): the windows of a composite (up to kWcWin windows of nb0
+// columns, bottom-up) are factored one by one; each window's P updates only
+// the composite's own rows above it ("near", the generic k_update) and is
+// folded into the composite W = [W12 (K x m); W22 (m x m)]:
+//     W12[window rows] <- P12,  W12[rows below] <- W12 P22,  W22 <- W22 P22
+// (k_wcomp); the rows above the composite then get ONE K-streamed update
+// (k_fark, one pass over the K columns).  The far rows' state x W22 share of
+// the work drops from 2m / nb0 (104% at m = 50, nb0 = 96) to 2m / K.
+// Same algebra as the two-level sweep's composites (ss_block.cuh).
+// ---------------------------------------------------------------------------
+constexpr int kWcWin = 4;
+struct WcShape {
+    int S, NST;
+};
+static bool wc_shape(int m, WcShape& w) {
+    if (m == 40 || m == 50) { w = {2, 3}; return true; }
+    if (m == 60) { w = {1, 4}; return true; }
+    return false;
+}
+static size_t wc_far_smem(int m) {
+    switch (m) {
+        case 40: return fark_smem_bytes<4, 2, 3>();
+        case 50: return fark_smem_bytes<5, 2, 3>();
+        case 60: return fark_smem_bytes<6, 1, 4>();
+        default: return ~(size_t)0;
+    }
+}
+static int wc_jz(int m) {
+    switch (m) {
+        case 40: return fark_jz<4, 2>();
+        case 50: return fark_jz<5, 2>();
+        default: return fark_jz<6, 1>();
+    }
+}
+static int launch_wc_far(ss_handle* h, int m, int grid, cudaStream_t st, const FarKDims& fk, double2* Z,
+                         const double2* W) {
+    switch (m) {
+        case 40: return launch_fark<4, 2, 3>(h, grid, st, fk, Z, W);
+        case 50: return launch_fark<5, 2, 3>(h, grid, st, fk, Z, W);
+        case 60: return launch_fark<6, 1, 4>(h, grid, st, fk, Z, W);
+        default: return ss::set_err(h, SS_EARG, "window composite: unsupported m");
+    }
+}
+
+constexpr int kWcRows = 32;  // W rows per k_wcomp CTA
+__host__ __device__ inline size_t wcomp_smem(int m) { return (size_t)(m * m + kWcRows * m) * 16; }
+
+// Fold window P (rows [0, nb) P12, [nb, nb + m) P22; P_l at P + l pstride)
+// into the composite W of shift l (W + l wstride, j-major rows of m):
+// rows [x, x + nb) <- P12; rows [x + nb, K + m) <- rows P22 (first window of
+// the composite, x + nb == K: W22 <- P22).  grid (sb, row chunks).
+__global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool first, int64_t pstride,
+                                               const double2* __restrict__ P, int64_t wstride,
+                                               double2* __restrict__ W) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* P22 = reinterpret_cast<double2*>(smem);  // m x m
+    double2* Wr = P22 + m * m;                        // [kWcRows][m]
+    const int l = blockIdx.x, tid = threadIdx.x;
+    const double2* Pl = P + (int64_t)l * pstride;
+    double2* Wl = W + (int64_t)l * wstride;
+    const int r0 = x + nb, nrows = K + m - r0;  // rows multiplied by P22
+    const int c0 = blockIdx.y * kWcRows;
+    if (blockIdx.y == 0)
+        for (int e = tid; e < nb * m; e += blockDim.x) Wl[(int64_t)x * m + e] = Pl[e];
+    if (first) {
+        if (blockIdx.y == 0)
+            for (int e = tid; e < m * m; e += blockDim.x) Wl[(int64_t)K * m + e] = Pl[(int64_t)nb * m + e];
+        return;
+    }
+    if (c0 >= nrows) return;
+    const int rc = min(kWcRows, nrows - c0);
+    for (int e = tid; e < m * m; e += blockDim.x) P22[e] = Pl[(int64_t)nb * m + e];
+    for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)(r0 + c0) * m + e];
+    __syncthreads();
+    for (int e = tid; e < rc * m; e += blockDim.x) {
+        const int r = e / m, c = e - r * m;
+        const double2* wr = Wr + r * m;
+        double2 a0 = cz(), a1 = cz();
+        int j = 0;
+        for (; j + 1 < m; j += 2) {
+            a0 = cfma(wr[j], P22[j * m + c], a0);
+            a1 = cfma(wr[j + 1], P22[(j + 1) * m + c], a1);
+        }
+        if (j < m) a0 = cfma(wr[j], P22[j * m + c], a0);
+        Wl[(int64_t)(r0 + c0) * m + e] = cadd(a0, a1);
+    }
 }
 
 // Enqueue the whole sweep (seed, window steps, head) for shifts
@@ -781,7 +872,7 @@ void account_ref_flops(ss_handle* h, int sb, int n, int m, int ptop, int nb0) {
 
 int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs B, int nb0,
                  int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, bool two_level,
-                 cudaStream_t st, Feed& feed) {
+                 bool wc, cudaStream_t st, Feed& feed) {
     const int n = a.n, m = a.m;
     const int ptop = a.mode == 0 ? a.p : (a.defer ? 0 : n);
     const int mode_far = a.defer ? 0 : a.mode;  // deferred reduced solve: far rows as tf with p = 0
@@ -1018,6 +1109,146 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 NBb = kBlkNB;
             }
             ko = kb;
+        }
+    }
+    if (wc) {
+        // ---- window composites (wide windows: k_rq_big + near k_update +
+        // k_wcomp per window, one k_fark per composite) ----
+        account_ref_flops(h, sb, n, m, ptop, nb0);  // the reference's stack
+        WcShape wsh;
+        wc_shape(m, wsh);
+        const int64_t wstride = (int64_t)(kWcWin * nb0 + m) * m;
+        static ss::DevMask configured;  // devices configured
+        if (!configured.has(h)) {
+            SS_CUDA_TRY(h, allow_max_smem(h, k_rq_big));
+            SS_CUDA_TRY(h, cudaFuncSetAttribute(k_wcomp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)wcomp_smem(m)));
+            configured.set(h);
+        }
+        while (k >= m + 1) {
+            int kw[kWcWin], nbw[kWcWin], g = 0;
+            for (int kk = k; kk >= m + 1 && g < kWcWin; ++g) {
+                kw[g] = kk;
+                nbw[g] = std::min(nb0, kk - m);
+                kk -= nbw[g];
+            }
+            const int ktop = kw[g - 1], nbtop = nbw[g - 1];
+            const int c0 = ktop - m - nbtop;          // first panel column of the composite
+            const int K = (k - m) - c0;               // its columns
+            const int r0G = ptop + ktop - nbtop;      // first row of its top window
+            for (int b = 0; b < g; ++b) {
+                const int nb = nbw[b], r0 = ptop + kw[b] - nb, cw = kw[b] - m - nb, nc = nb + m;
+                int rc = feed_wait(h, feed, st);  // this window's panel columns
+                if (rc) return rc;
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                RqDims rd;
+                rd.m = m;
+                rd.ptop = ptop;
+                rd.nb = nb;
+                rd.k = kw[b];
+                rd.c0 = cw;
+                rd.r0 = r0;
+                rd.nc = nc;
+                rd.sb = sb;
+                rd.A = a.A;
+                rd.lda = a.lda;
+                rd.shifts = d.shifts;
+                rd.LDZ = LDZ;
+                k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(nb, m), st>>>(rd, B.Z, B.P);
+                SS_LAUNCH_CHECK(h);
+                ss::timing_end(h, st, ev, ss::PH_RQ);
+                if (r0 > r0G) {
+                    // near: the composite's rows above this window (generic update)
+                    UpdDims u;
+                    u.n = n;
+                    u.m = m;
+                    u.ptop = ptop;
+                    u.ident_top = 0;
+                    u.A = a.A;
+                    u.lda = a.lda;
+                    u.T = a.C;
+                    u.ldt = a.ldc;
+                    u.shifts = d.shifts;
+                    u.sb = sb;
+                    u.LDZ = LDZ;
+                    u.nb = nb;
+                    u.mnb = std::min(m, nb);
+                    u.r0 = r0;
+                    u.c0 = cw;
+                    u.nc = nc;
+                    u.rlo = r0G;
+                    u.pstride = (int64_t)nc * m;
+                    u.p12off = 0;
+                    u.p22off = (int64_t)nb * m;
+                    u.zid = 0;
+                    u.flags = 0;
+                    u.nws = nws;
+                    u.ksplit = (tile.exact && 64 * nws <= 320) ? 2 : 1;
+                    u.jh = std::max(0, std::min(nb, (nb - 2 * m) / 2));
+                    u.S = std::max(1, 8 / (nws * u.ksplit));
+                    const size_t two_per_sm = h->smem_optin / 2 - 1024;
+                    while (u.S > 1 && upd_smem_bytes(nb, m, u.S) > two_per_sm) u.S--;
+                    u.SG = u.S * 4;
+                    const int rows = r0 - r0G;
+                    dim3 gu((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
+                    ev = ss::timing_begin(h, st);
+                    rc = launch_update(h, tile, gu, 32 * u.S * nws * u.ksplit, upd_smem_bytes(nb, m, u.S), st, u,
+                                       B.Z, B.Z, B.P);
+                    if (rc) return rc;
+                    ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
+                                   8.0 * rows * (double)sb * m * nb, 4.0 * m * (double)rows * nb * sb);
+                }
+                ev = ss::timing_begin(h, st);
+                const int nrows = K + m - (cw - c0 + nb);
+                dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
+                k_wcomp<<<gc, 256, wcomp_smem(m), st>>>(m, K, cw - c0, nb, b == 0, (int64_t)nc * m, B.P,
+                                                        wstride, B.W);
+                SS_LAUNCH_CHECK(h);
+                ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
+            }
+            // far rows [0, r0G): one K-streamed pass over the composite
+            const int rows = r0G;
+            if (rows > 0) {
+                FarKDims fk;
+                fk.m = m;
+                fk.ptop = ptop;
+                fk.ident_top = 0;
+                fk.A = a.A;
+                fk.lda = a.lda;
+                fk.T = a.C;
+                fk.ldt = a.ldc;
+                fk.shifts = d.shifts;
+                fk.sb = sb;
+                fk.LDZ = LDZ;
+                fk.r0 = r0G;
+                fk.rlo = 0;
+                fk.c0 = c0;
+                fk.K = K;
+                fk.mnb = std::min(m, K);
+                fk.wstride = wstride;
+                fk.woff = 0;
+                fk.nk = (K + kFkKC - 1) / kFkKC;
+                fk.jz = wc_jz(m);
+                fk.nz = (m + fk.jz - 1) / fk.jz;
+                fk.ntiles = (rows + kFkTile - 1) / kFkTile;
+                fk.pan = B.pan;
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                SS_LAUNCH_CHECK(h);
+                ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
+                const int64_t units = (int64_t)fk.ntiles * ((sb + wsh.S - 1) / wsh.S);
+                fk.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
+                const int grid = (int)std::max<int64_t>(
+                    fk.spl, std::min<int64_t>(units, h->num_sms) / fk.spl * fk.spl);
+                double nnz = (double)std::min(rows, ptop) * K;  // Chat rows dense
+                if (rows > ptop) nnz += (double)(rows - ptop) * K;
+                ev = ss::timing_begin(h, st);
+                int rc = launch_wc_far(h, m, grid, st, fk, B.Z, B.W);
+                if (rc) return rc;
+                ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
+                               8.0 * rows * (double)sb * m * K, 4.0 * m * nnz * sb);
+            }
+            k = ktop - nbtop;
         }
     }
     while (k >= m + 1) {
@@ -1523,6 +1754,12 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
                            far_smem_bytes(64, m, 64, m == 20 ? 4 : 8) + 1024 <= h->smem_optin;
     // reduced solve on the two-level sweep: identity top deferred (k_expand);
     // SS_NO_DEFER=1 sweeps the identity rows as the reference does
+    // wide windows (m = 40 / 50 / 60, transfer function): window composites
+    // with one K-streamed far pass per kWcWin windows (SS_ONE_LEVEL=1: per window)
+    WcShape wsh;
+    const bool wc = !two_level && a.mode == 0 && rq_big(m) && wc_shape(m, wsh) && !getenv("SS_ONE_LEVEL") &&
+                    wc_far_smem(m) <= h->smem_optin && wcomp_smem(m) <= h->smem_optin &&
+                    kWcWin * nb0 <= 4 * kBlkNB;
     a.defer = a.mode == 1 && two_level && !getenv("SS_NO_DEFER");
     const int mode_far = a.defer ? 0 : a.mode;
     a.group = two_level ? two_level_group(h, m, mode_far) : 1;
@@ -1571,7 +1808,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
 
     // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
-    const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)ncmax * m;
+    const int64_t wc_stride = wc ? (int64_t)(kWcWin * nb0 + m) * m : 0;  // composite W per shift
+    const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)ncmax * m + wc_stride;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64 +
                              (size_t)(xh_stride + w22h_stride + y_stride) * 16;
     int64_t sb_max = std::min<int64_t>(a.batch > 0 ? a.batch : a.s, a.s);
@@ -1596,7 +1834,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     double2* W22h0 = Xh0 + (size_t)sb_max * xh_stride;
     double2* Y0 = W22h0 + (size_t)sb_max * w22h_stride;
     double* pan = nullptr;  // k_fark's packed panel, after the 1 MB scratch of fro2_trace
-    if (two_level && fark_supported(h, m, mode_far)) {
+    if ((two_level && fark_supported(h, m, mode_far)) || wc) {
         int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(n, ptop), 1);
         if (rc) return rc;
         pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
@@ -1610,7 +1848,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     const bool far_m20 = !two_level && tile.exact && tile.G == 2 && tile.C == 5 &&
                          (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2;
     const bool far_m1 = !two_level && m == 1;
-    int NS = (two_level || far_m20 || far_m1) ? 1 : 2;
+    int NS = (two_level || wc || far_m20 || far_m1) ? 1 : 2;
     if (sb_max < 64 || feed.on) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
@@ -1629,6 +1867,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
             B.Z = Z0 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * pst;
             B.pan = pan;
+            if (wc) B.W = B.P + (size_t)cnt * ncmax * m;  // after the parts' window P
             if (a.defer) {
                 B.Xh = Xh0 + (size_t)off * xh_stride;
                 B.W22h = W22h0 + (size_t)off * w22h_stride;
@@ -1637,7 +1876,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
                 B.w22h_stride = w22h_stride;
             }
             int rc = enqueue_part(h, a, lo + off, cnt, B, nb0, LDZ, rtol, use_house, tile,
-                                  two_level, streams[p], feed);
+                                  two_level, wc, streams[p], feed);
             if (rc) return rc;
             off += cnt;
         }
