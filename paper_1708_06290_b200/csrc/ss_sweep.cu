@@ -715,7 +715,7 @@ int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, dou
 
 // ---------------------------------------------------------------------------
 // Window composites for wide windows (m = 40, 50, 60 on the shared-memory
-// RQ, k_rq_big): the windows of a composite (up to kWcWin windows of nb0
+// RQ, k_rq_big): the windows of a composite (up to kWcWin windows of kWcNb
 // columns, bottom-up) are factored one by one; each window's P updates only
 // the composite's own rows above it ("near", the generic k_update) and is
 // folded into the composite W = [W12 (K x m); W22 (m x m)]:
@@ -725,7 +725,12 @@ int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, dou
 // the work drops from 2m / nb0 (104% at m = 50, nb0 = 96) to 2m / K.
 // Same algebra as the two-level sweep's composites (ss_block.cuh).
 // ---------------------------------------------------------------------------
-constexpr int kWcWin = 4;
+// measured at config 5 (m = 50): (nb0, windows) = (96, 4) 315, (96, 6) 325,
+// (64, 6) 336, (64, 8) 341, (48, 8) 326, (32, 12) 326 shifts/s -- narrower
+// windows cut k_rq_big's chain (n nb / 2 row updates per shift), more
+// windows per composite cut the far rows' 2m / K share, both add near updates
+constexpr int kWcWin = 8;
+constexpr int kWcNb = 64;
 struct WcShape {
     int S, NST;
 };
@@ -1742,7 +1747,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     while (nb_big > 8 && (upd_smem_bytes(nb_big, m, 1) + 1024 > h->smem_optin ||
                           rq_big_smem_bytes(nb_big, m) + 1024 > h->smem_optin))
         nb_big -= 8;
-    const int nb0 = use_house ? std::min(nb0_req, 64) : (rq_big(m) ? nb_big : nb0_req);
+    int nb0 = use_house ? std::min(nb0_req, 64) : (rq_big(m) ? nb_big : nb0_req);
 
     // two-level sweep (ss_block.cuh) when the fused block kernel and the
     // warp-specialised far update cover m; SS_ONE_LEVEL=1 forces the
@@ -1759,7 +1764,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     WcShape wsh;
     const bool wc = !two_level && a.mode == 0 && rq_big(m) && wc_shape(m, wsh) && !getenv("SS_ONE_LEVEL") &&
                     wc_far_smem(m) <= h->smem_optin && wcomp_smem(m) <= h->smem_optin &&
-                    kWcWin * nb0 <= 4 * kBlkNB;
+                    kWcWin * kWcNb <= 4 * kBlkNB;
+    if (wc) nb0 = std::min(nb0, kWcNb);
     a.defer = a.mode == 1 && two_level && !getenv("SS_NO_DEFER");
     const int mode_far = a.defer ? 0 : a.mode;
     a.group = two_level ? two_level_group(h, m, mode_far) : 1;
