@@ -144,6 +144,16 @@ int ss_update_kernel_stats(ss_handle* h, int64_t* launches, double* seconds, dou
  * DFMA-chain kernel over all SMs -- the denominator of the FP64 roofline. */
 int ss_probe_dfma_peak(ss_handle* h, double* tflops);
 
+/* Diagnostics: measured FP64 tensor-core (DMMA m16n8k8) peak in TFLOP/s. */
+int ss_probe_dmma_peak(ss_handle* h, double* tflops);
+
+/* Diagnostics / tests: the reduction's FP64 tensor-core GEMM (ss_gemm.cuh),
+ * C = alpha op(A) op(B) + beta C, column-major device pointers, op(X) = X^T
+ * when ta / tb is nonzero.  Deterministic (split-K partials summed in order). */
+int ss_dgemm(ss_handle* h, int ta, int tb, int M, int N, int K, double alpha, const double* A,
+             int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+             void* stream);
+
 /* Number of device kernels this handle has launched since creation. */
 int64_t ss_launch_count(const ss_handle* h);
 

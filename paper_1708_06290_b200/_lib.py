@@ -20,7 +20,7 @@ SS_OK, SS_EDIM, SS_EARG, SS_ECUDA, SS_ENOMEM = 0, 1, 2, 3, 4
 EXPORTED = (
     "ss_version", "ss_create", "ss_destroy", "ss_last_error", "ss_greedy_schedule",
     "ss_tf_eval", "ss_tf_eval_stream", "ss_pspec_eval", "ss_solve_reduced", "ss_solve_transposed", "ss_reduce_chf", "ss_set_timing", "ss_phase_stats",
-    "ss_reset_stats", "ss_launch_count", "ss_update_kernel_stats", "ss_probe_dfma_peak",
+    "ss_reset_stats", "ss_launch_count", "ss_update_kernel_stats", "ss_probe_dfma_peak", "ss_probe_dmma_peak", "ss_dgemm",
 )
 
 _lib = None
@@ -78,6 +78,10 @@ def load():
         L.ss_update_kernel_stats.restype = I
         L.ss_probe_dfma_peak.argtypes = [P, P]
         L.ss_probe_dfma_peak.restype = I
+        L.ss_probe_dmma_peak.argtypes = [P, P]
+        L.ss_probe_dmma_peak.restype = I
+        L.ss_dgemm.argtypes = [P, I, I, I, I, I, D, P, I64, P, I64, D, P, I64, P]
+        L.ss_dgemm.restype = I
         _lib = L
     return _lib
 

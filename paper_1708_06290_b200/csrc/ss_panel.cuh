@@ -1,0 +1,270 @@
+// Panel columns of the blocked controller-Hessenberg reduction as ONE
+// persistent cooperative kernel per mini-block (reference hessenberg.py:99-146
+// _process_panel, mini_boundaries :83-96; kernels.py:74-99
+// householder_vector, :156-160 the T column).
+//
+// The per-column vector work of the reference (right update from the
+// panel's completed mini-blocks, left update with the panel's earlier
+// reflectors, the Householder vector, the T column) is a chain of small
+// dependent reductions over the panel's nk trailing rows.  As separate
+// launches it cost six kernels per column (80-210 us per column measured on
+// B200: 81% of the reduction at n = 1500, 420 ms of config 3's 2000
+// columns).  Here the trailing rows are split into contiguous slices, one per
+// CTA (one CTA per SM, co-resident by cooperative launch), and a column
+// costs two grid-wide barriers:
+//
+//   S2(j)  w = T^T (V^T a) from every CTA's partials (summed in CTA order by
+//          every CTA: identical values everywhere), a -= V w on the own rows,
+//          partial sum of squares below row j;
+//   --- grid sync ---
+//   S3(j)  Householder scalars (every CTA, same order), v_j = a / (alpha -
+//          beta) below row j, V[:, j] = v_j, a finalised; partials of V^T v_j
+//          (T column) and -- the next column's S1 fused in -- the right update
+//          of column j+1 from the completed mini-blocks (a -= Y V[vrow]^T) and
+//          the partials of V^T a_{j+1};
+//   --- grid sync ---
+//   T[:, j] = -tau T (V^T v_j), T[j, j] = tau: every CTA, in shared memory.
+//
+// The kernel covers the columns of one mini-block [js, jb); the Y extension
+// between mini-blocks is a DMMA GEMM over the trailing matrix (ss_reduce.cu).
+// All reductions run in a fixed order (per-warp lane-strided sums, warp
+// shuffles, CTA partials summed in CTA order): run-to-run reproducible.
+#pragma once
+
+#include <cooperative_groups.h>
+
+namespace ssr {
+
+namespace cg = cooperative_groups;
+
+constexpr int kPT = 256;     // threads per CTA
+constexpr int kPBmax = 128;  // widest panel (block_size is capped at 128)
+
+struct Pan {
+    double* a0;    // panel column j: a0 + j * lda, rows [0, nk)
+    int64_t lda;
+    int nk, bw, m;
+    int yext;      // band panel (1): right updates from Y; B's QR (0)
+    int vrow0;     // V row of column j's right update: j + vrow0 (= j - m)
+    double* V;     // nk x bw, ld ldv (zero above the diagonal)
+    const double* Y;  // nk x bw, ld ldv
+    int64_t ldv;
+    double* T;     // bw x bw, ld ldt: columns < js in, [js, jb) out
+    int64_t ldt;
+    double* ws;    // scratch: pan_ws_doubles(G)
+};
+
+__host__ __device__ inline size_t pan_ws_doubles(int G) { return (size_t)G * kPBmax * 2 + (size_t)G + 8; }
+__host__ __device__ inline size_t pan_smem_bytes(int bw, int nown_staged) {
+    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (size_t)2 * nown_staged * bw) * 8;
+}
+
+// The CTA's own rows of V and Y, staged in shared memory when they fit
+// (rows [rlo, rhi): element (i, t) at base[(i - off) + t * ld]; global
+// otherwise: off = 0, ld = ldv)
+struct Own {
+    const double* v;
+    const double* y;
+    int off;
+    int64_t ld;
+};
+
+// out[t * ostride] = sum over own rows i of V[i, t] x[i], t < nt (warp per t,
+// lanes over rows); partials are stored t-major (the G CTAs' values of one t
+// contiguous) so the cross-CTA sums below read them coalesced
+__device__ __forceinline__ void own_vdots(const Own& o, int rlo, int rhi, const double* x, int nt, double* out,
+                                          int ostride) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < nt; t += kPT / 32) {
+        const double* vc = o.v + (int64_t)t * o.ld - o.off;
+        double s = 0.0;
+        for (int i = rlo + lane; i < rhi; i += 32) s = fma(vc[i], x[i], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) out[(size_t)t * ostride] = s;
+    }
+}
+
+// d[t] = sum over CTAs c of part[t * G + c], t < nt: a warp per t, lanes
+// over c in a fixed order, then a fixed shuffle tree (deterministic)
+__device__ __forceinline__ void cta_sums(const double* part, int G, int nt, double* d) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < nt; t += kPT / 32) {
+        const double* pt = part + (size_t)t * G;
+        double s = 0.0;
+        for (int c = lane; c < G; c += 32) s += pt[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) d[t] = s;
+    }
+}
+
+// S1(j): right update of column j from the completed mini-blocks (Y columns
+// t < jr), own rows; then the partials of V^T a_j (t < j)
+__device__ __forceinline__ void s1_right(const Pan& p, const Own& o, double* vrs, int j, int js, int rlo, int rhi,
+                                         double* ppart_c, int G) {
+    double* a = p.a0 + (int64_t)j * p.lda;
+    const int jr = p.yext ? min(js, max(j - p.m + 1, 0)) : 0;
+    if (jr > 0) {
+        // V row j - m (another CTA's row) into shared memory once
+        const double* vr = p.V + (j + p.vrow0);
+        for (int t = threadIdx.x; t < jr; t += kPT) vrs[t] = vr[(int64_t)t * p.ldv];
+        __syncthreads();
+        for (int i = rlo + (int)threadIdx.x; i < rhi; i += kPT) {
+            const double* yr = o.y + (i - o.off);
+            double v0 = a[i], v1 = 0.0;
+            int t = 0;
+            for (; t + 1 < jr; t += 2) {
+                v0 = fma(-yr[(int64_t)t * o.ld], vrs[t], v0);
+                v1 = fma(-yr[(int64_t)(t + 1) * o.ld], vrs[t + 1], v1);
+            }
+            if (t < jr) v0 = fma(-yr[(int64_t)t * o.ld], vrs[t], v0);
+            a[i] = v0 + v1;
+        }
+        __syncthreads();
+    }
+    own_vdots(o, rlo, rhi, a, j, ppart_c, G);
+}
+
+__global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int stage) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int bw = p.bw, nk = p.nk;
+    double* Ts = sm;               // bw x bw, col-major (ld bw)
+    double* w = Ts + bw * bw;      // [kPBmax]
+    double* d = w + kPBmax;        // [kPBmax]
+    double* red = d + kPBmax;      // [kPT / 32]
+    double* sc = red + kPT / 32;   // [8] tau, beta, scale
+    double* vrs = sc + 8;          // [kPBmax] V row of the right update
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const int rlo = (int)((int64_t)nk * cta / G), rhi = (int)((int64_t)nk * (cta + 1) / G);
+    const int nown = rhi - rlo;
+    Own o{p.V, p.Y, 0, p.ldv};
+    double* Vs = nullptr;
+    if (stage) {
+        // own rows of V (columns < jb; column j written here as it is formed)
+        // and Y (columns < js, read-only in this kernel)
+        Vs = vrs + kPBmax;
+        double* Ys = Vs + (size_t)nown * bw;
+        for (int e = tid; e < nown * jb; e += kPT) {
+            const int r = e % nown, t = e / nown;
+            Vs[e] = t < js ? p.V[rlo + r + (int64_t)t * p.ldv] : 0.0;
+        }
+        if (p.yext)
+            for (int e = tid; e < nown * js; e += kPT) {
+                const int r = e % nown, t = e / nown;
+                Ys[e] = p.Y[rlo + r + (int64_t)t * p.ldv];
+            }
+        o = Own{Vs, Ys, rlo, nown};
+    }
+    double* ppart = p.ws;                        // [kPBmax][G]
+    double* qpart = ppart + (size_t)G * kPBmax;  // [kPBmax][G]
+    double* spart = qpart + (size_t)G * kPBmax;  // [G]
+    double* scal = spart + G;                    // [8]: alpha
+    // T columns of the earlier mini-blocks (upper triangle)
+    for (int e = tid; e < bw * bw; e += kPT) {
+        const int r = e % bw, c = e / bw;
+        Ts[e] = (c < js && r <= c) ? p.T[r + (int64_t)c * p.ldt] : 0.0;
+    }
+    __syncthreads();
+    s1_right(p, o, vrs, js, js, rlo, rhi, ppart + cta, G);
+    grid.sync();
+    for (int j = js; j < jb; ++j) {
+        double* a = p.a0 + (int64_t)j * p.lda;
+        // ---- S2: w = T^T (sum of partials); a -= V w; squares below row j ----
+        cta_sums(ppart, G, j, d);
+        __syncthreads();
+        for (int t = tid; t < j; t += kPT) {
+            double s = 0.0;
+            for (int k = 0; k <= t; ++k) s = fma(Ts[k + t * bw], d[k], s);  // (T^T d)_t
+            w[t] = s;
+        }
+        __syncthreads();
+        double sq = 0.0;
+        for (int i = rlo + tid; i < rhi; i += kPT) {
+            const double* vr = o.v + (i - o.off);
+            double v0 = a[i], v1 = 0.0;
+            int t = 0;
+            for (; t + 1 < j; t += 2) {
+                v0 = fma(-vr[(int64_t)t * o.ld], w[t], v0);
+                v1 = fma(-vr[(int64_t)(t + 1) * o.ld], w[t + 1], v1);
+            }
+            if (t < j) v0 = fma(-vr[(int64_t)t * o.ld], w[t], v0);
+            const double v = v0 + v1;
+            a[i] = v;
+            if (i > j) sq = fma(v, v, sq);
+            if (i == j) scal[0] = v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) red[tid >> 5] = sq;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int q = 0; q < kPT / 32; ++q) t += red[q];
+            spart[cta] = t;
+        }
+        grid.sync();
+        // ---- S3: Householder scalars (householder_vector, kernels.py:74-99) ----
+        if (tid < 32) {
+            double sg = 0.0;
+            for (int c = tid; c < G; c += 32) sg += spart[c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+            if (tid == 0) red[0] = sg;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const double sigma = red[0];
+            const double alpha = scal[0];
+            double tau, beta, scale;
+            if (sigma == 0.0) {
+                tau = 0.0;
+                beta = alpha;
+                scale = 0.0;
+            } else {
+                const double anorm = sqrt(alpha * alpha + sigma);
+                beta = alpha >= 0.0 ? -anorm : anorm;
+                tau = (beta - alpha) / beta;
+                scale = 1.0 / (alpha - beta);
+            }
+            sc[0] = tau;
+            sc[1] = beta;
+            sc[2] = scale;
+        }
+        __syncthreads();
+        const double tau = sc[0], beta = sc[1], scale = sc[2];
+        double* vj = p.V + (int64_t)j * p.ldv;
+        for (int i = rlo + tid; i < rhi; i += kPT) {
+            double v;
+            if (i < j) v = 0.0;
+            else if (i == j) v = 1.0;
+            else v = tau == 0.0 ? 0.0 : a[i] * scale;
+            vj[i] = v;
+            if (Vs) Vs[(i - rlo) + (size_t)j * nown] = v;
+            if (i == j) a[i] = beta;
+            else if (i > j) a[i] = 0.0;
+        }
+        __syncthreads();
+        own_vdots(o, rlo, rhi, vj, j, qpart + cta, G);
+        if (j + 1 < jb) s1_right(p, o, vrs, j + 1, js, rlo, rhi, ppart + cta, G);
+        grid.sync();
+        // ---- T column (kernels.py:156-160; every CTA, same order) ----
+        cta_sums(qpart, G, j, d);
+        __syncthreads();
+        for (int r = tid; r < j; r += kPT) {
+            double s = 0.0;
+            for (int k = r; k < j; ++k) s = fma(Ts[r + k * bw], d[k], s);
+            Ts[r + j * bw] = -tau * s;
+        }
+        if (tid == 0) Ts[j + j * bw] = tau;
+        __syncthreads();
+    }
+    if (cta == 0)
+        for (int e = tid; e < bw * (jb - js); e += kPT) {
+            const int r = e % bw, c = js + e / bw;
+            p.T[r + (int64_t)c * p.ldt] = r <= c ? Ts[r + c * bw] : 0.0;
+        }
+}
+
+}  // namespace ssr

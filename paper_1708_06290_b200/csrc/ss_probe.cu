@@ -1,5 +1,6 @@
-// Diagnostic: measured FP64 FMA peak of the device (the FP64 roofline
-// denominator; MEASURED_PEAKS.json only carries HBM and bf16 peaks).
+// Diagnostics: measured FP64 FMA (DFMA) and FP64 tensor-core (DMMA) peaks
+// of the device (the FP64 roofline denominators; MEASURED_PEAKS.json only
+// carries HBM and bf16 peaks).
 #include "ss_internal.h"
 
 namespace {
@@ -20,7 +21,58 @@ __global__ void __launch_bounds__(512) k_dfma_chain(int iters, double x, double 
     if (s == 12345.678) out[0] = s;  // never true; keeps the chains alive
 }
 
+// 8 independent m16n8k8 f64 accumulators per warp
+__global__ void __launch_bounds__(256) k_dmma_chain(int iters, double x, double* out) {
+    double c[8][4];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) c[q][v] = 0.0;
+    const double a[4] = {x, x * 0.5, x * 0.25, x * 0.125};
+    const double b[2] = {x * 0.75, x * 0.375};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            asm volatile(
+                "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 "
+                "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                : "+d"(c[q][0]), "+d"(c[q][1]), "+d"(c[q][2]), "+d"(c[q][3])
+                : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1] + c[q][2] + c[q][3];
+    if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace
+
+extern "C" int ss_probe_dmma_peak(ss_handle* h, double* tflops) {
+    if (!h || !tflops) return SS_EARG;
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
+    const int blocks = h->num_sms * 4, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    SS_CUDA_TRY(h, cudaEventCreate(&a));
+    SS_CUDA_TRY(h, cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a, 0);
+        k_dmma_chain<<<blocks, threads>>>(iters, 1e-3, h->d_scal + 32);
+        SS_LAUNCH_CHECK(h);
+        cudaEventRecord(b, 0);
+        SS_CUDA_TRY(h, cudaEventSynchronize(b));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    // per warp-instruction: 16 x 8 x 8 FMA = 2048 flops
+    const double flops = 2048.0 * 8.0 * iters * (double)blocks * (threads / 32);
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return SS_OK;
+}
 
 extern "C" int ss_probe_dfma_peak(ss_handle* h, double* tflops) {
     if (!h || !tflops) return SS_EARG;

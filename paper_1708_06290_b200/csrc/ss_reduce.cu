@@ -13,289 +13,28 @@
 //     the column receives the right update of the panel's earlier
 //     mini-blocks (Y V^T) and the left update (I - V T^T V^T), then its
 //     reflector is generated and the T factor grows (reference
-//     _process_panel, hessenberg.py:99-146).  Every m columns (a "mini-block",
-//     mini_boundaries hessenberg.py:83-96) Y = A V T is extended by one GEMM
-//     over the trailing matrix -- the band-width trick that reads the
-//     trailing matrix n/m times instead of n times.  After the panel the
-//     trailing updates (tasks (a), (b), (c) of hessenberg.py:149-193) and the
-//     C / Q right updates are GEMMs.
+//     _process_panel, hessenberg.py:99-146).  These run as one persistent
+//     cooperative kernel per mini-block (k_panel, ss_panel.cuh: two grid
+//     barriers per column instead of six launches).  Every m columns (a
+//     "mini-block", mini_boundaries hessenberg.py:83-96) Y = A V T is
+//     extended by one GEMM over the trailing matrix -- the band-width trick
+//     that reads the trailing matrix n/m times instead of n times.  After the
+//     panel the trailing updates (tasks (a), (b), (c) of
+//     hessenberg.py:149-193) and the C / Q right updates are GEMMs.
 //
-// All dense contractions go through k_dgemm, a hand-written FP64 tensor-core
-// GEMM (mma.sync m16n8k8 .f64, i.e. DMMA) -- the only place DMMA is used.
-// Per-column vector work runs in small multi-CTA kernels with deterministic
-// (fixed-order) partial reductions, so results are run-to-run reproducible.
+// All dense contractions go through k_dmma (ss_gemm.cuh), a hand-written
+// FP64 tensor-core GEMM (mma.sync m16n8k8 .f64, i.e. DMMA, cp.async ring,
+// deterministic split-K) -- the only place DMMA is used.  Every reduction
+// runs in a fixed order, so results are run-to-run reproducible.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 
 #include "ss_internal.h"
+#include "ss_gemm.cuh"
+#include "ss_panel.cuh"
 
 namespace {
-
-// ---------------------------------------------------------------------------
-// FP64 GEMM on DMMA:  C = alpha op(A) op(B) + beta C   (column-major)
-// CTA tile 64x64x16, 4 warps each 32x32 (2 x 4 m16n8k8 tiles).
-// ---------------------------------------------------------------------------
-constexpr int GBM = 64, GBN = 64, GBK = 16, GS = 68;  // GS = 4 mod 16: conflict-free frags
-
-__device__ __forceinline__ void dmma16n8k8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 "
-        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
-}
-
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(128)
-    k_dgemm(int M, int N, int K, double alpha, const double* __restrict__ A, int64_t lda,
-            const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C,
-            int64_t ldc) {
-    __shared__ double As[2][GBK * GS];
-    __shared__ double Bs[2][GBK * GS];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int g = lane >> 2, tq = lane & 3;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
-    const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;
-    double acc[2][4][4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
-
-    // 64x16 tile = 1024 values, 8 per thread
-    double ra[8], rb[8];
-    auto load = [&](int k0) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = tid + u * 128;
-            int mi, kk;
-            if (!TA) { mi = e & 63; kk = e >> 6; } else { kk = e & 15; mi = e >> 4; }
-            const int gm = m0 + mi, gk = k0 + kk;
-            double v = 0.0;
-            if (gm < M && gk < K) v = TA ? A[gk + (int64_t)gm * lda] : A[gm + (int64_t)gk * lda];
-            ra[u] = v;
-            int ni, kb;
-            if (!TB) { kb = e & 15; ni = e >> 4; } else { ni = e & 63; kb = e >> 6; }
-            const int gn = n0 + ni, gk2 = k0 + kb;
-            double w = 0.0;
-            if (gn < N && gk2 < K) w = TB ? B[gn + (int64_t)gk2 * ldb] : B[gk2 + (int64_t)gn * ldb];
-            rb[u] = w;
-        }
-    };
-    auto store = [&](int buf) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = tid + u * 128;
-            int mi, kk;
-            if (!TA) { mi = e & 63; kk = e >> 6; } else { kk = e & 15; mi = e >> 4; }
-            As[buf][kk * GS + mi] = ra[u];
-            int ni, kb;
-            if (!TB) { kb = e & 15; ni = e >> 4; } else { ni = e & 63; kb = e >> 6; }
-            Bs[buf][kb * GS + ni] = rb[u];
-        }
-    };
-    const int nk = (K + GBK - 1) / GBK;
-    if (nk > 0) {
-        load(0);
-        store(0);
-    }
-    __syncthreads();
-    for (int kt = 0; kt < nk; ++kt) {
-        const int buf = kt & 1;
-        if (kt + 1 < nk) load((kt + 1) * GBK);
-#pragma unroll
-        for (int ks = 0; ks < GBK; ks += 8) {
-            double af[2][4], bf[4][2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int mb = wm + i * 16;
-                af[i][0] = As[buf][(ks + tq) * GS + mb + g];
-                af[i][1] = As[buf][(ks + tq) * GS + mb + g + 8];
-                af[i][2] = As[buf][(ks + tq + 4) * GS + mb + g];
-                af[i][3] = As[buf][(ks + tq + 4) * GS + mb + g + 8];
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int nb = wn + j * 8;
-                bf[j][0] = Bs[buf][(ks + tq) * GS + nb + g];
-                bf[j][1] = Bs[buf][(ks + tq + 4) * GS + nb + g];
-            }
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma16n8k8(acc[i][j], af[i], bf[j]);
-        }
-        if (kt + 1 < nk) store(buf ^ 1);
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const int gm = m0 + wm + i * 16 + g + ((v >> 1) << 3);
-                const int gn = n0 + wn + j * 8 + 2 * tq + (v & 1);
-                if (gm < M && gn < N) {
-                    double* cp = C + gm + (int64_t)gn * ldc;
-                    double r = alpha * acc[i][j][v];
-                    if (beta != 0.0) r = fma(beta, *cp, r);
-                    *cp = r;
-                }
-            }
-}
-
-// ---------------------------------------------------------------------------
-// per-column panel kernels.  The working column a = A[kb:, col] (nk rows).
-// V is nk x b (ld ldv), T is b x b (ld ldt), Y is nk x b (ld ldy).
-// ---------------------------------------------------------------------------
-constexpr int CT = 256;  // threads per CTA of the row-parallel kernels
-
-struct Col {
-    double* a;   // column (nk rows)
-    int nk;      // rows
-    int j;       // reflector index within the panel
-    int jr;      // right-update width (reflectors 0..jr-1 of Y)
-    int vrow;    // row of V multiplying the right update (col - kb)
-    const double* V;
-    int64_t ldv;
-    const double* T;
-    int64_t ldt;
-    const double* Y;
-    int64_t ldy;
-    double* part;  // per-CTA partials, stride b
-    int b;
-    double* scal;  // [0] tau [1] beta [2] scale [3] alpha [4..] w / dots
-};
-
-// warp w of the CTA accumulates dot(V[rows, t], x[rows]) for t = w, w+8, ...
-__device__ __forceinline__ void cta_vdots(const Col& c, const double* xs, int i0, int cnt, int nt,
-                                          double* out) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int t = warp; t < nt; t += CT / 32) {
-        const double* vc = c.V + (int64_t)t * c.ldv + i0;
-        double s = 0.0;
-        for (int r = lane; r < cnt; r += 32) s = fma(vc[r], xs[r], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) out[t] = s;
-    }
-}
-
-// (1) right update from earlier mini-blocks, then partial V^T a
-__global__ void __launch_bounds__(CT) k_col_right_dots(Col c) {
-    __shared__ double xs[CT];
-    const int i0 = blockIdx.x * CT, i = i0 + threadIdx.x;
-    const int cnt = min(CT, c.nk - i0);
-    if (i < c.nk) {
-        double v = c.a[i];
-        for (int t = 0; t < c.jr; ++t) v = fma(-c.Y[i + (int64_t)t * c.ldy], c.V[c.vrow + (int64_t)t * c.ldv], v);
-        c.a[i] = v;
-        xs[threadIdx.x] = v;
-    }
-    __syncthreads();
-    cta_vdots(c, xs, i0, cnt, c.j, c.part + (int64_t)blockIdx.x * c.b);
-}
-
-// (2) w = T^T (sum of partials)   (left update coefficients)
-__global__ void k_col_w(Col c, int nparts) {
-    extern __shared__ double w0[];  // j entries
-    for (int t = threadIdx.x; t < c.j; t += blockDim.x) {
-        double s = 0.0;
-        for (int p = 0; p < nparts; ++p) s += c.part[(int64_t)p * c.b + t];
-        w0[t] = s;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < c.j; t += blockDim.x) {
-        double s = 0.0;
-        for (int k = 0; k <= t; ++k) s = fma(c.T[k + (int64_t)t * c.ldt], w0[k], s);  // (T^T w0)_t
-        c.scal[8 + t] = s;
-    }
-}
-
-// (3) a -= V w; partial sum of squares of a[j+1:], alpha = a[j]
-__global__ void __launch_bounds__(CT) k_col_left(Col c) {
-    __shared__ double red[CT / 32];
-    const int i = blockIdx.x * CT + threadIdx.x;
-    double sq = 0.0;
-    if (i < c.nk) {
-        double v = c.a[i];
-        for (int t = 0; t < c.j; ++t) v = fma(-c.V[i + (int64_t)t * c.ldv], c.scal[8 + t], v);
-        c.a[i] = v;
-        if (i > c.j) sq = v * v;
-    }
-    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < CT / 32; ++w) s += red[w];
-        c.part[(int64_t)blockIdx.x * c.b] = s;
-    }
-}
-
-// (4) householder_vector scalars (kernels.py:74-99, real case)
-__global__ void k_col_house(Col c, int nparts) {
-    if (threadIdx.x != 0) return;
-    double sigma = 0.0;
-    for (int p = 0; p < nparts; ++p) sigma += c.part[(int64_t)p * c.b];
-    const double alpha = c.a[c.j];
-    double tau, beta, scale;
-    if (sigma == 0.0) {
-        tau = 0.0;
-        beta = alpha;
-        scale = 0.0;
-    } else {
-        const double anorm = sqrt(alpha * alpha + sigma);
-        beta = alpha >= 0.0 ? -anorm : anorm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-    }
-    c.scal[0] = tau;
-    c.scal[1] = beta;
-    c.scal[2] = scale;
-    c.scal[3] = alpha;
-}
-
-// (5) write v_j into V, finalize the column, partial V^T v
-__global__ void __launch_bounds__(CT) k_col_vec(Col c, double* Vw) {
-    __shared__ double xs[CT];
-    const int i0 = blockIdx.x * CT, i = i0 + threadIdx.x;
-    const int cnt = min(CT, c.nk - i0);
-    if (i < c.nk) {
-        double v;
-        const double tau = c.scal[0];
-        if (i < c.j) v = 0.0;
-        else if (i == c.j) v = 1.0;
-        else v = tau == 0.0 ? 0.0 : c.a[i] * c.scal[2];
-        Vw[i + (int64_t)c.j * c.ldv] = v;
-        xs[threadIdx.x] = v;
-        if (i == c.j) c.a[i] = c.scal[1];
-        else if (i > c.j) c.a[i] = 0.0;
-    }
-    __syncthreads();
-    cta_vdots(c, xs, i0, cnt, c.j, c.part + (int64_t)blockIdx.x * c.b);
-}
-
-// (6) T[:j, j] = -tau T[:j,:j] (V[:, :j]^T v_j), T[j, j] = tau  (kernels.py:156-160)
-__global__ void k_col_tcol(Col c, double* Tw, int nparts) {
-    extern __shared__ double d[];  // j entries
-    const double tau = c.scal[0];
-    for (int t = threadIdx.x; t < c.j; t += blockDim.x) {
-        double s = 0.0;
-        for (int p = 0; p < nparts; ++p) s += c.part[(int64_t)p * c.b + t];
-        d[t] = s;
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < c.j; r += blockDim.x) {
-        double s = 0.0;
-        for (int k = r; k < c.j; ++k) s = fma(c.T[r + (int64_t)k * c.ldt], d[k], s);
-        Tw[r + (int64_t)c.j * c.ldt] = -tau * s;
-    }
-    if (threadIdx.x == 0) Tw[c.j + (int64_t)c.j * c.ldt] = tau;
-}
 
 __global__ void k_zero(double* p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -324,18 +63,72 @@ __global__ void k_eye(double* p, int n, int64_t ld) {
 struct Ctx {
     ss_handle* h;
     cudaStream_t st;
+    double* split = nullptr;  // split-K partial tiles
+    size_t split_cap = 0;     // doubles
 };
+
+template <bool TA, bool TB, int MT, int NT, int WM, int WN>
+int gemm_launch(Ctx& x, const ssr::GemmArgs& g, dim3 grid) {
+    using Cfg = ssr::GemmCfg<TA, TB, MT, NT, WM, WN>;
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(x.h)) {
+        SS_CUDA_TRY(x.h, cudaFuncSetAttribute(ssr::k_dmma<TA, TB, MT, NT, WM, WN>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+        configured.set(x.h);
+    }
+    ssr::k_dmma<TA, TB, MT, NT, WM, WN><<<grid, ssr::kGThreads, Cfg::SMEM, x.st>>>(g);
+    SS_LAUNCH_CHECK(x.h);
+    return SS_OK;
+}
+
+template <bool TA, bool TB>
+int gemm_t(Ctx& x, ssr::GemmArgs g) {
+    // tile shape from the output shape: narrow outputs (the Y extension's
+    // A0 V, M V) take narrow N tiles, short M (V^T M) a 64-row tile
+    int BM = 128, BN = 64, shape = 2;
+    if (g.N <= 8) { BN = 8; shape = 0; }
+    else if (g.N <= 32) { BN = 32; shape = 1; }
+    else if (g.N <= 64) { BN = 64; shape = 2; }
+    else if (g.M <= 64) { BM = 64; shape = 4; }
+    // else 128 x 64 at two CTAs per SM (n = 20000: 1.99 s vs 2.12 s with 128 x 128 at one)
+    const int64_t tiles = (int64_t)((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+    const int nkt = (g.K + ssr::kGBK - 1) / ssr::kGBK;
+    // split K when the output has too few tiles to fill the SMs
+    int ks = 1;
+    const int64_t want = 2 * (int64_t)x.h->num_sms;
+    if (tiles < want && nkt >= 32) {
+        ks = (int)std::min<int64_t>({(want + tiles - 1) / tiles, nkt / 16, 32});
+        while (ks > 1 && (size_t)ks * g.M * g.N > x.split_cap) --ks;
+        ks = std::max(ks, 1);
+    }
+    g.ksplit = ks;
+    g.part = x.split;
+    dim3 grid((unsigned)((g.M + BM - 1) / BM), (unsigned)((g.N + BN - 1) / BN), (unsigned)ks);
+    int rc;
+    switch (shape) {
+        case 0: rc = gemm_launch<TA, TB, 1, 1, 8, 1>(x, g, grid); break;
+        case 1: rc = gemm_launch<TA, TB, 1, 4, 8, 1>(x, g, grid); break;
+        case 4: rc = gemm_launch<TA, TB, 2, 4, 2, 4>(x, g, grid); break;
+        default: rc = gemm_launch<TA, TB, 2, 4, 4, 2>(x, g, grid); break;
+    }
+    if (rc) return rc;
+    if (ks > 1) {
+        const int64_t tot = (int64_t)g.M * g.N;
+        const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 4 * (int64_t)x.h->num_sms);
+        ssr::k_gemm_splitk_reduce<<<blocks, 256, 0, x.st>>>(g);
+        SS_LAUNCH_CHECK(x.h);
+    }
+    return SS_OK;
+}
 
 int gemm(Ctx& x, bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int64_t lda,
          const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (M <= 0 || N <= 0) return SS_OK;
-    dim3 grid((M + GBM - 1) / GBM, (N + GBN - 1) / GBN);
-    if (!ta && !tb) k_dgemm<false, false><<<grid, 128, 0, x.st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (!ta && tb) k_dgemm<false, true><<<grid, 128, 0, x.st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (ta && !tb) k_dgemm<true, false><<<grid, 128, 0, x.st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else k_dgemm<true, true><<<grid, 128, 0, x.st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    SS_LAUNCH_CHECK(x.h);
-    return SS_OK;
+    ssr::GemmArgs g{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, 1, nullptr};
+    if (!ta && !tb) return gemm_t<false, false>(x, g);
+    if (!ta && tb) return gemm_t<false, true>(x, g);
+    if (ta && !tb) return gemm_t<true, false>(x, g);
+    return gemm_t<true, true>(x, g);
 }
 
 #define SS_TRY(expr)            \
@@ -343,27 +136,6 @@ int gemm(Ctx& x, bool ta, bool tb, int M, int N, int K, double alpha, const doub
         int _rc = (expr);       \
         if (_rc) return _rc;    \
     } while (0)
-
-// Factor one column of a panel: right update (jr reflectors of Y), left
-// update with the panel's j earlier reflectors, Householder, T column.
-int panel_column(Ctx& x, Col c, double* V, double* T) {
-    const int nparts = (c.nk + CT - 1) / CT;
-    k_col_right_dots<<<nparts, CT, 0, x.st>>>(c);
-    SS_LAUNCH_CHECK(x.h);
-    if (c.j > 0) {
-        k_col_w<<<1, 256, (size_t)c.j * sizeof(double), x.st>>>(c, nparts);
-        SS_LAUNCH_CHECK(x.h);
-    }
-    k_col_left<<<nparts, CT, 0, x.st>>>(c);
-    SS_LAUNCH_CHECK(x.h);
-    k_col_house<<<1, 32, 0, x.st>>>(c, nparts);
-    SS_LAUNCH_CHECK(x.h);
-    k_col_vec<<<nparts, CT, 0, x.st>>>(c, V);
-    SS_LAUNCH_CHECK(x.h);
-    k_col_tcol<<<1, 256, (size_t)std::max(c.j, 1) * sizeof(double), x.st>>>(c, T, nparts);
-    SS_LAUNCH_CHECK(x.h);
-    return SS_OK;
-}
 
 // Apply Q = I - V T V^T (V: rows x k, ld ldv) to M from the right:
 // M[:, 0:rows] <- M (I - V T V^T), M has mrows rows.  Work: W1 = M V, W2 = W1 T.
@@ -386,7 +158,46 @@ int apply_left(Ctx& x, double* M, int64_t ldm, int mcols, const double* V, int64
     return SS_OK;
 }
 
+// One mini-block [js, jb) of panel columns: the cooperative panel kernel
+// (ss_panel.cuh), one CTA per SM.
+int panel_cols(Ctx& x, ssr::Pan& p, int js, int jb) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(x.h)) {
+        SS_CUDA_TRY(x.h, cudaFuncSetAttribute(ssr::k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)x.h->smem_optin));
+        configured.set(x.h);
+    }
+    // the CTAs' own rows of V and Y in shared memory when they fit
+    const int nown = (p.nk + x.h->num_sms - 1) / x.h->num_sms;
+    int stage = ssr::pan_smem_bytes(p.bw, nown) <= x.h->smem_optin ? 1 : 0;
+    const size_t smem = ssr::pan_smem_bytes(p.bw, stage ? nown : 0);
+    void* args[] = {(void*)&p, (void*)&js, (void*)&jb, (void*)&stage};
+    SS_CUDA_TRY(x.h, cudaLaunchCooperativeKernel((const void*)ssr::k_panel, dim3(x.h->num_sms), dim3(ssr::kPT),
+                                                 args, smem, x.st));
+    x.h->launches++;
+    return SS_OK;
+}
+
 }  // namespace
+
+// The reduction's DMMA GEMM behind the C ABI (diagnostics / tests):
+// C = alpha op(A) op(B) + beta C, column-major, op = transpose if ta / tb.
+extern "C" int ss_dgemm(ss_handle* h, int ta, int tb, int M, int N, int K, double alpha, const double* A,
+                        int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                        void* stream) {
+    if (!h) return SS_EARG;
+    if (M < 0 || N < 0 || K < 0) return ss::set_err(h, SS_EDIM, "negative dimension");
+    if (ldc < std::max(M, 1) || lda < std::max(ta ? K : M, 1) || ldb < std::max(tb ? N : K, 1))
+        return ss::set_err(h, SS_EDIM, "leading dimension too small");
+    ss::DevGuard dg(h->device);
+    SS_CUDA_TRY(h, dg.err);
+    Ctx x{h, (cudaStream_t)stream};
+    const size_t split_cap = (size_t)8 << 20;
+    SS_TRY(ss::ensure_ws(h, split_cap * sizeof(double), 1));
+    x.split = (double*)h->ws2;
+    x.split_cap = split_cap;
+    return gemm(x, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
 
 extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64_t lda, double* B,
                              int64_t ldb, double* C, int64_t ldc, double* Q, int64_t ldq,
@@ -408,15 +219,15 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
     // workspace: V, Y (n x bw), T (bw x bw), W1/W2 (max(n,p) x max(bw, n) as needed), partials
     const int64_t ldv = n;
     const int64_t ldw = std::max<int64_t>(std::max(n, p), 1);
-    const int nparts_max = (n + CT - 1) / CT;
     size_t need = 0;
     need += (size_t)ldv * bw_max;        // V
     need += (size_t)ldv * bw_max;        // Y (bottom)
     need += (size_t)bw_max * bw_max;     // T
     need += (size_t)ldw * bw_max * 2;    // W1, W2 for right updates (mrows x k)
     need += (size_t)bw_max * n * 2;      // W1, W2 for left updates (k x mcols)
-    need += (size_t)nparts_max * bw_max; // partials
-    need += 16 + 2 * (size_t)bw_max;     // scalars + w
+    need += ssr::pan_ws_doubles(h->num_sms);  // panel kernel partials
+    const size_t split_cap = (size_t)8 << 20;    // split-K partials (64 MB)
+    need += split_cap;
     SS_TRY(ss::ensure_ws(h, need * sizeof(double), 1));
     double* V = (double*)h->ws2;
     double* Y = V + (size_t)ldv * bw_max;
@@ -426,9 +237,11 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
     double* W2 = W1 + (size_t)ldw * bw_max;
     double* L1 = W2 + (size_t)ldw * bw_max;
     double* L2 = L1 + (size_t)bw_max * n;
-    double* part = L2 + (size_t)bw_max * n;
-    double* scal = part + (size_t)nparts_max * bw_max;
+    double* pws = L2 + (size_t)bw_max * n;
+    x.split = pws + ssr::pan_ws_doubles(h->num_sms);
+    x.split_cap = split_cap;
     const int64_t ldl = bw_max;
+    if (b > ssr::kPBmax || m > ssr::kPBmax) return ss::set_err(h, SS_EARG, "reduction: block size / m > 128");
 
     if (Q) {
         k_eye<<<256, 256, 0, st>>>(Q, n, ldq);
@@ -441,23 +254,22 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
     SS_LAUNCH_CHECK(h);
     k_zero_mat<<<16, 256, 0, st>>>(T, kB, kB, ldt);
     SS_LAUNCH_CHECK(h);
-    for (int j = 0; j < kB; ++j) {
-        Col c;
-        c.a = B + (int64_t)j * ldb;
-        c.nk = n;
-        c.j = j;
-        c.jr = 0;
-        c.vrow = 0;
-        c.V = V;
-        c.ldv = ldv;
-        c.T = T;
-        c.ldt = ldt;
-        c.Y = Y;
-        c.ldy = ldv;
-        c.part = part;
-        c.b = bw_max;
-        c.scal = scal;
-        SS_TRY(panel_column(x, c, V, T));
+    {
+        ssr::Pan pp;
+        pp.a0 = B;
+        pp.lda = ldb;
+        pp.nk = n;
+        pp.bw = kB;
+        pp.m = kB;
+        pp.yext = 0;
+        pp.vrow0 = 0;
+        pp.V = V;
+        pp.Y = Y;
+        pp.ldv = ldv;
+        pp.T = T;
+        pp.ldt = ldt;
+        pp.ws = pws;
+        SS_TRY(panel_cols(x, pp, 0, kB));
     }
     // Bhat[m:, :] = 0 exactly (hessenberg.py:315) and the columns past kB
     // (only when m == n, excluded above) need no work.
@@ -477,28 +289,27 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
         SS_LAUNCH_CHECK(h);
         k_zero_mat<<<16, 256, 0, st>>>(T, bw, bw, ldt);
         SS_LAUNCH_CHECK(h);
+        ssr::Pan pp;
+        pp.a0 = A + kb + (int64_t)zc * lda;
+        pp.lda = lda;
+        pp.nk = nk;
+        pp.bw = bw;
+        pp.m = m;
+        pp.yext = 1;
+        pp.vrow0 = zc - kb;  // V row of column j's right update: col - kb = j - m
+        pp.V = V;
+        pp.Y = Y;
+        pp.ldv = ldv;
+        pp.T = T;
+        pp.ldt = ldt;
+        pp.ws = pws;
         int js = 0;  // first reflector of the current mini-block
         for (int j = 0; j < bw; ++j) {
-            const int col = zc + j;
-            Col c;
-            c.a = A + kb + (int64_t)col * lda;
-            c.nk = nk;
-            c.j = j;
-            // right update from complete mini-blocks: reflectors i <= j - m
-            c.jr = std::min(js, std::max(j - m + 1, 0));
-            c.vrow = col - kb;  // = j - m (only used when jr > 0)
-            c.V = V;
-            c.ldv = ldv;
-            c.T = T;
-            c.ldt = ldt;
-            c.Y = Y;
-            c.ldy = ldv;
-            c.part = part;
-            c.b = bw_max;
-            c.scal = scal;
-            SS_TRY(panel_column(x, c, V, T));
             const int jb = j + 1;
             if (jb % m == 0 || jb == bw) {
+                // panel columns [js, jb) (right update from the complete
+                // mini-blocks, reflectors i <= j - m), then Y for them
+                SS_TRY(panel_cols(x, pp, js, jb));
                 // Y[:, js:jb] = (A0[kb:, kb+js:] V[js:, js:jb] - Y[:, :js] (V[:, :js]^T V[:, js:jb])) T[js:jb, js:jb]
                 const int cw = jb - js;
                 SS_TRY(gemm(x, false, false, nk, cw, nk - js, 1.0, A + kb + (int64_t)(kb + js) * lda, lda,

@@ -1,7 +1,7 @@
 """Text summary of ncu captures for profiles/ (experiment tooling):
 key metrics + top stall reasons per captured kernel, and the per-kernel
 totals of a launch-list CSV.
-  python tools/ncu_summary.py launches.csv rep1.ncu-rep [rep2.ncu-rep ...]"""
+  python tools/ncu_summary.py launches.csv|- rep1.ncu-rep [rep2.ncu-rep ...]"""
 import csv, io, subprocess, sys
 from collections import defaultdict
 
@@ -68,5 +68,6 @@ if __name__ == "__main__":
     out = []
     for rep in sys.argv[2:]:
         out += rep_summary(rep)
-    out += [""] + launch_summary(sys.argv[1])
+    if sys.argv[1] != "-":
+        out += [""] + launch_summary(sys.argv[1])
     print("\n".join(out))
