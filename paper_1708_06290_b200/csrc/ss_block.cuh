@@ -34,8 +34,8 @@ namespace ssd {
 
 constexpr int kBlkNB = 128;   // outer block (rows per CTA = threads)
 constexpr int kBlkInner = 32; // inner window (one warp)
-#ifndef SS_BLK_MINB
-#define SS_BLK_MINB 4  // resident CTAs per SM the register budget targets
+#ifndef SS_BLK_OCC
+#define SS_BLK_OCC 8  // resident one-warp CTAs per SM the register budget targets
 #endif
 
 struct BlkDims {
@@ -101,7 +101,7 @@ __host__ __device__ inline size_t blk_smem_bytes(int m) {
 //    at no extra instruction; lanes < m carry the m rows of P22 (e_{nbi+j})
 //    in a second window.
 template <int M, int NSW>
-__global__ void __launch_bounds__(32, NSW == 1 ? 8 : 6)
+__global__ void __launch_bounds__(32, NSW == 1 ? SS_BLK_OCC : 6)
     k_block(BlkDims d, double2* __restrict__ Z, double2* __restrict__ W, int sb) {
     constexpr int L = M + 1;
     constexpr int HW = (L + 1) / 2;  // window entries per lane of a column pair

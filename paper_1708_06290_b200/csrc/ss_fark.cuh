@@ -286,4 +286,154 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// m = 1 (config 3's pseudospectrum grid): the composite's far pass with the
+// shifts as columns.  A unit is (64-row tile, group of kFkmShifts = 80
+// shifts); consumer warp w owns shifts 10 w .. 10 w + 9 of the group (lane
+// q = lane & 1 five of them) with the same 4 x 5 register tile and the same
+// packed panel as k_fark.  Per shift the composite is W12 (K entries) and the
+// scalar W22, stored group-major [group][row][80] (k_wcomp) so a KC-row chunk
+// of the group's W is ONE contiguous bulk copy.  W22 is diagonal across the
+// unit's columns: z <- z W22 + Pan W12 is applied in the epilogue from the Z
+// values read there (no Z chunks through the ring).
+// ---------------------------------------------------------------------------
+constexpr int kFkmShifts = 80;
+__host__ __device__ constexpr size_t farkm_stage_bytes() {
+    return (size_t)kFkKC * kFkTile * 8 + (size_t)kFkKC * kFkmShifts * 16;
+}
+template <int NST>
+__host__ __device__ constexpr size_t farkm_smem_bytes() {
+    return 256 + NST * farkm_stage_bytes();
+}
+
+template <int NST>
+__global__ void __launch_bounds__(32 * 9, 1) k_farkm(FarKDims u, double2* Z, const double2* __restrict__ W) {
+    constexpr int S = kFkmShifts, R = 4, C = 5, RG = 16, TILE = kFkTile, KC = kFkKC;
+    constexpr size_t SB = farkm_stage_bytes();
+    constexpr size_t PANB = (size_t)KC * TILE * 8;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NST]
+    uint64_t* empty = full + NST;                         // [NST] (count 8)
+    unsigned char* stages = smem + 256;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = u.r0, sb = u.sb, K = u.K, nk = u.nk;
+    const int nsu = (sb + S - 1) / S;  // shift groups
+    const int64_t units = (int64_t)u.ntiles * nsu;
+    const int64_t gstride = (int64_t)u.wstride;  // complex per group: (Kmax + 1) x 80
+    const int spl = u.spl, team = blockIdx.x / spl, h = blockIdx.x - team * spl, nteams = gridDim.x / spl;
+    const int64_t ua0 = units * team / nteams, ub = units * (team + 1) / nteams;
+    const int64_t ua = ua0 + h;
+    const int nun = ua < ub ? (int)((ub - ua + spl - 1) / spl) : 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (nun <= 0) return;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int g = 0;
+            for (int k = 0; k < nun; ++k) {
+                const int64_t unit = ua + (int64_t)k * spl;
+                const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = g % NST, use = g / NST;
+                    if (use > 0) mbar_wait_sleep(empty + s, (use - 1) & 1);
+                    unsigned char* st = stages + (size_t)s * SB;
+                    const int kcols = min(KC, K - kc * KC);
+                    mbar_expect_tx(full + s, (unsigned)PANB + (unsigned)(kcols * S * 16));
+                    tma_bulk_g2s(st, u.pan + ((size_t)tile * nk + kc) * KC * TILE, (unsigned)PANB, full + s);
+                    tma_bulk_g2s(st + PANB, W + grp * gstride + (int64_t)kc * KC * S, (unsigned)(kcols * S * 16),
+                                 full + s);
+                }
+            }
+        }
+        return;
+    }
+
+    const int cw = warp - 1;  // shifts 10 cw .. 10 cw + 9 of the group
+    const int rg = lane >> 1, q = lane & 1;
+    const int cb = cw * 10 + q * C;  // first of this lane's 5 shifts (group-local)
+    const int dlo = r0 - 1;
+    int g = 0;
+    for (int k = 0; k < nun; ++k) {
+        const int64_t unit = ua + (int64_t)k * spl;
+        const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles);
+        const int l0 = grp * S;
+        const int i0 = u.rlo + tile * TILE;
+        const bool interior = i0 + TILE <= (u.mnb > 0 ? dlo : r0);
+        double2 acc[R][C];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[r][c] = cz();
+        for (int kc = 0; kc < nk; ++kc, ++g) {
+            const int s = g % NST, use = g / NST;
+            mbar_wait(full + s, use & 1);
+            const unsigned char* st = stages + (size_t)s * SB;
+            const int kcols = min(KC, K - kc * KC);
+            const double* pan = reinterpret_cast<const double*>(st) + rg * 2;
+            const double2* ws = reinterpret_cast<const double2*>(st + PANB) + cb;
+            if (!interior && kc == 0) {
+                // the lazy shift: the one row r0 - 1 carries -sigma_l W12_l[0]
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (i0 + rg + RG * r == dlo) {
+#pragma unroll
+                        for (int c = 0; c < C; ++c) {
+                            const int l = min(l0 + cb + c, sb - 1);
+                            acc[r][c] = csub(acc[r][c], cmul(u.shifts[l], ws[c]));
+                        }
+                    }
+                }
+            }
+#pragma unroll 4
+            for (int j = 0; j < kcols; ++j) {
+                double a[R];
+#pragma unroll
+                for (int p = 0; p < R / 2; ++p) {
+                    const double2 v = *reinterpret_cast<const double2*>(pan + j * TILE + p * (2 * RG));
+                    a[2 * p] = v.x;
+                    a[2 * p + 1] = v.y;
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const double2 pv = ws[j * S + c];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        // epilogue: z <- z W22 + acc for the lane's 4 rows x 5 shifts
+        // (every load before any store: Z is not restrict)
+        const double2* w22 = W + grp * gstride + (int64_t)K * S + cb;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int64_t l = l0 + cb + c;
+            if (l >= sb) continue;
+            const double2 wz = w22[c];
+            const double2* zc = Z + l * u.LDZ + i0 + rg;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (i0 + rg + RG * r < r0) acc[r][c] = cfma(__ldg(zc + RG * r), wz, acc[r][c]);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int64_t l = l0 + cb + c;
+            if (l >= sb) continue;
+            double2* zc = Z + l * u.LDZ + i0 + rg;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (i0 + rg + RG * r < r0) zc[RG * r] = acc[r][c];
+        }
+    }
+}
+
 }  // namespace ssd

@@ -735,12 +735,14 @@ struct WcShape {
     int S, NST;
 };
 static bool wc_shape(int m, WcShape& w) {
+    if (m == 1) { w = {kFkmShifts, 4}; return true; }
     if (m == 40 || m == 50) { w = {2, 3}; return true; }
     if (m == 60) { w = {1, 4}; return true; }
     return false;
 }
 static size_t wc_far_smem(int m) {
     switch (m) {
+        case 1: return farkm_smem_bytes<4>();
         case 40: return fark_smem_bytes<4, 2, 3>();
         case 50: return fark_smem_bytes<5, 2, 3>();
         case 60: return fark_smem_bytes<6, 1, 4>();
@@ -753,6 +755,18 @@ static int wc_jz(int m) {
         case 50: return fark_jz<5, 2>();
         default: return fark_jz<6, 1>();
     }
+}
+static int launch_farkm(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z,
+                        const double2* W) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)farkm_smem_bytes<4>()));
+        configured.set(h);
+    }
+    k_farkm<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
 }
 static int launch_wc_far(ss_handle* h, int m, int grid, cudaStream_t st, const FarKDims& fk, double2* Z,
                          const double2* W) {
@@ -767,32 +781,45 @@ static int launch_wc_far(ss_handle* h, int m, int grid, cudaStream_t st, const F
 constexpr int kWcRows = 32;  // W rows per k_wcomp CTA
 __host__ __device__ inline size_t wcomp_smem(int m) { return (size_t)(m * m + kWcRows * m) * 16; }
 
+// Composite W layout: element (row, c) of shift l at
+//   W + (l / G) gs + (l % G) ls + row rs + c
+// (m > 1: G = 1, gs = per-shift stride, rs = m, j-major rows of one shift;
+//  m = 1, k_farkm: G = 80, gs = (Kmax + 1) 80, ls = 1, rs = 80, the group's
+//  shifts side by side in every row).
+struct WcLayout {
+    int G;
+    int64_t gs, ls, rs;
+    __host__ __device__ int64_t off(int l) const { return (int64_t)(l / G) * gs + (int64_t)(l % G) * ls; }
+};
+
 // Fold window P (rows [0, nb) P12, [nb, nb + m) P22; P_l at P + l pstride)
-// into the composite W of shift l (W + l wstride, j-major rows of m):
-// rows [x, x + nb) <- P12; rows [x + nb, K + m) <- rows P22 (first window of
-// the composite, x + nb == K: W22 <- P22).  grid (sb, row chunks).
+// into the composite W of shift l: rows [x, x + nb) <- P12; rows
+// [x + nb, K + m) <- rows P22 (first window of the composite, x + nb == K:
+// W22 <- P22).  grid (sb, row chunks).
 __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool first, int64_t pstride,
-                                               const double2* __restrict__ P, int64_t wstride,
+                                               const double2* __restrict__ P, WcLayout lw,
                                                double2* __restrict__ W) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2* P22 = reinterpret_cast<double2*>(smem);  // m x m
     double2* Wr = P22 + m * m;                        // [kWcRows][m]
     const int l = blockIdx.x, tid = threadIdx.x;
     const double2* Pl = P + (int64_t)l * pstride;
-    double2* Wl = W + (int64_t)l * wstride;
+    double2* Wl = W + lw.off(l);
+    const int64_t rs = lw.rs;
     const int r0 = x + nb, nrows = K + m - r0;  // rows multiplied by P22
     const int c0 = blockIdx.y * kWcRows;
     if (blockIdx.y == 0)
-        for (int e = tid; e < nb * m; e += blockDim.x) Wl[(int64_t)x * m + e] = Pl[e];
+        for (int e = tid; e < nb * m; e += blockDim.x) Wl[(int64_t)(x + e / m) * rs + e % m] = Pl[e];
     if (first) {
         if (blockIdx.y == 0)
-            for (int e = tid; e < m * m; e += blockDim.x) Wl[(int64_t)K * m + e] = Pl[(int64_t)nb * m + e];
+            for (int e = tid; e < m * m; e += blockDim.x)
+                Wl[(int64_t)(K + e / m) * rs + e % m] = Pl[(int64_t)nb * m + e];
         return;
     }
     if (c0 >= nrows) return;
     const int rc = min(kWcRows, nrows - c0);
     for (int e = tid; e < m * m; e += blockDim.x) P22[e] = Pl[(int64_t)nb * m + e];
-    for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)(r0 + c0) * m + e];
+    for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)(r0 + c0 + e / m) * rs + e % m];
     __syncthreads();
     for (int e = tid; e < rc * m; e += blockDim.x) {
         const int r = e / m, c = e - r * m;
@@ -804,7 +831,30 @@ __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool
             a1 = cfma(wr[j + 1], P22[(j + 1) * m + c], a1);
         }
         if (j < m) a0 = cfma(wr[j], P22[j * m + c], a0);
-        Wl[(int64_t)(r0 + c0) * m + e] = cadd(a0, a1);
+        Wl[(int64_t)(r0 + c0 + r) * rs + c] = cadd(a0, a1);
+    }
+}
+
+// m = 1: the same fold elementwise in the group layout (row-major across the
+// 80 shifts of a group: coalesced), one thread per (row, shift).
+__global__ void __launch_bounds__(256) k_wcomp1(int K, int x, int nb, bool first, int sb, int64_t pstride,
+                                                const double2* __restrict__ P, int64_t gstride,
+                                                double2* __restrict__ W) {
+    constexpr int S = kFkmShifts;
+    const int ngroups = (sb + S - 1) / S;
+    const int r_lo = first ? x : x;  // rows [x, K + 1)
+    const int64_t per = (int64_t)(K + 1 - r_lo) * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per * ngroups;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int grp = (int)(e / per);
+        const int64_t rem = e - grp * per;
+        const int row = r_lo + (int)(rem / S), c = (int)(rem % S);
+        const int l = min(grp * S + c, sb - 1);
+        const double2* Pl = P + (int64_t)l * pstride;
+        double2* w = W + grp * gstride + (int64_t)row * S + c;
+        if (row < x + nb) *w = Pl[row - x];
+        else if (first) *w = Pl[nb];  // row K: W22 <- P22
+        else *w = cmul(*w, Pl[nb]);
     }
 }
 
@@ -1122,12 +1172,14 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
         account_ref_flops(h, sb, n, m, ptop, nb0);  // the reference's stack
         WcShape wsh;
         wc_shape(m, wsh);
-        const int64_t wstride = (int64_t)(kWcWin * nb0 + m) * m;
+        // composite W layout (k_fark: per shift j-major; m = 1, k_farkm:
+        // groups of 80 shifts side by side)
+        const int64_t wstride = m == 1 ? (int64_t)(kWcWin * nb0 + 1) * kFkmShifts : (int64_t)(kWcWin * nb0 + m) * m;
+        const WcLayout lw = m == 1 ? WcLayout{kFkmShifts, wstride, 1, kFkmShifts} : WcLayout{1, wstride, 0, m};
         static ss::DevMask configured;  // devices configured
         if (!configured.has(h)) {
             SS_CUDA_TRY(h, allow_max_smem(h, k_rq_big));
-            SS_CUDA_TRY(h, cudaFuncSetAttribute(k_wcomp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)wcomp_smem(m)));
+            SS_CUDA_TRY(h, allow_max_smem(h, k_wcomp));
             configured.set(h);
         }
         while (k >= m + 1) {
@@ -1159,10 +1211,54 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 rd.lda = a.lda;
                 rd.shifts = d.shifts;
                 rd.LDZ = LDZ;
-                k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(nb, m), st>>>(rd, B.Z, B.P);
+                if (m == 1)
+                    k_rq_m1<<<(sb + 4 * kM1Warps - 1) / (4 * kM1Warps), 32 * kM1Warps, 0, st>>>(rd, B.Z, B.P);
+                else
+                    k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(nb, m), st>>>(rd, B.Z, B.P);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_RQ);
-                if (r0 > r0G) {
+                if (r0 > r0G && m == 1) {
+                    // near (m = 1): the one-level far kernel with ten shifts per
+                    // unit as its columns, rows [r0G, r0)
+                    UpdDims u;
+                    u.n = n;
+                    u.m = m;
+                    u.ptop = ptop;
+                    u.ident_top = 0;
+                    u.A = a.A;
+                    u.lda = a.lda;
+                    u.T = a.C;
+                    u.ldt = a.ldc;
+                    u.shifts = d.shifts;
+                    u.sb = sb;
+                    u.LDZ = LDZ;
+                    u.nb = nb;
+                    u.mnb = std::min(m, nb);
+                    u.r0 = r0;
+                    u.c0 = cw;
+                    u.nc = nb + 1;
+                    u.rlo = r0G;
+                    u.nws = 1;
+                    u.ksplit = 2;
+                    u.S = 1;
+                    u.SG = 32;
+                    u.pstride = (int64_t)nc;
+                    u.p12off = 0;
+                    u.p22off = nb;
+                    u.zid = 0;
+                    u.flags = 0;
+                    u.jh = std::max(0, std::min(nb, (nb - 2) / 2));
+                    FarShape f{2, 5, 4, 4, 8, 1};
+                    f.MSH = true;
+                    const int rows = r0 - r0G;
+                    const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * ((sb + 9) / 10);
+                    const int grid = (int)std::min<int64_t>(units, h->num_sms);
+                    ev = ss::timing_begin(h, st);
+                    rc = launch_far(h, f, grid, far_smem_bytes(nb, 10, f.tile(), f.NST), st, u, B.Z, B.P);
+                    if (rc) return rc;
+                    ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * (double)sb,
+                                   8.0 * rows * (double)sb * nb, 4.0 * (double)rows * nb * sb);
+                } else if (r0 > r0G) {
                     // near: the composite's rows above this window (generic update)
                     UpdDims u;
                     u.n = n;
@@ -1205,9 +1301,15 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 }
                 ev = ss::timing_begin(h, st);
                 const int nrows = K + m - (cw - c0 + nb);
-                dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
-                k_wcomp<<<gc, 256, wcomp_smem(m), st>>>(m, K, cw - c0, nb, b == 0, (int64_t)nc * m, B.P,
-                                                        wstride, B.W);
+                if (m == 1) {
+                    const int64_t tot = (int64_t)(K + 1 - (cw - c0)) * kFkmShifts * ((sb + kFkmShifts - 1) / kFkmShifts);
+                    const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 8 * (int64_t)h->num_sms);
+                    k_wcomp1<<<blocks, 256, 0, st>>>(K, cw - c0, nb, b == 0, sb, (int64_t)nc, B.P, wstride, B.W);
+                } else {
+                    dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
+                    k_wcomp<<<gc, 256, wcomp_smem(m), st>>>(m, K, cw - c0, nb, b == 0, (int64_t)nc * m, B.P,
+                                                            lw, B.W);
+                }
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
             }
@@ -1248,7 +1350,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 double nnz = (double)std::min(rows, ptop) * K;  // Chat rows dense
                 if (rows > ptop) nnz += (double)(rows - ptop) * K;
                 ev = ss::timing_begin(h, st);
-                int rc = launch_wc_far(h, m, grid, st, fk, B.Z, B.W);
+                int rc = m == 1 ? launch_farkm(h, grid, st, fk, B.Z, B.W) : launch_wc_far(h, m, grid, st, fk, B.Z, B.W);
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
                                8.0 * rows * (double)sb * m * K, 4.0 * m * nnz * sb);
@@ -1762,7 +1864,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     // wide windows (m = 40 / 50 / 60, transfer function): window composites
     // with one K-streamed far pass per kWcWin windows (SS_ONE_LEVEL=1: per window)
     WcShape wsh;
-    const bool wc = !two_level && a.mode == 0 && rq_big(m) && wc_shape(m, wsh) && !getenv("SS_ONE_LEVEL") &&
+    const bool wc = !two_level && a.mode == 0 && (rq_big(m) || (m == 1 && use_house)) && wc_shape(m, wsh) &&
+                    !getenv("SS_ONE_LEVEL") && !(m == 1 && getenv("SS_RQ_M1_OFF")) &&
                     wc_far_smem(m) <= h->smem_optin && wcomp_smem(m) <= h->smem_optin &&
                     kWcWin * kWcNb <= 4 * kBlkNB;
     if (wc) nb0 = std::min(nb0, kWcNb);
@@ -1815,6 +1918,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     // batch size from memory: the window state + P (or W) per shift
     const int ncmax = nb0 + m;
     const int64_t wc_stride = wc ? (int64_t)(kWcWin * nb0 + m) * m : 0;  // composite W per shift
+    const size_t wc_slack = m == 1 ? (size_t)kFkmShifts * wc_stride * 16 : 0;  // last group of 80 shifts
     const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)ncmax * m + wc_stride;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64 +
                              (size_t)(xh_stride + w22h_stride + y_stride) * 16;
@@ -1831,7 +1935,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     }
     sb_max = std::min<int64_t>(sb_max, a.s);
     {
-        int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256, 0);
+        int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256 + wc_slack, 0);
         if (rc) return rc;
     }
     double2* Z0 = (double2*)h->ws;
