@@ -993,7 +993,11 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 fk.wstride = wstride;
                 fk.woff = woff;
                 fk.nk = (ncols + kFkKC - 1) / kFkKC;
-                fk.jz = m == 10 ? fark_jz<1, 8>() : fark_jz<2, 4>();
+                // m = 20: 4 shifts x 2 column blocks per unit, 4 stages (measured
+                // at config 4 against 3 x 4 / 5 x 3 / 6 x 2: 4.01k / 4.31k / 4.70k
+                // vs 4.82k shifts/s)
+                constexpr int S20 = 4, N20 = kFarkStages;
+                fk.jz = m == 10 ? fark_jz<1, 8>() : fark_jz<2, S20>();
                 fk.nz = (m + fk.jz - 1) / fk.jz;
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
@@ -1001,7 +1005,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
-                const int S = m == 10 ? 8 : 4;
+                const int S = m == 10 ? 8 : S20;
                 const int64_t units = (int64_t)fk.ntiles * ((sb + S - 1) / S);
                 // teams of 4 CTAs per shift group: the live W set drops from ~100 MB
                 // (over L2) to ~25 MB, DRAM bytes per launch 8.5 -> 2.6 GB at config 4
@@ -1014,7 +1018,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (r0 > std::max(rlo, ptop)) nnz += (double)(r0 - std::max(rlo, ptop)) * ncols;
                 ev = ss::timing_begin(h, st);
                 int rc = m == 10 ? launch_fark<1, 8>(h, grid, st, fk, B.Z, B.P)
-                                 : launch_fark<2, 4>(h, grid, st, fk, B.Z, B.P);
+                                 : launch_fark<2, S20, N20>(h, grid, st, fk, B.Z, B.P);
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
                                8.0 * rows * (double)sb * m * ncols, 4.0 * m * nnz * sb);
