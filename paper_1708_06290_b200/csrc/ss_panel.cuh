@@ -39,6 +39,7 @@ namespace cg = cooperative_groups;
 
 constexpr int kPT = 256;     // threads per CTA
 constexpr int kPBmax = 128;  // widest panel (block_size is capped at 128)
+constexpr int kPTC = kPT / 4;  // t's per gathered chunk of cross-CTA partials (64)
 
 struct Pan {
     double* a0;    // panel column j: a0 + j * lda, rows [0, nk)
@@ -55,8 +56,8 @@ struct Pan {
 };
 
 __host__ __device__ inline size_t pan_ws_doubles(int G) { return (size_t)G * kPBmax * 2 + (size_t)G + 8; }
-__host__ __device__ inline size_t pan_smem_bytes(int bw, int nown_staged) {
-    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (size_t)2 * nown_staged * bw) * 8;
+__host__ __device__ inline size_t pan_smem_bytes(int bw, int G, int nown_staged) {
+    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (size_t)kPTC * G + (size_t)2 * nown_staged * bw) * 8;
 }
 
 // The CTA's own rows of V and Y, staged in shared memory when they fit
@@ -85,17 +86,29 @@ __device__ __forceinline__ void own_vdots(const Own& o, int rlo, int rhi, const 
     }
 }
 
-// d[t] = sum over CTAs c of part[t * G + c], t < nt: a warp per t, lanes
-// over c in a fixed order, then a fixed shuffle tree (deterministic)
-__device__ __forceinline__ void cta_sums(const double* part, int G, int nt, double* d) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int t = warp; t < nt; t += kPT / 32) {
-        const double* pt = part + (size_t)t * G;
+// d[t] = sum over CTAs c of part[t * G + c], t < nt.  The nt x G partials
+// (contiguous) are gathered into shared memory with cp.async -- every load
+// in flight at once: one L2 round trip instead of one per t (the per-t warp
+// loop measured ~1 us per t, 60% of the kernel) -- then four threads per t
+// sum strided quarters and combine them with a fixed shuffle tree
+// (deterministic: the same order in every CTA and run).
+__device__ __forceinline__ void cta_sums(const double* part, int G, int nt, double* d, double* buf) {
+    const int tid = threadIdx.x;
+    for (int t0 = 0; t0 < nt; t0 += kPTC) {
+        const int nc = min(kPTC, nt - t0);
+        const double* src = part + (size_t)t0 * G;
+        for (int e = tid; e < nc * G; e += kPT) cpa8(buf + e, src + e, true);
+        cpa_commit();
+        cpa_wait<0>();
+        __syncthreads();
+        const int t = tid >> 2, q = tid & 3;
         double s = 0.0;
-        for (int c = lane; c < G; c += 32) s += pt[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) d[t] = s;
+        if (t < nc)
+            for (int c = q; c < G; c += 4) s += buf[t * G + c];
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (q == 0 && t < nc) d[t0 + t] = s;
+        __syncthreads();  // buf is reused by the next chunk / call
     }
 }
 
@@ -136,6 +149,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     double* red = d + kPBmax;      // [kPT / 32]
     double* sc = red + kPT / 32;   // [8] tau, beta, scale
     double* vrs = sc + 8;          // [kPBmax] V row of the right update
+    double* pbuf = vrs + kPBmax;   // [kPTC * G] cross-CTA partials (cta_sums)
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
     const int rlo = (int)((int64_t)nk * cta / G), rhi = (int)((int64_t)nk * (cta + 1) / G);
     const int nown = rhi - rlo;
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     if (stage) {
         // own rows of V (columns < jb; column j written here as it is formed)
         // and Y (columns < js, read-only in this kernel)
-        Vs = vrs + kPBmax;
+        Vs = pbuf + (size_t)kPTC * gridDim.x;
         double* Ys = Vs + (size_t)nown * bw;
         for (int e = tid; e < nown * jb; e += kPT) {
             const int r = e % nown, t = e / nown;
@@ -172,7 +186,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     for (int j = js; j < jb; ++j) {
         double* a = p.a0 + (int64_t)j * p.lda;
         // ---- S2: w = T^T (sum of partials); a -= V w; squares below row j ----
-        cta_sums(ppart, G, j, d);
+        cta_sums(ppart, G, j, d, pbuf);
         __syncthreads();
         for (int t = tid; t < j; t += kPT) {
             double s = 0.0;
@@ -206,13 +220,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
         }
         grid.sync();
         // ---- S3: Householder scalars (householder_vector, kernels.py:74-99) ----
-        if (tid < 32) {
-            double sg = 0.0;
-            for (int c = tid; c < G; c += 32) sg += spart[c];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
-            if (tid == 0) red[0] = sg;
-        }
+        cta_sums(spart, G, 1, red, pbuf);
         __syncthreads();
         if (tid == 0) {
             const double sigma = red[0];
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
         if (j + 1 < jb) s1_right(p, o, vrs, j + 1, js, rlo, rhi, ppart + cta, G);
         grid.sync();
         // ---- T column (kernels.py:156-160; every CTA, same order) ----
-        cta_sums(qpart, G, j, d);
+        cta_sums(qpart, G, j, d, pbuf);
         __syncthreads();
         for (int r = tid; r < j; r += kPT) {
             double s = 0.0;

@@ -169,10 +169,12 @@ int panel_cols(Ctx& x, ssr::Pan& p, int js, int jb) {
     }
     // the CTAs' own rows of V and Y in shared memory when they fit
     const int nown = (p.nk + x.h->num_sms - 1) / x.h->num_sms;
-    int stage = ssr::pan_smem_bytes(p.bw, nown) <= x.h->smem_optin ? 1 : 0;
-    const size_t smem = ssr::pan_smem_bytes(p.bw, stage ? nown : 0);
+    const int G = x.h->num_sms;
+    int stage = ssr::pan_smem_bytes(p.bw, G, nown) <= x.h->smem_optin ? 1 : 0;
+    const size_t smem = ssr::pan_smem_bytes(p.bw, G, stage ? nown : 0);
+    if (smem > x.h->smem_optin) return ss::set_err(x.h, SS_EARG, "reduction: panel too wide for shared memory");
     void* args[] = {(void*)&p, (void*)&js, (void*)&jb, (void*)&stage};
-    SS_CUDA_TRY(x.h, cudaLaunchCooperativeKernel((const void*)ssr::k_panel, dim3(x.h->num_sms), dim3(ssr::kPT),
+    SS_CUDA_TRY(x.h, cudaLaunchCooperativeKernel((const void*)ssr::k_panel, dim3(G), dim3(ssr::kPT),
                                                  args, smem, x.st));
     x.h->launches++;
     return SS_OK;
