@@ -21,10 +21,13 @@
 //             and the reference's mirrored Givens schedule give the same
 //             |L_ii| (the LQ factor is unique up to phases), so the
 //             singularity decisions agree.
-//   k_tupd    rows below the window: S <- S T + Pan(A^T, -I) U12 (the
+//   update    rows below the window: S <- S T + Pan(A^T, -I) U12 (the
 //             reference's update_shift + trail_shift, solvers.py:431-468),
 //             with w treated as an extra state column; lazy-shift rows get
-//             -sigma P12.
+//             -sigma P12.  The forward sweep's window-update kernel with the
+//             [A^T; -I] panel (k_update<..., TR>, register tiles, staged P and
+//             rows; the -I rows past the window's last column are skipped:
+//             their state is still zero); k_tupd (row per thread) for m > 99.
 //   k_ttail   one CTA per shift: the unblocked m-column tail with the
 //             reference's Givens rotations fused with the last substitutions
 //             (solvers.py:470-486); x = w[n:].
@@ -35,8 +38,14 @@
 #include "ss_device.cuh"
 #include "ss_internal.h"
 #include "ss_rq_house.cuh"
+#include "ss_update.cuh"
 
 using namespace ssd;
+
+namespace ss {
+// ss_sweep.cu: the window-update kernel on the [A^T; -I] panel
+int launch_update_tr(ss_handle* h, ssd::UpdDims u, int rows, double2* S, const double2* P, cudaStream_t st);
+}
 
 namespace {
 
@@ -748,9 +757,39 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
             int rc = launch_lq(h, m, sb, st, d, ls, Sb, Pb);
             if (rc) return rc;
             ss::timing_end(h, st, ev, ss::PH_RQ);
-            const int rows = 2 * n - (k0 + ls.nb);
+            // rows below the window with a nonzero state or panel entry: all of
+            // A^T's, and the -I rows up to this window's last column (the rest
+            // of the stacked state is still the seed's zero)
+            const int rend = std::min(2 * n, n + ls.c0 + ls.nb);
+            const int rows = rend - (k0 + ls.nb);
             ev = ss::timing_begin(h, st);
-            rc = launch_tupd(h, st, d, ls, Sb, Pb, rows);
+            {
+                UpdDims u;
+                u.n = n;
+                u.m = mp;
+                u.ptop = 0;
+                u.ident_top = 0;
+                u.A = Ahat;
+                u.lda = lda;
+                u.T = nullptr;
+                u.ldt = 0;
+                u.shifts = d.shifts;
+                u.sb = sb;
+                u.LDZ = LDS;
+                u.nb = ls.nb;
+                u.mnb = std::min(m, ls.nb);
+                u.r0 = rend;
+                u.c0 = ls.c0;
+                u.nc = ls.nb + mp;
+                u.rlo = k0 + ls.nb;
+                u.lz0 = k0 + ls.nb + (m - u.mnb);
+                u.lzp = ls.nb - u.mnb;
+                // the window-update kernel covers <= 10 column blocks of 10
+                // (mp <= 100); wider states keep the row-per-thread k_tupd
+                if (rows <= 0) rc = SS_OK;
+                else if (mp <= 100) rc = ss::launch_update_tr(h, u, rows, Sb, Pb, st);
+                else rc = launch_tupd(h, st, d, ls, Sb, Pb, rows);
+            }
             if (rc) return rc;
             const double fl_b = (double)sb * 8.0 * rows * mp * mp;
             const double fl_o = (double)sb * 8.0 * rows * mp * ls.nb;

@@ -597,6 +597,65 @@ int launch_update(ss_handle* h, const UpdTile& t, dim3 grid, int threads, size_t
     return ss::set_err(h, SS_EARG, "unsupported update tile");
 }
 
+// Transposed sweep's rows-below update (ss_lq.cu) on the window-update
+// kernel with the [A^T; -I] panel (k_update<..., TR = true>): the state has
+// mp = m + 1 columns (the m active columns and w).
+template <int G, int C, bool EXACT>
+int launch_update_tr_t(ss_handle* h, dim3 grid, int threads, size_t smem, cudaStream_t st, const UpdDims& u,
+                       double2* S, const double2* P) {
+    static ss::DevMask configured;  // devices configured
+    if (!configured.has(h)) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320, false, true>));
+        SS_CUDA_TRY(h, allow_max_smem(h, k_update<G, C, EXACT, 320, true, true>));
+        configured.set(h);
+    }
+    if (smem > h->smem_optin)
+        k_update<G, C, EXACT, 320, true, true><<<grid, threads, upd_smem_bytes(u.nb, u.m, u.S, true), st>>>(u, S, S, P);
+    else
+        k_update<G, C, EXACT, 320, false, true><<<grid, threads, smem, st>>>(u, S, S, P);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+}  // namespace
+
+namespace ss {
+int launch_update_tr(ss_handle* h, UpdDims u, int rows, double2* S, const double2* P, cudaStream_t st) {
+    const UpdTile t = pick_tile(u.m);
+    const int nws = (u.m + t.G * t.C - 1) / (t.G * t.C);
+    u.nws = nws;
+    u.ksplit = 1;
+    u.jh = u.nb;
+    u.S = std::max(1, std::min(8 / nws, 4));
+    const size_t two_per_sm = h->smem_optin / 2 - 1024;
+    while (u.S > 1 && upd_smem_bytes(u.nb, u.m, u.S) > two_per_sm) u.S--;
+    u.SG = u.S * 4;
+    u.pstride = (int64_t)u.nc * u.m;
+    u.p12off = 0;
+    u.p22off = (int64_t)u.nb * u.m;
+    u.zid = 0;
+    u.flags = 0;
+    const dim3 grid((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((u.sb + u.SG - 1) / u.SG));
+    const int threads = 32 * u.S * nws;
+    const size_t smem = upd_smem_bytes(u.nb, u.m, u.S);
+    if (t.G == 2 && t.C == 5 && t.exact) return launch_update_tr_t<2, 5, true>(h, grid, threads, smem, st, u, S, P);
+    if (t.G == 2 && t.C == 5) return launch_update_tr_t<2, 5, false>(h, grid, threads, smem, st, u, S, P);
+    if (t.G == 2 && t.C == 4) return launch_update_tr_t<2, 4, true>(h, grid, threads, smem, st, u, S, P);
+    if (t.G == 1) {
+        switch (t.C) {
+#define SS_CASE(K) \
+    case K: return launch_update_tr_t<1, K, true>(h, grid, threads, smem, st, u, S, P);
+            SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8)
+#undef SS_CASE
+            default: break;
+        }
+    }
+    return ss::set_err(h, SS_EARG, "unsupported update tile");
+}
+}  // namespace ss
+
+namespace {
+
 // widest window <= nb_req whose block RQ and update fit one SM's shared
 // memory (the update may read P from global memory, k_update<..., PG>);
 // 0 if none does (m too wide for this device)

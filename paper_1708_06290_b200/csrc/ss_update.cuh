@@ -66,6 +66,10 @@ struct UpdDims {
     int64_t pstride, p12off, p22off;
     int zid;
     int flags;  // experiment knobs (bit 0: producer spins instead of parking)
+    // transposed sweep (k_update<..., TR = true>, ss_lq.cu): the panel is
+    // [A^T; -I] (rows i < n: A(c0 + j, i), rows n + r: -[r == c0 + j]); the
+    // lazy -sigma rows are [lz0, lz0 + mnb) with P12 rows lzp + (i - lz0)
+    int lz0 = 0, lzp = 0;
 };
 
 __host__ __device__ inline size_t upd_smem_bytes(int nb, int m, int S, bool pg = false) {
@@ -86,7 +90,7 @@ __device__ __forceinline__ int pan_index(int row) {
 // PG: P_l is read from global memory (L1 / L2; every lane of a row group
 // reads the same entries) instead of being staged -- windows so wide
 // (m >~ 90) that the staged P does not fit shared memory.
-template <int G, int C, bool EXACT, int MAXT = 256, bool PG = false>
+template <int G, int C, bool EXACT, int MAXT = 256, bool PG = false, bool TR = false>
 __global__ void __launch_bounds__(MAXT)
     k_update(UpdDims u, const double2* __restrict__ Zin, double2* __restrict__ Zout,
              const double2* __restrict__ Pbuf) {
@@ -103,10 +107,16 @@ __global__ void __launch_bounds__(MAXT)
 
     // ---- panel tile (once per CTA) ----
     for (int v = tid; v < nb * kUpdRows; v += blockDim.x) {
-        const int j = v >> 6, rr = v & 63;
+        // transposed: consecutive threads along a row of A^T (= a column of
+        // A, contiguous) instead of down a column
+        const int j = TR ? v % nb : v >> 6, rr = TR ? v / nb : v & 63;
         const int i = i0 + rr, col = u.c0 + j;
         double* dst = Pan + j * kUpdRows + pan_index<G>(rr);
-        if (i >= r0) {
+        if (TR) {
+            if (i >= r0) *dst = 0.0;
+            else if (i < u.n) cp_async8(dst, u.A + col + (int64_t)i * u.lda, true);
+            else *dst = (i - u.n == col) ? -1.0 : 0.0;
+        } else if (i >= r0) {
             *dst = 0.0;
         } else if (i >= u.ptop) {
             cp_async8(dst, u.A + (i - u.ptop) + (int64_t)col * u.lda, true);
@@ -126,7 +136,8 @@ __global__ void __launch_bounds__(MAXT)
     const int cb = blk * (G * C) + q * C;                     // first output column of this lane
     const int ncol = EXACT ? C : max(0, min(C, m - cb));
     const int rbase = rg * R;                                 // first tile row of this lane
-    const int dlo = r0 - m;
+    const int dlo = TR ? u.lz0 : r0 - m;  // first lazy-shift row
+    const int dp = TR ? u.lzp : 0;         // its P12 row
     const int jlo = half == 0 ? 0 : u.jh;
     const int jhi = (u.ksplit == 1 || half == 1) ? nb : u.jh;
 
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(MAXT)
             for (int c = 0; c < C; ++c) {
                 if (EXACT || c < ncol) {
                     double2 v = acc[r][c];
-                    if (corr) v = csub(v, cmul(sig, Pl[dd * m + c]));
+                    if (corr) v = csub(v, cmul(sig, Pl[(dp + dd) * m + c]));
                     zo[(int64_t)c * u.LDZ + row] = v;
                 }
             }
