@@ -32,6 +32,12 @@ __device__ __forceinline__ void cpa8(double* s, const double* g, bool valid) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(valid ? 8 : 0));
 }
+// 16-byte copy of the pair (g[0], g[1]); `bytes` 16, 8 (second element past
+// the matrix edge: zero-filled) or 0
+__device__ __forceinline__ void cpa16(double* s, const double* g, int bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(bytes));
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -39,20 +45,20 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 // Operand tile of R rows (m or n) x BK: "row-contiguous" (global contiguous
 // along m/n): s[k][r], stride R + 4; "k-contiguous": s[r][k], stride BK + 4.
 // Both strides are 4 mod 16 doubles: fragment loads are conflict-free.
-template <int R, bool KC>
+template <int R, bool KC, int BK = kGBK>
 struct Tile {
-    static constexpr int STRIDE = KC ? kGBK + 4 : R + 4;
-    static constexpr int ELEMS = KC ? R * STRIDE : kGBK * STRIDE;
+    static constexpr int STRIDE = KC ? BK + 4 : R + 4;
+    static constexpr int ELEMS = KC ? R * STRIDE : BK * STRIDE;
     __device__ static __forceinline__ int idx(int r, int k) { return KC ? r * STRIDE + k : k * STRIDE + r; }
 };
 
-template <bool TA, bool TB, int MT, int NT, int WM, int WN>
+template <bool TA, bool TB, int MT, int NT, int WM, int WN, int BK_ = kGBK>
 struct GemmCfg {
-    static constexpr int BM = 16 * MT * WM, BN = 8 * NT * WN;
+    static constexpr int BM = 16 * MT * WM, BN = 8 * NT * WN, BK = BK_;
     // A (m, k): !TA -> A[m + k lda] m-contiguous; TA -> A[k + m lda] k-contiguous
-    using TA_ = Tile<BM, TA>;
+    using TA_ = Tile<BM, TA, BK>;
     // B (k, n): !TB -> B[k + n ldb] k-contiguous; TB -> B[n + k ldb] n-contiguous
-    using TB_ = Tile<BN, !TB>;
+    using TB_ = Tile<BN, !TB, BK>;
     static constexpr int STAGE = TA_::ELEMS + TB_::ELEMS;
     static constexpr size_t SMEM = (size_t)kGS * STAGE * 8;
 };
@@ -72,9 +78,12 @@ struct GemmArgs {
 
 // two CTAs per SM for warp tiles of <= 8 DMMA tiles (acc 32 doubles): one
 // CTA's epilogue / pipeline fill overlaps the other's DMMAs
-template <bool TA, bool TB, int MT, int NT, int WM, int WN>
+// V16: both operands' contiguous dimensions are 16-byte aligned (base
+// pointers and leading dimensions even): pairs of elements per cp.async
+// (half the copy instructions; the 8-byte path serves odd row offsets).
+template <bool TA, bool TB, int MT, int NT, int WM, int WN, bool V16 = false, int BK = kGBK>
 __global__ void __launch_bounds__(kGThreads, MT * NT <= 8 ? 2 : 1) k_dmma(GemmArgs g) {
-    using Cfg = GemmCfg<TA, TB, MT, NT, WM, WN>;
+    using Cfg = GemmCfg<TA, TB, MT, NT, WM, WN, BK>;
     constexpr int BM = Cfg::BM, BN = Cfg::BN;
     using TAt = typename Cfg::TA_;
     using TBt = typename Cfg::TB_;
@@ -83,7 +92,7 @@ __global__ void __launch_bounds__(kGThreads, MT * NT <= 8 ? 2 : 1) k_dmma(GemmAr
     const int gq = lane >> 2, tq = lane & 3;
     const int wm = (warp % WM) * 16 * MT, wn = (warp / WM) * 8 * NT;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int nkt_all = (g.K + kGBK - 1) / kGBK;
+    const int nkt_all = (g.K + BK - 1) / BK;
     const int split = blockIdx.z;
     const int kt0 = (int)((int64_t)nkt_all * split / g.ksplit), kt1 = (int)((int64_t)nkt_all * (split + 1) / g.ksplit);
     const int nkt = kt1 - kt0;
@@ -91,19 +100,41 @@ __global__ void __launch_bounds__(kGThreads, MT * NT <= 8 ? 2 : 1) k_dmma(GemmAr
     auto load = [&](int kt, int buf) {
         double* As = gsm + (size_t)buf * Cfg::STAGE;
         double* Bs = As + TAt::ELEMS;
-        const int k0 = kt * kGBK;
+        const int k0 = kt * BK;
+        if (V16) {
+            // pairs along each operand's contiguous dimension
+            for (int e = tid; e < BM * BK / 2; e += kGThreads) {
+                int r, k;
+                if (!TA) { r = 2 * (e % (BM / 2)); k = e / (BM / 2); } else { k = 2 * (e % (BK / 2)); r = e / (BK / 2); }
+                const int gm = m0 + r, gk = k0 + k;
+                const int lim = !TA ? g.M - gm : g.K - gk;   // elements left along the pair
+                const bool ok = (!TA ? gk < g.K : gm < g.M) && lim > 0;
+                const double* src = g.A + (ok ? (TA ? gk + (int64_t)gm * g.lda : gm + (int64_t)gk * g.lda) : 0);
+                cpa16(As + TAt::idx(r, k), src, ok ? (lim >= 2 ? 16 : 8) : 0);
+            }
+            for (int e = tid; e < BN * BK / 2; e += kGThreads) {
+                int r, k;
+                if (TB) { r = 2 * (e % (BN / 2)); k = e / (BN / 2); } else { k = 2 * (e % (BK / 2)); r = e / (BK / 2); }
+                const int gn = n0 + r, gk = k0 + k;
+                const int lim = TB ? g.N - gn : g.K - gk;
+                const bool ok = (TB ? gk < g.K : gn < g.N) && lim > 0;
+                const double* src = g.B + (ok ? (TB ? gn + (int64_t)gk * g.ldb : gk + (int64_t)gn * g.ldb) : 0);
+                cpa16(Bs + TBt::idx(r, k), src, ok ? (lim >= 2 ? 16 : 8) : 0);
+            }
+            return;
+        }
         // A tile: BM x BK
-        for (int e = tid; e < BM * kGBK; e += kGThreads) {
+        for (int e = tid; e < BM * BK; e += kGThreads) {
             int r, k;
-            if (!TA) { r = e % BM; k = e / BM; } else { k = e % kGBK; r = e / kGBK; }
+            if (!TA) { r = e % BM; k = e / BM; } else { k = e % BK; r = e / BK; }
             const int gm = m0 + r, gk = k0 + k;
             const bool ok = gm < g.M && gk < g.K;
             const double* src = g.A + (ok ? (TA ? gk + (int64_t)gm * g.lda : gm + (int64_t)gk * g.lda) : 0);
             cpa8(As + TAt::idx(r, k), src, ok);
         }
-        for (int e = tid; e < BN * kGBK; e += kGThreads) {
+        for (int e = tid; e < BN * BK; e += kGThreads) {
             int r, k;
-            if (TB) { r = e % BN; k = e / BN; } else { k = e % kGBK; r = e / kGBK; }
+            if (TB) { r = e % BN; k = e / BN; } else { k = e % BK; r = e / BK; }
             const int gn = n0 + r, gk = k0 + k;
             const bool ok = gn < g.N && gk < g.K;
             const double* src = g.B + (ok ? (TB ? gn + (int64_t)gk * g.ldb : gk + (int64_t)gn * g.ldb) : 0);
@@ -133,7 +164,7 @@ __global__ void __launch_bounds__(kGThreads, MT * NT <= 8 ? 2 : 1) k_dmma(GemmAr
         const double* As = gsm + (size_t)(it % kGS) * Cfg::STAGE;
         const double* Bs = As + TAt::ELEMS;
 #pragma unroll
-        for (int ks = 0; ks < kGBK; ks += 8) {
+        for (int ks = 0; ks < BK; ks += 8) {
             double af[MT][4], bf[NT][2];
 #pragma unroll
             for (int i = 0; i < MT; ++i) {

@@ -18,14 +18,14 @@ from paper_1708_06290_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 
-def run(ta, tb, M, N, K, alpha, beta, off=0, pad=0, seed=0):
+def run(ta, tb, M, N, K, alpha, beta, off=0, pad=0, seed=0, pad_fn=None):
     g = torch.Generator(device="cuda").manual_seed(seed)
     dev = torch.device("cuda", 0)
     ra, ca = (K, M) if ta else (M, K)
     rb, cb = (N, K) if tb else (K, N)
 
     def mat(r, c):  # column-major with an odd leading dimension and an offset start
-        ld = r + off + pad
+        ld = r + off + (pad if pad_fn is None else pad_fn(r + off))
         buf = torch.randn(ld * c + off + 8, dtype=torch.float64, device=dev, generator=g)
         return buf, ld
 
@@ -85,3 +85,17 @@ def test_dgemm_deterministic():
         outs.append(C.clone())
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("ta", [0, 1])
+@pytest.mark.parametrize("tb", [0, 1])
+@pytest.mark.parametrize("M,N,K", [(301, 7, 257), (516, 30, 96), (1000, 51, 64), (41, 700, 333),
+                                   (1100, 901, 64), (64, 1500, 2001), (3001, 1, 3000)])
+def test_dgemm_aligned_path(ta, tb, M, N, K):
+    """Even leading dimensions and 16-byte aligned bases take the paired
+    16-byte copies (odd extents end in a half-filled pair)."""
+    def pad_even(r):  # leading dimension r + pad made even
+        return 0 if r % 2 == 0 else 1
+    err = run(ta, tb, M, N, K, alpha=-1.0, beta=1.0, off=0, pad=0, seed=M * 3 + N + K,
+              pad_fn=pad_even)
+    assert err <= 1e-13
