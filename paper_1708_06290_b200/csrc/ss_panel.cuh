@@ -48,16 +48,24 @@ struct Pan {
     int yext;      // band panel (1): right updates from Y; B's QR (0)
     int vrow0;     // V row of column j's right update: j + vrow0 (= j - m)
     double* V;     // nk x bw, ld ldv (zero above the diagonal)
-    const double* Y;  // nk x bw, ld ldv
+    double* Y;     // nk x bw, ld ldv
     int64_t ldv;
     double* T;     // bw x bw, ld ldt: columns < js in, [js, jb) out
     int64_t ldt;
     double* ws;    // scratch: pan_ws_doubles(G)
+    // small m (mini-blocks of <= kPYin columns): the Y extension runs inside
+    // the kernel (tr = A0[kb:, kb:], ld lda) and one launch covers the panel
+    const double* tr;
+    int yin;
 };
+constexpr int kPYin = 4;
 
-__host__ __device__ inline size_t pan_ws_doubles(int G) { return (size_t)G * kPBmax * 2 + (size_t)G + 8; }
+__host__ __device__ inline size_t pan_ws_doubles(int G) {
+    return (size_t)G * kPBmax * 2 + (size_t)G + 8 + (size_t)G * kPBmax * kPYin;  // + V^T V partials
+}
 __host__ __device__ inline size_t pan_smem_bytes(int bw, int G, int nown_staged) {
-    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (size_t)kPTC * G + (size_t)2 * nown_staged * bw) * 8;
+    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (size_t)kPTC * G + (size_t)kPBmax * kPYin +
+            (size_t)(kPT / 32) * 32 * kPYin + (size_t)2 * nown_staged * bw) * 8;
 }
 
 // The CTA's own rows of V and Y, staged in shared memory when they fit
@@ -139,6 +147,104 @@ __device__ __forceinline__ void s1_right(const Pan& p, const Own& o, double* vrs
     own_vdots(o, rlo, rhi, a, j, ppart_c, G);
 }
 
+// Y[:, ms:me] = (A0 V[:, ms:me] - Y[:, :ms] (V[:, :ms]^T V[:, ms:me])) T[ms:me, ms:me]
+// for the own rows (hessenberg.py:83-96 mini_boundaries; me - ms <= kPYin):
+// V^T V across CTAs (partials, one grid barrier, gathered sums), A0 V with
+// the warps splitting the trailing columns and lanes on rows (a fixed-order
+// combine in shared memory), the rest row-local.
+__device__ void yext_inline(const Pan& p, const Own& o, int ms, int me, int rlo, int rhi, int G, const double* Ts,
+                            int bw, double* vpart, double* vtv, double* avs, double* pbuf) {
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cta = blockIdx.x;
+    const int cw = me - ms, ne = ms * cw;
+    // (1) V^T V partials: entry e = t + u ms (t < ms, u < cw), stored [e][G]
+    for (int e = warp; e < ne; e += kPT / 32) {
+        const int t = e % ms, u = e / ms;
+        const double* vt = o.v + (int64_t)t * o.ld - o.off;
+        const double* vu = o.v + (int64_t)(ms + u) * o.ld - o.off;
+        double s = 0.0;
+        for (int i = rlo + lane; i < rhi; i += 32) s = fma(vt[i], vu[i], s);
+#pragma unroll
+        for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+        if (lane == 0) vpart[(size_t)e * G + cta] = s;
+    }
+    // (2) A0 V for the own rows, 8 rows at a time: every thread takes trailing
+    // columns c = tid, tid + 256, ... (the 8 rows of a column are contiguous:
+    // two sectors, and every lane's loads are independent -- the CTA's slice
+    // of A0 streams at L2 bandwidth instead of one latency per column), then
+    // a fixed shuffle tree over the lanes and a fixed-order sum over warps
+    const int ncol = p.nk - ms;
+    for (int r0 = rlo; r0 < rhi; r0 += 8) {
+        const int nr = min(8, rhi - r0);
+        double acc[8][kPYin];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int u = 0; u < kPYin; ++u) acc[r][u] = 0.0;
+        for (int c = tid; c < ncol; c += kPT) {
+            double vv[kPYin];
+#pragma unroll
+            for (int u = 0; u < kPYin; ++u) vv[u] = u < cw ? p.V[(ms + c) + (int64_t)(ms + u) * p.ldv] : 0.0;
+            const double* col = p.tr + r0 + (int64_t)(ms + c) * p.lda;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if (r < nr) {
+                    const double av = col[r];
+#pragma unroll
+                    for (int u = 0; u < kPYin; ++u) acc[r][u] = fma(av, vv[u], acc[r][u]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int u = 0; u < kPYin; ++u) {
+                double v = acc[r][u];
+#pragma unroll
+                for (int q = 16; q > 0; q >>= 1) v += __shfl_xor_sync(0xffffffffu, v, q);
+                if (lane == 0) avs[(warp * 8 + r) * kPYin + u] = v;
+            }
+        __syncthreads();
+        if (tid < nr * cw) {
+            const int r = tid / cw, u = tid - (tid / cw) * cw;
+            double v = 0.0;
+            for (int w = 0; w < kPT / 32; ++w) v += avs[(w * 8 + r) * kPYin + u];
+            p.Y[r0 + r + (int64_t)(ms + u) * p.ldv] = v;  // A0 V, before the corrections
+        }
+        __syncthreads();
+    }
+    grid.sync();
+    if (ne > 0) {
+        cta_sums(vpart, G, ne, vtv, pbuf);
+        __syncthreads();
+    }
+    // (3) own rows: (A0 V - Y VtV) T, written to Y (and the staged copy)
+    for (int i = rlo + tid; i < rhi; i += kPT) {
+        double z[kPYin];
+#pragma unroll
+        for (int u = 0; u < kPYin; ++u) {
+            z[u] = 0.0;
+            if (u < cw) {
+                double v = p.Y[i + (int64_t)(ms + u) * p.ldv];
+                for (int t = 0; t < ms; ++t) v = fma(-o.y[(i - o.off) + (int64_t)t * o.ld], vtv[t + u * ms], v);
+                z[u] = v;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPYin; ++u) {
+            if (u < cw) {
+                double y = 0.0;
+#pragma unroll
+                for (int k = 0; k < kPYin; ++k)
+                    if (k <= u) y = fma(z[k], Ts[(ms + k) + (ms + u) * bw], y);
+                p.Y[i + (int64_t)(ms + u) * p.ldv] = y;
+                if (o.y != p.Y) const_cast<double*>(o.y)[(i - o.off) + (int64_t)(ms + u) * o.ld] = y;
+            }
+        }
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int stage) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
@@ -150,6 +256,8 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     double* sc = red + kPT / 32;   // [8] tau, beta, scale
     double* vrs = sc + 8;          // [kPBmax] V row of the right update
     double* pbuf = vrs + kPBmax;   // [kPTC * G] cross-CTA partials (cta_sums)
+    double* vtv = pbuf + (size_t)kPTC * gridDim.x;  // [kPBmax * kPYin] V^T V of the Y extension
+    double* avs = vtv + kPBmax * kPYin;             // [8 warps][32 rows][kPYin] A0 V partials
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
     const int rlo = (int)((int64_t)nk * cta / G), rhi = (int)((int64_t)nk * (cta + 1) / G);
     const int nown = rhi - rlo;
@@ -158,7 +266,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     if (stage) {
         // own rows of V (columns < jb; column j written here as it is formed)
         // and Y (columns < js, read-only in this kernel)
-        Vs = pbuf + (size_t)kPTC * gridDim.x;
+        Vs = avs + (kPT / 32) * 32 * kPYin;
         double* Ys = Vs + (size_t)nown * bw;
         for (int e = tid; e < nown * jb; e += kPT) {
             const int r = e % nown, t = e / nown;
@@ -175,13 +283,15 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     double* qpart = ppart + (size_t)G * kPBmax;  // [kPBmax][G]
     double* spart = qpart + (size_t)G * kPBmax;  // [G]
     double* scal = spart + G;                    // [8]: alpha
+    double* vpart = scal + 8;                    // [kPBmax * kPYin][G] V^T V partials
     // T columns of the earlier mini-blocks (upper triangle)
     for (int e = tid; e < bw * bw; e += kPT) {
         const int r = e % bw, c = e / bw;
         Ts[e] = (c < js && r <= c) ? p.T[r + (int64_t)c * p.ldt] : 0.0;
     }
     __syncthreads();
-    s1_right(p, o, vrs, js, js, rlo, rhi, ppart + cta, G);
+    int ms = js;  // first column of the current mini-block
+    s1_right(p, o, vrs, js, ms, rlo, rhi, ppart + cta, G);
     grid.sync();
     for (int j = js; j < jb; ++j) {
         double* a = p.a0 + (int64_t)j * p.lda;
@@ -255,7 +365,9 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
         }
         __syncthreads();
         own_vdots(o, rlo, rhi, vj, j, qpart + cta, G);
-        if (j + 1 < jb) s1_right(p, o, vrs, j + 1, js, rlo, rhi, ppart + cta, G);
+        // in-kernel Y extension: a mini-block ends at this column
+        const bool ybnd = p.yin && ((j + 1 - ms) == p.m || j + 1 == jb);
+        if (j + 1 < jb && !ybnd) s1_right(p, o, vrs, j + 1, ms, rlo, rhi, ppart + cta, G);
         grid.sync();
         // ---- T column (kernels.py:156-160; every CTA, same order) ----
         cta_sums(qpart, G, j, d, pbuf);
@@ -267,6 +379,15 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
         }
         if (tid == 0) Ts[j + j * bw] = tau;
         __syncthreads();
+        if (ybnd) {
+            yext_inline(p, o, ms, j + 1, rlo, rhi, G, Ts, bw, vpart, vtv, avs, pbuf);
+            ms = j + 1;
+            if (j + 1 < jb) {
+                __syncthreads();
+                s1_right(p, o, vrs, j + 1, ms, rlo, rhi, ppart + cta, G);
+                grid.sync();
+            }
+        }
     }
     if (cta == 0)
         for (int e = tid; e < bw * (jb - js); e += kPT) {

@@ -284,6 +284,8 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
         pp.T = T;
         pp.ldt = ldt;
         pp.ws = pws;
+        pp.tr = nullptr;
+        pp.yin = 0;
         SS_TRY(panel_cols(x, pp, 0, kB));
     }
     // Bhat[m:, :] = 0 exactly (hessenberg.py:315) and the columns past kB
@@ -318,8 +320,14 @@ extern "C" int ss_reduce_chf(ss_handle* h, int n, int m, int p, double* A, int64
         pp.T = T;
         pp.ldt = ldt;
         pp.ws = pws;
+        pp.tr = A + kb + (int64_t)kb * lda;
+        pp.yin = m <= ssr::kPYin ? 1 : 0;
+        if (pp.yin) {
+            // small m: the Y extension inside the panel kernel, one launch per panel
+            SS_TRY(panel_cols(x, pp, 0, bw));
+        }
         int js = 0;  // first reflector of the current mini-block
-        for (int j = 0; j < bw; ++j) {
+        for (int j = 0; j < bw && !pp.yin; ++j) {
             const int jb = j + 1;
             if (jb % m == 0 || jb == bw) {
                 // panel columns [js, jb) (right update from the complete
