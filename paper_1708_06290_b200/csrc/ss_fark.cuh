@@ -57,7 +57,31 @@ struct FarKDims {
     int nk, jz, nz, ntiles;
     int spl;  // CTAs per team (grid is a multiple of spl)
     const double* pan;  // packed panel [ntiles][nk][KC][64]
+    // lazy -sigma rows: [lz0, lz0 + mnb) take W12 rows lzp + (i - lz0).
+    // lzset = 0: the forward sweep's rows r0 - m .. r0 - 1 with W12 rows 0 .. m-1
+    // (lz0 = r0 - M, lzp = 0); the transposed sweep sets them (its diagonal
+    // entries sit at the top of the far rows, in the composite's last columns)
+    int lz0 = 0, lzp = 0, lzset = 0;
+    int n = 0;  // k_pack_panel_tr: rows >= n are the -I block
 };
+
+// The transposed sweep's panel [A^T; -I]: rows i < n are A(c, i) (row i of
+// A^T; contiguous along c, so threads run along the 32 columns of a chunk),
+// rows n + r are -[r == c]; zero outside [rlo, r0) x [c0, c0 + K).
+__global__ void __launch_bounds__(256) k_pack_panel_tr(FarKDims u, double* __restrict__ pan) {
+    const int tile = blockIdx.x / u.nk, kc = blockIdx.x - tile * u.nk;
+    double* dst = pan + (size_t)blockIdx.x * kFkKC * kFkTile;
+    for (int e = threadIdx.x; e < kFkKC * kFkTile; e += blockDim.x) {
+        const int j = e % kFkKC, rr = e / kFkKC;
+        const int i = u.rlo + tile * kFkTile + rr, jc = kc * kFkKC + j, col = u.c0 + jc;
+        double v = 0.0;
+        if (i < u.r0 && jc < u.K) {
+            if (i < u.n) v = u.A[col + (int64_t)i * u.lda];
+            else v = (i - u.n == col) ? -1.0 : 0.0;
+        }
+        dst[j * kFkTile + far_pan_index<2>(rr)] = v;
+    }
+}
 
 template <int NCB, int S>
 __host__ __device__ constexpr size_t fark_stage_bytes() {
@@ -175,7 +199,8 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
     const int cw = warp - 1, sw = cw / NCB, cbk = cw - sw * NCB;
     const int rg = lane >> 1, q = lane & 1;
     const int cb = cbk * 10 + q * C;  // first output column of this lane
-    const int dlo = r0 - M;
+    const int dlo = u.lzset ? u.lz0 : r0 - M;  // first lazy row
+    const int dp = u.lzset ? u.lzp : 0;         // its W12 row
     int g = 0;
     for (int k = 0; k < nun; ++k) {
         const int64_t unit = ua + (int64_t)k * spl;
@@ -184,7 +209,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
         const int64_t l = valid ? l0 + sw : 0;
         const int i0 = u.rlo + tile * TILE;
         // boundary tile: rows r0 - m + dd (dd < mnb) carry the lazy shift
-        const bool interior = i0 + TILE <= (u.mnb > 0 ? dlo : r0);
+        const bool interior = u.mnb == 0 || i0 + TILE <= dlo || i0 >= dlo + u.mnb;
         const double2 sig = interior ? cz() : u.shifts[l];
         double2 acc[R][C];
 #pragma unroll
@@ -215,17 +240,16 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                     const int kc = ch - nz, kcols = min(KC, K - kc * KC);
                     const double* pan = reinterpret_cast<const double*>(st) + rg * 2;
                     const double2* ws = reinterpret_cast<const double2*>(st + PANB) + (size_t)sw * KC * M + cb;
-                    if (!interior && kc * KC < u.mnb) {
-                        // acc -= sigma W12[dd, :] for the lazy rows whose W12 row is
-                        // in this chunk (m > KC: they span two chunks)
-                        const int dhi = min(u.mnb, kc * KC + kcols);
+                    if (!interior && dp < kc * KC + kcols && dp + u.mnb > kc * KC) {
+                        // acc -= sigma W12[dp + dd, :] for the lazy rows whose W12 row
+                        // is in this chunk (they may span two chunks)
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
                             const int dd = i0 + rg + RG * r - dlo;
-                            if (dd >= kc * KC && dd < dhi) {
+                            const int wr = dp + dd - kc * KC;  // chunk-local W12 row
+                            if (dd >= 0 && dd < u.mnb && wr >= 0 && wr < kcols) {
 #pragma unroll
-                                for (int c = 0; c < C; ++c)
-                                    acc[r][c] = csub(acc[r][c], cmul(sig, ws[(dd - kc * KC) * M + c]));
+                                for (int c = 0; c < C; ++c) acc[r][c] = csub(acc[r][c], cmul(sig, ws[wr * M + c]));
                             }
                         }
                     }

@@ -43,16 +43,25 @@
 using namespace ssd;
 
 namespace ss {
-// ss_sweep.cu: the window-update kernel on the [A^T; -I] panel
+// ss_sweep.cu: the window-update kernel on the [A^T; -I] panel, and the
+// composite fold / K-streamed far pass
 int launch_update_tr(ss_handle* h, ssd::UpdDims u, int rows, double2* S, const double2* P, cudaStream_t st);
+int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool first, int sb, const double2* P,
+            double2* W, int64_t wstride);
+bool tr_far_supported(ss_handle* h, int M);
+int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, int64_t lda,
+           const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0, int c0, int K,
+           const double2* W, int64_t wstride);
 }
 
 namespace {
 
 constexpr int kLqMaxNb = 32;
+constexpr int kTrK = 512;  // panel columns per transposed composite (the packed panel's capacity)
 
 struct TDims {
     int n, m, mp;  // mp = m + 1 state columns per shift
+    int ms;        // columns per shift in S and P: mp, or mp padded to a multiple of 10 (composites)
     const double* A;
     int64_t lda;
     const double2* shifts;  // batch-local
@@ -71,7 +80,8 @@ __global__ void k_tseed(TDims d, const double2* __restrict__ rhs, int64_t ldr,
     const int l = blockIdx.y;
     if (i >= d.LDS) return;
     const double2 sig = d.shifts[l];
-    double2* Sl = S + (int64_t)l * d.mp * d.LDS;
+    double2* Sl = S + (int64_t)l * d.ms * d.LDS;
+    for (int c = d.mp; c < d.ms; ++c) Sl[(int64_t)c * d.LDS + i] = cz();  // padding columns
     for (int c = 0; c < d.m; ++c) {
         double2 v = cz();
         if (i < d.n) {
@@ -110,9 +120,13 @@ __global__ void __launch_bounds__(32) k_lq(TDims d, LqStep st, const double2* __
     const int lane = threadIdx.x;
     const int m = d.m, L = m + 1, nb = st.nb, mp = d.mp;
     const double2 sig = d.shifts[l];
-    const double2* Sl = S + (int64_t)l * mp * d.LDS;
-    double2* Po = Pout + (int64_t)l * (nb + mp) * mp;
+    const int ms = d.ms;
+    const double2* Sl = S + (int64_t)l * ms * d.LDS;
+    double2* Po = Pout + (int64_t)l * (nb + ms) * ms;
     if (d.fail[l] >= 0) return;  // failed in an earlier window: left as is (NaN at the end)
+    // padding of a widened P (composites): zero rows nb + mp .. and columns mp ..
+    for (int e = lane; e < (nb + ms) * (ms - mp); e += 32) Po[(int64_t)(e / (ms - mp)) * ms + mp + e % (ms - mp)] = cz();
+    for (int e = lane; e < (ms - mp) * mp; e += 32) Po[(int64_t)(nb + mp + e / mp) * ms + e % mp] = cz();
     const bool mine = lane < nb;
     const int row = st.k0 + lane;  // A^T row / stacked row of this lane
     // window of row `lane` at step 0: columns 0..m = [z2 row | panel col 0]
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(32) k_lq(TDims d, LqStep st, const double2* __
                     if (j == m) v = w[j];
                 if (q == m) v = make_double2(-v.x, -v.y);
                 const int prow = e < m ? nb + e : e - m;  // Pout row of block column e
-                Po[(int64_t)prow * mp + q] = v;
+                Po[(int64_t)prow * ms + q] = v;
             }
 #pragma unroll
             for (int j = LMAX - 1; j > 0; --j) w[j] = w[j - 1];
@@ -253,11 +267,11 @@ __global__ void __launch_bounds__(32) k_lq(TDims d, LqStep st, const double2* __
                 double2 v = w[j];
                 if (q == m) v = make_double2(-v.x, -v.y);
                 const int prow = e < m ? nb + e : e - m;
-                Po[(int64_t)prow * mp + q] = v;
+                Po[(int64_t)prow * ms + q] = v;
             }
         }
         // w row: identity on the w column
-        Po[(int64_t)(nb + m) * mp + q] = make_double2(q == m ? 1.0 : 0.0, 0.0);
+        Po[(int64_t)(nb + m) * ms + q] = make_double2(q == m ? 1.0 : 0.0, 0.0);
     }
 }
 
@@ -300,8 +314,9 @@ __global__ void __launch_bounds__(kLqBigThreads) k_lq_big(TDims d, LqStep st, co
     const int l = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (d.fail[l] >= 0) return;  // failed in an earlier window: left as is (NaN at the end)
     const double2 sig = d.shifts[l];
-    const double2* Sl = S + (int64_t)l * mp * d.LDS;
-    double2* Po = Pout + (int64_t)l * (nb + mp) * mp;
+    const int ms = d.ms;
+    const double2* Sl = S + (int64_t)l * ms * d.LDS;
+    double2* Po = Pout + (int64_t)l * (nb + ms) * ms;
     // stage the block rows: state columns (coalesced along rows), then the
     // panel of A^T (coalesced along columns: A^T(row, c) = A[c + row lda])
     for (int v = tid; v < nb * m; v += blockDim.x) {
@@ -314,6 +329,10 @@ __global__ void __launch_bounds__(kLqBigThreads) k_lq_big(TDims d, LqStep st, co
         if (i == m + j) x = csub(x, sig);  // block diagonal (lazy shift), solvers.py:398-400
         R[i * RS + m + j] = x;
     }
+    // padding of a widened P (composites): zero rows nb + mp .. and columns mp ..
+    for (int e = tid; e < (nb + ms) * (ms - mp); e += blockDim.x)
+        Po[(int64_t)(e / (ms - mp)) * ms + mp + e % (ms - mp)] = cz();
+    for (int e = tid; e < (ms - mp) * mp; e += blockDim.x) Po[(int64_t)(nb + mp + e / mp) * ms + e % mp] = cz();
     __syncthreads();
     if (warp == 0) {
         const bool mine = lane < nb;
@@ -424,7 +443,7 @@ __global__ void __launch_bounds__(kLqBigThreads) k_lq_big(TDims d, LqStep st, co
             // entry t + m (block column e = t + m >= m: Pout row t) is final
             if (act && base <= m && m < base + HW) {
                 if (q == m) fin = make_double2(-fin.x, -fin.y);
-                Po[(int64_t)t * mp + q] = fin;
+                Po[(int64_t)t * ms + q] = fin;
             }
             // slide right by one across the group
             const double nx = __shfl_up_sync(gmask, w[HW - 1].x, 1);
@@ -441,10 +460,10 @@ __global__ void __launch_bounds__(kLqBigThreads) k_lq_big(TDims d, LqStep st, co
                 if (j >= 1 && j <= m) {
                     double2 v = w[k];
                     if (q == m) v = make_double2(-v.x, -v.y);
-                    Po[(int64_t)(nb + j - 1) * mp + q] = v;
+                    Po[(int64_t)(nb + j - 1) * ms + q] = v;
                 }
             }
-            if (gi == 0) Po[(int64_t)(nb + m) * mp + q] = make_double2(q == m ? 1.0 : 0.0, 0.0);
+            if (gi == 0) Po[(int64_t)(nb + m) * ms + q] = make_double2(q == m ? 1.0 : 0.0, 0.0);
         }
     }
 }
@@ -534,8 +553,8 @@ __global__ void __launch_bounds__(256) k_ttail(TDims d, double2* __restrict__ S,
     __shared__ double2 s_s, s_r, s_w;
     __shared__ int s_fail;
     const int l = blockIdx.x, tid = threadIdx.x;
-    const int n = d.n, m = d.m, mp = d.mp;
-    double2* Sl = S + (int64_t)l * mp * d.LDS;
+    const int n = d.n, m = d.m;
+    double2* Sl = S + (int64_t)l * d.ms * d.LDS;
     double2* wv = Sl + (int64_t)m * d.LDS;
     const int lo = n - m, hi = 2 * n;
     if (tid == 0) s_fail = d.fail[l];
@@ -701,7 +720,16 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
         int rc = ss::fro2_trace(h, n, Ahat, lda, st);
         if (rc) return rc;
     }
-    const size_t per_shift = (size_t)LDS * mp * 16 + (size_t)(nb0 + mp) * mp * 16 + 8 + 64;
+    // Composites (as the forward sweep's window composites): up to kTrK
+    // columns of windows, the rows below them updated ONCE by the K-streamed
+    // far kernel; the state is padded to M = 10 ceil(mp / 10) columns for its
+    // register tiles (zero columns stay zero: P and W are zero there)
+    const int M = 10 * ((mp + 9) / 10);
+    const bool comp = M <= 60 && ss::tr_far_supported(h, M) && n - m > 2 * nb0;
+    const int ms = comp ? M : mp;
+    const int G = std::max(1, std::min(64, kTrK / nb0)), Kmax = G * nb0;
+    const int64_t wstride = comp ? (int64_t)(Kmax + M) * M : 0;
+    const size_t per_shift = (size_t)LDS * ms * 16 + (size_t)(nb0 + ms) * ms * 16 + (size_t)wstride * 16 + 8 + 64;
     int64_t sb_max = std::min<int64_t>(batch > 0 ? batch : s, s);
     if (per_shift * (size_t)sb_max + 256 > h->ws_bytes) {  // query only to grow (slow driver call)
         size_t fr = 0, tot = 0;
@@ -715,8 +743,9 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
         if (rc) return rc;
     }
     double2* Sb = (double2*)h->ws;
-    double2* Pb = Sb + (size_t)sb_max * mp * LDS;
-    double* tolb = (double*)(Pb + (size_t)sb_max * (nb0 + mp) * mp);
+    double2* Pb = Sb + (size_t)sb_max * ms * LDS;
+    double2* Wb = Pb + (size_t)sb_max * (nb0 + ms) * ms;
+    double* tolb = (double*)(Wb + (size_t)sb_max * wstride);
     static ss::DevMask attrs;  // devices configured
     if (!attrs.has(h)) {
         SS_CUDA_TRY(h, allow_smem(h, k_tupd<128, true>));
@@ -734,6 +763,7 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
         d.n = n;
         d.m = m;
         d.mp = mp;
+        d.ms = ms;
         d.A = Ahat;
         d.lda = lda;
         d.shifts = (const double2*)shifts + lo;
@@ -748,7 +778,67 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
             k_tseed<<<g, 256, 0, st>>>(d, (const double2*)rhs + lo * ldr, ldr, Sb);
             SS_LAUNCH_CHECK(h);
         }
-        for (int k0 = 0; k0 < n - m;) {
+        for (int k0 = 0; comp && k0 < n - m;) {
+            // ---- one composite: windows top-down, near rows, fold; far pass ----
+            int k0w[64], nbw[64], g = 0;
+            for (int kk = k0; kk < n - m && g < G; ++g) {
+                k0w[g] = kk;
+                nbw[g] = std::min(nb0, n - m - kk);
+                kk += nbw[g];
+            }
+            const int c0 = k0 + m;                       // first panel column
+            const int kend = k0w[g - 1] + nbw[g - 1];    // first far row
+            const int K = kend - k0;                     // panel columns of the composite
+            for (int b = 0; b < g; ++b) {
+                LqStep ls;
+                ls.k0 = k0w[b];
+                ls.nb = nbw[b];
+                ls.c0 = k0w[b] + m;
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                int rc = launch_lq(h, m, sb, st, d, ls, Sb, Pb);
+                if (rc) return rc;
+                ss::timing_end(h, st, ev, ss::PH_RQ);
+                const int rows = kend - (ls.k0 + ls.nb);  // near: the composite's rows below this window
+                if (rows > 0) {
+                    UpdDims u;
+                    u.n = n;
+                    u.m = M;
+                    u.ptop = 0;
+                    u.ident_top = 0;
+                    u.A = Ahat;
+                    u.lda = lda;
+                    u.T = nullptr;
+                    u.ldt = 0;
+                    u.shifts = d.shifts;
+                    u.sb = sb;
+                    u.LDZ = LDS;
+                    u.nb = ls.nb;
+                    u.mnb = std::min(m, ls.nb);
+                    u.r0 = kend;
+                    u.c0 = ls.c0;
+                    u.nc = ls.nb + M;
+                    u.rlo = ls.k0 + ls.nb;
+                    u.lz0 = ls.k0 + ls.nb + (m - u.mnb);
+                    u.lzp = ls.nb - u.mnb;
+                    ev = ss::timing_begin(h, st);
+                    rc = ss::launch_update_tr(h, u, rows, Sb, Pb, st);
+                    if (rc) return rc;
+                    ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * M * M * (double)sb,
+                                   8.0 * rows * (double)sb * M * ls.nb, 4.0 * mp * (double)rows * ls.nb * sb);
+                }
+                ev = ss::timing_begin(h, st);
+                rc = ss::tr_fold(h, st, M, K, ls.k0 - k0, ls.nb, b == 0, sb, Pb, Wb, wstride);
+                if (rc) return rc;
+                ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
+            }
+            // far rows: the rest of A^T's rows and the -I rows up to the
+            // composite's last column
+            const int rend = std::min(2 * n, n + c0 + K);
+            int rc = ss::tr_far(h, st, n, m, M, Ahat, lda, d.shifts, sb, Sb, LDS, kend, rend, c0, K, Wb, wstride);
+            if (rc) return rc;
+            k0 = kend;
+        }
+        for (int k0 = 0; !comp && k0 < n - m;) {
             LqStep ls;
             ls.k0 = k0;
             ls.nb = std::min(nb0, n - m - k0);

@@ -857,7 +857,7 @@ struct WcLayout {
 // W22 <- P22).  grid (sb, row chunks).
 __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool first, int64_t pstride,
                                                const double2* __restrict__ P, WcLayout lw,
-                                               double2* __restrict__ W) {
+                                               double2* __restrict__ W, int ra, int rb) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2* P22 = reinterpret_cast<double2*>(smem);  // m x m
     double2* Wr = P22 + m * m;                        // [kWcRows][m]
@@ -865,7 +865,11 @@ __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool
     const double2* Pl = P + (int64_t)l * pstride;
     double2* Wl = W + lw.off(l);
     const int64_t rs = lw.rs;
-    const int r0 = x + nb, nrows = K + m - r0;  // rows multiplied by P22
+    // rows multiplied by P22: the earlier windows' W12 rows [ra, rb) (below
+    // the window in the forward sweep, above it in the transposed one), then
+    // W22 (rows [K, K + m))
+    const int n1 = rb - ra, nrows = n1 + m;
+    auto wrow = [&](int q) { return q < n1 ? ra + q : K + (q - n1); };
     const int c0 = blockIdx.y * kWcRows;
     if (blockIdx.y == 0)
         for (int e = tid; e < nb * m; e += blockDim.x) Wl[(int64_t)(x + e / m) * rs + e % m] = Pl[e];
@@ -878,7 +882,7 @@ __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool
     if (c0 >= nrows) return;
     const int rc = min(kWcRows, nrows - c0);
     for (int e = tid; e < m * m; e += blockDim.x) P22[e] = Pl[(int64_t)nb * m + e];
-    for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)(r0 + c0 + e / m) * rs + e % m];
+    for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)wrow(c0 + e / m) * rs + e % m];
     __syncthreads();
     for (int e = tid; e < rc * m; e += blockDim.x) {
         const int r = e / m, c = e - r * m;
@@ -890,7 +894,7 @@ __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool
             a1 = cfma(wr[j + 1], P22[(j + 1) * m + c], a1);
         }
         if (j < m) a0 = cfma(wr[j], P22[j * m + c], a0);
-        Wl[(int64_t)(r0 + c0 + r) * rs + c] = cadd(a0, a1);
+        Wl[(int64_t)wrow(c0 + r) * rs + c] = cadd(a0, a1);
     }
 }
 
@@ -1371,7 +1375,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 } else {
                     dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
                     k_wcomp<<<gc, 256, wcomp_smem(m), st>>>(m, K, cw - c0, nb, b == 0, (int64_t)nc * m, B.P,
-                                                            lw, B.W);
+                                                            lw, B.W, cw - c0 + nb, K);
                 }
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
@@ -2069,6 +2073,117 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
 }
 
 }  // namespace
+
+namespace ss {
+// ---- transposed-sweep composites (ss_lq.cu): fold and far pass ----------
+// Fold window P ((nb + M) x M per shift, M = padded state width) into the
+// composite W ((K + M) x M per shift): W12[x, x + nb) <- P12, W12[0, x) and
+// W22 <- . P22 (the earlier windows sit ABOVE in the top-down sweep).
+int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool first, int sb, const double2* P,
+            double2* W, int64_t wstride) {
+    static ss::DevMask configured;
+    if (!configured.has(h)) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_wcomp));
+        configured.set(h);
+    }
+    const WcLayout lw{1, wstride, 0, M};
+    const int nrows = x + M;
+    dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
+    k_wcomp<<<gc, 256, wcomp_smem(M), st>>>(M, K, x, nb, first, (int64_t)(nb + M) * M, P, lw, W, 0, x);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
+
+// state widths the composite far pass supports (M = 10 NCB)
+bool tr_far_supported(ss_handle* h, int M) {
+    switch (M) {
+        case 10: return fark_smem_bytes<1, 8, kFarkStages>() <= h->smem_optin;
+        case 20: return fark_smem_bytes<2, 4, kFarkStages>() <= h->smem_optin;
+        case 30: return fark_smem_bytes<3, 3, 3>() <= h->smem_optin;
+        case 40: case 50: case 60: return wc_far_smem(M) <= h->smem_optin;
+        default: return false;
+    }
+}
+
+// Far rows [rlo, r0) of the transposed sweep from the composite over panel
+// columns [c0, c0 + K) of [A^T; -I]: one K-streamed k_fark pass (packed panel
+// from k_pack_panel_tr); the lazy -sigma rows are the first min(m, K) far
+// rows (the composite's last columns' diagonal).
+int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, int64_t lda,
+           const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0, int c0, int K,
+           const double2* W, int64_t wstride) {
+    const int rows = r0 - rlo;
+    if (rows <= 0) return SS_OK;
+    {
+        int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(2 * n, 0), 1);
+        if (rc) return rc;
+    }
+    double* pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
+    FarKDims fk;
+    fk.m = M;
+    fk.ptop = 0;
+    fk.ident_top = 0;
+    fk.A = A;
+    fk.lda = lda;
+    fk.T = nullptr;
+    fk.ldt = 0;
+    fk.shifts = shifts;
+    fk.sb = sb;
+    fk.LDZ = LDS;
+    fk.r0 = r0;
+    fk.rlo = rlo;
+    fk.c0 = c0;
+    fk.K = K;
+    // diagonal entries (c, c) of the composite's columns that fall in the far rows
+    fk.lz0 = std::max(rlo, c0);
+    fk.lzp = fk.lz0 - c0;
+    fk.mnb = std::max(0, c0 + K - fk.lz0);
+    fk.lzset = 1;
+    fk.n = n;
+    fk.wstride = wstride;
+    fk.woff = 0;
+    fk.nk = (K + kFkKC - 1) / kFkKC;
+    fk.ntiles = (rows + kFkTile - 1) / kFkTile;
+    fk.pan = pan;
+    int S_ = 1;
+    switch (M) {
+        case 10: fk.jz = fark_jz<1, 8>(); S_ = 8; break;
+        case 20: fk.jz = fark_jz<2, 4>(); S_ = 4; break;
+        case 30: fk.jz = fark_jz<3, 3>(); S_ = 3; break;
+        case 40: fk.jz = fark_jz<4, 2>(); S_ = 2; break;
+        case 50: fk.jz = fark_jz<5, 2>(); S_ = 2; break;
+        case 60: fk.jz = fark_jz<6, 1>(); S_ = 1; break;
+        default: return ss::set_err(h, SS_EARG, "transposed composite: unsupported width");
+    }
+    fk.nz = (M + fk.jz - 1) / fk.jz;
+    cudaEvent_t ev = ss::timing_begin(h, st);
+    k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    SS_LAUNCH_CHECK(h);
+    ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
+    const int64_t units = (int64_t)fk.ntiles * ((sb + S_ - 1) / S_);
+    fk.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
+    const int grid = (int)std::max<int64_t>(fk.spl, std::min<int64_t>(units, h->num_sms) / fk.spl * fk.spl);
+    // algorithmic flops: the A^T rows are dense in the panel columns, the -I
+    // rows have one entry per column (m + 1 real state columns)
+    const int arows = std::max(0, std::min(r0, n) - rlo);
+    const double nnz = (double)arows * K + (double)std::min(K, std::max(0, r0 - std::max(rlo, n)));
+    ev = ss::timing_begin(h, st);
+    int rc;
+    switch (M) {
+        case 10: rc = launch_fark<1, 8>(h, grid, st, fk, S, W); break;
+        case 20: rc = launch_fark<2, 4>(h, grid, st, fk, S, W); break;
+        case 30: rc = launch_fark<3, 3, 3>(h, grid, st, fk, S, W); break;
+        case 40: rc = launch_fark<4, 2, 3>(h, grid, st, fk, S, W); break;
+        case 50: rc = launch_fark<5, 2, 3>(h, grid, st, fk, S, W); break;
+        default: rc = launch_fark<6, 1, 4>(h, grid, st, fk, S, W); break;
+    }
+    if (rc) return rc;
+    ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * M * M * (double)sb, 8.0 * rows * (double)sb * M * K,
+                   4.0 * (m + 1) * nnz * sb);
+    return SS_OK;
+}
+
+}  // namespace ss
 
 extern "C" {
 
