@@ -2094,6 +2094,39 @@ int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool fir
     return SS_OK;
 }
 
+// The far pass's -I rows [rlo, r0) (rlo >= n): their panel row has at most
+// one entry (-1 in column i - n), so instead of the dense K-streamed pass:
+//   z_i <- z_i W22 - [0 <= i - dlo < K] W12[i - dlo]        (dlo = n + c0)
+// One CTA per (128-row tile, shift): the rows' M state columns and W22 in
+// shared memory, a thread per row.
+__global__ void __launch_bounds__(128) k_tr_lower(int M, int64_t LDS, double2* __restrict__ S, int rlo, int r0,
+                                                  int dlo, int K, const double2* __restrict__ W, int64_t wstride) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* W22 = reinterpret_cast<double2*>(smem);  // M x M
+    double2* Zs = W22 + M * M;                         // [M][128]
+    const int l = blockIdx.y, t = threadIdx.x;
+    const int i = rlo + blockIdx.x * 128 + t;
+    const double2* Wl = W + (int64_t)l * wstride;
+    double2* Sl = S + (int64_t)l * M * LDS;
+    for (int e = t; e < M * M; e += 128) W22[e] = Wl[(int64_t)K * M + e];
+    for (int j = 0; j < M; ++j) Zs[j * 128 + t] = i < r0 ? Sl[(int64_t)j * LDS + i] : cz();
+    __syncthreads();
+    if (i >= r0) return;
+    const int dd = i - dlo;
+    for (int c = 0; c < M; ++c) {
+        double2 a0 = cz(), a1 = cz();
+        int j = 0;
+        for (; j + 1 < M; j += 2) {
+            a0 = cfma(Zs[j * 128 + t], W22[j * M + c], a0);
+            a1 = cfma(Zs[(j + 1) * 128 + t], W22[(j + 1) * M + c], a1);
+        }
+        if (j < M) a0 = cfma(Zs[j * 128 + t], W22[j * M + c], a0);
+        double2 v = cadd(a0, a1);
+        if (dd >= 0 && dd < K) v = csub(v, Wl[(int64_t)dd * M + c]);
+        Sl[(int64_t)c * LDS + i] = v;
+    }
+}
+
 // state widths the composite far pass supports (M = 10 NCB)
 bool tr_far_supported(ss_handle* h, int M) {
     switch (M) {
@@ -2110,8 +2143,23 @@ bool tr_far_supported(ss_handle* h, int M) {
 // from k_pack_panel_tr); the lazy -sigma rows are the first min(m, K) far
 // rows (the composite's last columns' diagonal).
 int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, int64_t lda,
-           const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0, int c0, int K,
+           const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0_all, int c0, int K,
            const double2* W, int64_t wstride) {
+    // the -I rows first (k_tr_lower), then the dense A^T rows (k_fark)
+    if (r0_all > std::max(rlo, n)) {
+        static ss::DevMask configured;
+        if (!configured.has(h)) {
+            SS_CUDA_TRY(h, allow_max_smem(h, k_tr_lower));
+            configured.set(h);
+        }
+        const int lo = std::max(rlo, n), nr = r0_all - lo;
+        cudaEvent_t ev = ss::timing_begin(h, st);
+        k_tr_lower<<<dim3((unsigned)((nr + 127) / 128), (unsigned)sb), 128, (size_t)(M * M + M * 128) * 16, st>>>(
+            M, LDS, S, lo, r0_all, n + c0, K, W, wstride);
+        SS_LAUNCH_CHECK(h);
+        ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
+    }
+    const int r0 = std::min(r0_all, n);
     const int rows = r0 - rlo;
     if (rows <= 0) return SS_OK;
     {
