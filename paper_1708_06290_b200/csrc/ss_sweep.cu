@@ -2097,33 +2097,55 @@ int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool fir
 // The far pass's -I rows [rlo, r0) (rlo >= n): their panel row has at most
 // one entry (-1 in column i - n), so instead of the dense K-streamed pass:
 //   z_i <- z_i W22 - [0 <= i - dlo < K] W12[i - dlo]        (dlo = n + c0)
-// One CTA per (128-row tile, shift): the rows' M state columns and W22 in
-// shared memory, a thread per row.
-__global__ void __launch_bounds__(128) k_tr_lower(int M, int64_t LDS, double2* __restrict__ S, int rlo, int r0,
+// One CTA per (64-row tile, shift): the rows' M state columns and W22 in
+// shared memory; a thread owns 4 rows x 4 columns (rows rg + 16 r, columns
+// cg + 16 c) in registers: 8 shared loads per 16 complex FMAs.
+constexpr int kTlRows = 64;
+__global__ void __launch_bounds__(256) k_tr_lower(int M, int64_t LDS, double2* __restrict__ S, int rlo, int r0,
                                                   int dlo, int K, const double2* __restrict__ W, int64_t wstride) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2* W22 = reinterpret_cast<double2*>(smem);  // M x M
-    double2* Zs = W22 + M * M;                         // [M][128]
+    double2* Zs = W22 + M * M;                         // [M][kTlRows]
     const int l = blockIdx.y, t = threadIdx.x;
-    const int i = rlo + blockIdx.x * 128 + t;
+    const int i0 = rlo + blockIdx.x * kTlRows;
     const double2* Wl = W + (int64_t)l * wstride;
     double2* Sl = S + (int64_t)l * M * LDS;
-    for (int e = t; e < M * M; e += 128) W22[e] = Wl[(int64_t)K * M + e];
-    for (int j = 0; j < M; ++j) Zs[j * 128 + t] = i < r0 ? Sl[(int64_t)j * LDS + i] : cz();
+    for (int e = t; e < M * M; e += 256) W22[e] = Wl[(int64_t)K * M + e];
+    for (int e = t; e < M * kTlRows; e += 256) {
+        const int j = e / kTlRows, r = e - j * kTlRows;
+        Zs[e] = i0 + r < r0 ? Sl[(int64_t)j * LDS + i0 + r] : cz();
+    }
     __syncthreads();
-    if (i >= r0) return;
-    const int dd = i - dlo;
-    for (int c = 0; c < M; ++c) {
-        double2 a0 = cz(), a1 = cz();
-        int j = 0;
-        for (; j + 1 < M; j += 2) {
-            a0 = cfma(Zs[j * 128 + t], W22[j * M + c], a0);
-            a1 = cfma(Zs[(j + 1) * 128 + t], W22[(j + 1) * M + c], a1);
+    const int rg = t & 15, cg = t >> 4;
+    double2 acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = cz();
+    for (int j = 0; j < M; ++j) {
+        double2 z[4], w[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) z[r] = Zs[j * kTlRows + rg + 16 * r];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[c] = cg + 16 * c < M ? W22[j * M + cg + 16 * c] : cz();
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = cfma(z[r], w[c], acc[r][c]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int i = i0 + rg + 16 * r;
+        if (i >= r0) continue;
+        const int dd = i - dlo;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int col = cg + 16 * c;
+            if (col >= M) continue;
+            double2 v = acc[r][c];
+            if (dd >= 0 && dd < K) v = csub(v, Wl[(int64_t)dd * M + col]);
+            Sl[(int64_t)col * LDS + i] = v;
         }
-        if (j < M) a0 = cfma(Zs[j * 128 + t], W22[j * M + c], a0);
-        double2 v = cadd(a0, a1);
-        if (dd >= 0 && dd < K) v = csub(v, Wl[(int64_t)dd * M + c]);
-        Sl[(int64_t)c * LDS + i] = v;
     }
 }
 
@@ -2154,8 +2176,8 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
         }
         const int lo = std::max(rlo, n), nr = r0_all - lo;
         cudaEvent_t ev = ss::timing_begin(h, st);
-        k_tr_lower<<<dim3((unsigned)((nr + 127) / 128), (unsigned)sb), 128, (size_t)(M * M + M * 128) * 16, st>>>(
-            M, LDS, S, lo, r0_all, n + c0, K, W, wstride);
+        k_tr_lower<<<dim3((unsigned)((nr + kTlRows - 1) / kTlRows), (unsigned)sb), 256,
+                     (size_t)(M * M + M * kTlRows) * 16, st>>>(M, LDS, S, lo, r0_all, n + c0, K, W, wstride);
         SS_LAUNCH_CHECK(h);
         ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
     }
