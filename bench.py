@@ -583,6 +583,40 @@ def main(argv=None):
                    "failures": int((fail_r >= 0).sum().item())}
         del X, bd
 
+    # ---- SURVEY 8(f) row 1 on the same shifts: solve_shifted_transposed ----
+    # (IRKA's left solves; general complex right-hand sides, unit norm)
+    transposed = None
+    if not args.no_reduced and cfg == 4:
+        rng = np.random.default_rng(2000 + rank)
+        rhs_h = rng.standard_normal((n, s_loc)) + 1j * rng.standard_normal((n, s_loc))
+        rhs_h /= np.linalg.norm(rhs_h, axis=0, keepdims=True)
+        rhs = torch.from_numpy(np.asfortranarray(rhs_h)).to(dev).t().contiguous().t()
+        del rhs_h
+        Xt = torch.empty((s_loc, n), dtype=torch.complex128, device=dev).t()
+        fail_t = torch.empty(s_loc, dtype=torch.int32, device=dev)
+
+        def step_tr():
+            rc = L.ss_solve_transposed(h.ptr, n, m, D.ptr(A), D.ld(A), D.ptr(sh_d), s_loc, D.ptr(rhs),
+                                       D.ld(rhs), 32, args.batch, nan, D.ptr(Xt), n, D.ptr(fail_t),
+                                       ctypes.c_void_p(stream.cuda_stream))
+            D.check(h, rc)
+
+        step_tr()
+        torch.cuda.synchronize()
+        k_t = max(1, min(args.steps, 3))
+        ms_t = timed(step_tr, k_t)
+        v_t = s_total / (ms_t * 1e-3)
+        # structural nonzeros of [A^T; -I] (n^2 / 2 + n (m + 1) + n) meet the m + 1
+        # state columns once at 4 flops each
+        fa_t = 4.0 * (m + 1) * (n * n / 2.0 + n * (m + 2))
+        transposed = {"op": "solve_shifted_transposed ((Ahat - sigma_l I)^T x_l = c_l, unit-norm "
+                            "complex Gaussian c_l; SURVEY 8(f) row 1)",
+                      "value": v_t, "unit": "shifts/s", "ms_per_step": ms_t, "steps": k_t,
+                      "sweep_tflops": fa_t * v_t / world / 1e12,
+                      "frac_of_fp64_peak": fa_t * v_t / world / 1e12 / fp64_peak if fp64_peak else None,
+                      "failures": int((fail_t >= 0).sum().item())}
+        del Xt, rhs
+
     # ---- e2e through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -661,6 +695,7 @@ def main(argv=None):
                                "frac": sweep_tflops / fp64_peak if fp64_peak else None,
                                "f_alg_per_shift": fa},
             "reduced": reduced,
+            "transposed": transposed,
             "phase_seconds": {k: sec5[i] for i, k in enumerate(ss.counters.ALL_PHASES)},
             "reduction_ms": red_ms,
             "cpu_baseline": cpu,
