@@ -14,7 +14,7 @@ def triple(n, m, p, rng):
     return ss.ControllerHessForm(Ahat=np.asfortranarray(A), Bhat=B, Chat=C, m=m, n=n, p=p)
 
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
-ms = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 16, 20, 24, 31, 32, 40, 50, 63]
+ms = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 16, 20, 24, 29, 31, 32, 40, 50, 59, 60, 63, 70]
 worst, bad = 0.0, 0
 for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     m = int(rng.choice(ms))
@@ -33,7 +33,7 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     Go, _ = O.tf_eval(chf.Ahat, chf.Bhat, chf.Chat, sh[idx], nb=nb)
     err = max(np.linalg.norm(G[:, l * m:(l + 1) * m] - Go[:, k * m:(k + 1) * m]) /
               np.linalg.norm(Go[:, k * m:(k + 1) * m]) for k, l in enumerate(idx))
-    # reduced solve (identity top) and, for m + 1 <= 32, the transposed solve
+    # reduced solve (identity top) and the transposed solve
     k2 = [0, s - 1]
     bd = rng.standard_normal((m, len(k2))) + 1j * rng.standard_normal((m, len(k2)))
     try:
@@ -41,7 +41,7 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
         for k, l in enumerate(k2):
             xo = O.lu_solve_shifted(chf.Ahat, sh[l], chf.Bhat @ bd[:, k])
             err = max(err, np.linalg.norm(X[:, k] - xo) / np.linalg.norm(xo))
-        if m + 1 <= 32:
+        if m + 1 <= 256:
             rhs = rng.standard_normal((n, len(k2))) + 1j * rng.standard_normal((n, len(k2)))
             Xt = ss.solve_shifted_transposed(chf, sh[k2], rhs, nb=min(nb, 32), batch_size=bs).x
             for k, l in enumerate(k2):
