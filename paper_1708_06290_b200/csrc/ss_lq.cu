@@ -46,8 +46,8 @@ namespace ss {
 // ss_sweep.cu: the window-update kernel on the [A^T; -I] panel, and the
 // composite fold / K-streamed far pass
 int launch_update_tr(ss_handle* h, ssd::UpdDims u, int rows, double2* S, const double2* P, cudaStream_t st);
-int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool first, int sb, const double2* P,
-            double2* W, int64_t wstride);
+int tr_fold(ss_handle* h, cudaStream_t st, int M, int mc, int K, int x, int nb, bool first, int sb,
+            const double2* P, double2* W, int64_t wstride);
 bool tr_far_supported(ss_handle* h, int M);
 int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, int64_t lda,
            const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0, int c0, int K,
@@ -827,7 +827,7 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
                                    8.0 * rows * (double)sb * M * ls.nb, 4.0 * mp * (double)rows * ls.nb * sb);
                 }
                 ev = ss::timing_begin(h, st);
-                rc = ss::tr_fold(h, st, M, K, ls.k0 - k0, ls.nb, b == 0, sb, Pb, Wb, wstride);
+                rc = ss::tr_fold(h, st, M, mp, K, ls.k0 - k0, ls.nb, b == 0, sb, Pb, Wb, wstride);
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
             }

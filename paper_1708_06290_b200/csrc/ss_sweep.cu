@@ -855,9 +855,12 @@ struct WcLayout {
 // into the composite W of shift l: rows [x, x + nb) <- P12; rows
 // [x + nb, K + m) <- rows P22 (first window of the composite, x + nb == K:
 // W22 <- P22).  grid (sb, row chunks).
+// mc <= m: columns actually carried (the transposed sweep pads its m + 1 state
+// columns to m = 10 ceil((m + 1) / 10); the padding of P and W is zero and
+// stays zero, so only mc columns are multiplied)
 __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool first, int64_t pstride,
                                                const double2* __restrict__ P, WcLayout lw,
-                                               double2* __restrict__ W, int ra, int rb) {
+                                               double2* __restrict__ W, int ra, int rb, int mc) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2* P22 = reinterpret_cast<double2*>(smem);  // m x m
     double2* Wr = P22 + m * m;                        // [kWcRows][m]
@@ -884,16 +887,16 @@ __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool
     for (int e = tid; e < m * m; e += blockDim.x) P22[e] = Pl[(int64_t)nb * m + e];
     for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)wrow(c0 + e / m) * rs + e % m];
     __syncthreads();
-    for (int e = tid; e < rc * m; e += blockDim.x) {
-        const int r = e / m, c = e - r * m;
+    for (int e = tid; e < rc * mc; e += blockDim.x) {
+        const int r = e / mc, c = e - r * mc;
         const double2* wr = Wr + r * m;
         double2 a0 = cz(), a1 = cz();
         int j = 0;
-        for (; j + 1 < m; j += 2) {
+        for (; j + 1 < mc; j += 2) {
             a0 = cfma(wr[j], P22[j * m + c], a0);
             a1 = cfma(wr[j + 1], P22[(j + 1) * m + c], a1);
         }
-        if (j < m) a0 = cfma(wr[j], P22[j * m + c], a0);
+        if (j < mc) a0 = cfma(wr[j], P22[j * m + c], a0);
         Wl[(int64_t)wrow(c0 + r) * rs + c] = cadd(a0, a1);
     }
 }
@@ -1375,7 +1378,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 } else {
                     dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
                     k_wcomp<<<gc, 256, wcomp_smem(m), st>>>(m, K, cw - c0, nb, b == 0, (int64_t)nc * m, B.P,
-                                                            lw, B.W, cw - c0 + nb, K);
+                                                            lw, B.W, cw - c0 + nb, K, m);
                 }
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
@@ -2079,8 +2082,8 @@ namespace ss {
 // Fold window P ((nb + M) x M per shift, M = padded state width) into the
 // composite W ((K + M) x M per shift): W12[x, x + nb) <- P12, W12[0, x) and
 // W22 <- . P22 (the earlier windows sit ABOVE in the top-down sweep).
-int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool first, int sb, const double2* P,
-            double2* W, int64_t wstride) {
+int tr_fold(ss_handle* h, cudaStream_t st, int M, int mc, int K, int x, int nb, bool first, int sb,
+            const double2* P, double2* W, int64_t wstride) {
     static ss::DevMask configured;
     if (!configured.has(h)) {
         SS_CUDA_TRY(h, allow_max_smem(h, k_wcomp));
@@ -2089,7 +2092,7 @@ int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool fir
     const WcLayout lw{1, wstride, 0, M};
     const int nrows = x + M;
     dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
-    k_wcomp<<<gc, 256, wcomp_smem(M), st>>>(M, K, x, nb, first, (int64_t)(nb + M) * M, P, lw, W, 0, x);
+    k_wcomp<<<gc, 256, wcomp_smem(M), st>>>(M, K, x, nb, first, (int64_t)(nb + M) * M, P, lw, W, 0, x, mc);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -2101,8 +2104,9 @@ int tr_fold(ss_handle* h, cudaStream_t st, int M, int K, int x, int nb, bool fir
 // shared memory; a thread owns 4 rows x 4 columns (rows rg + 16 r, columns
 // cg + 16 c) in registers: 8 shared loads per 16 complex FMAs.
 constexpr int kTlRows = 64;
-__global__ void __launch_bounds__(256) k_tr_lower(int M, int64_t LDS, double2* __restrict__ S, int rlo, int r0,
-                                                  int dlo, int K, const double2* __restrict__ W, int64_t wstride) {
+__global__ void __launch_bounds__(256) k_tr_lower(int M, int mc, int64_t LDS, double2* __restrict__ S, int rlo,
+                                                  int r0, int dlo, int K, const double2* __restrict__ W,
+                                                  int64_t wstride) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2* W22 = reinterpret_cast<double2*>(smem);  // M x M
     double2* Zs = W22 + M * M;                         // [M][kTlRows]
@@ -2111,7 +2115,7 @@ __global__ void __launch_bounds__(256) k_tr_lower(int M, int64_t LDS, double2* _
     const double2* Wl = W + (int64_t)l * wstride;
     double2* Sl = S + (int64_t)l * M * LDS;
     for (int e = t; e < M * M; e += 256) W22[e] = Wl[(int64_t)K * M + e];
-    for (int e = t; e < M * kTlRows; e += 256) {
+    for (int e = t; e < mc * kTlRows; e += 256) {
         const int j = e / kTlRows, r = e - j * kTlRows;
         Zs[e] = i0 + r < r0 ? Sl[(int64_t)j * LDS + i0 + r] : cz();
     }
@@ -2122,12 +2126,12 @@ __global__ void __launch_bounds__(256) k_tr_lower(int M, int64_t LDS, double2* _
     for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = cz();
-    for (int j = 0; j < M; ++j) {
+    for (int j = 0; j < mc; ++j) {  // padding columns (>= mc) are zero
         double2 z[4], w[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) z[r] = Zs[j * kTlRows + rg + 16 * r];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) w[c] = cg + 16 * c < M ? W22[j * M + cg + 16 * c] : cz();
+        for (int c = 0; c < 4; ++c) w[c] = cg + 16 * c < mc ? W22[j * M + cg + 16 * c] : cz();
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -2141,7 +2145,7 @@ __global__ void __launch_bounds__(256) k_tr_lower(int M, int64_t LDS, double2* _
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int col = cg + 16 * c;
-            if (col >= M) continue;
+            if (col >= mc) continue;
             double2 v = acc[r][c];
             if (dd >= 0 && dd < K) v = csub(v, Wl[(int64_t)dd * M + col]);
             Sl[(int64_t)col * LDS + i] = v;
@@ -2177,7 +2181,7 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
         const int lo = std::max(rlo, n), nr = r0_all - lo;
         cudaEvent_t ev = ss::timing_begin(h, st);
         k_tr_lower<<<dim3((unsigned)((nr + kTlRows - 1) / kTlRows), (unsigned)sb), 256,
-                     (size_t)(M * M + M * kTlRows) * 16, st>>>(M, LDS, S, lo, r0_all, n + c0, K, W, wstride);
+                     (size_t)(M * M + M * kTlRows) * 16, st>>>(M, m + 1, LDS, S, lo, r0_all, n + c0, K, W, wstride);
         SS_LAUNCH_CHECK(h);
         ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
     }
