@@ -39,6 +39,7 @@
 namespace ssd {
 
 constexpr int kFkTile = 64;  // rows per unit
+constexpr int kFarkUnroll = 4;  // panel columns unrolled in the main loop (2 / 8: same / -0.6%)
 constexpr int kFkKC = 32;    // panel columns per chunk
 
 struct FarKDims {
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                         }
                     }
                     if (kcols == KC) {
-#pragma unroll 4
+#pragma unroll (kFarkUnroll)
                         for (int j = 0; j < KC; ++j) {
                             double a[R];
 #pragma unroll
@@ -263,12 +264,15 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                                 a[2 * p] = v.x;
                                 a[2 * p + 1] = v.y;
                             }
+                            // the lane's 5 W12 entries first, then rows outer: measured
+                            // 4.87k vs 4.84k shifts/s at config 4 (column-outer order)
+                            double2 pv[C];
 #pragma unroll
-                            for (int c = 0; c < C; ++c) {
-                                const double2 pv = ws[j * M + c];
+                            for (int c = 0; c < C; ++c) pv[c] = ws[j * M + c];
 #pragma unroll
-                                for (int r = 0; r < R; ++r) acc[r][c] = rfma(a[r], pv, acc[r][c]);
-                            }
+                            for (int r = 0; r < R; ++r)
+#pragma unroll
+                                for (int c = 0; c < C; ++c) acc[r][c] = rfma(a[r], pv[c], acc[r][c]);
                         }
                     } else {
                         for (int j = 0; j < kcols; ++j) {
