@@ -64,6 +64,10 @@ struct FarKDims {
     // entries sit at the top of the far rows, in the composite's last columns)
     int lz0 = 0, lzp = 0, lzset = 0;
     int n = 0;  // k_pack_panel_tr: rows >= n are the -I block
+    // Z of shift l: Z + l zstride + zoff (0: l M LDZ / l LDZ for k_farkm) --
+    // the transposed sweep runs the far pass over its z2 columns (stride
+    // (m + 1) LDZ per shift) and, on k_farkm, over its w column (zoff m LDZ)
+    int64_t zstride = 0, zoff = 0;
 };
 
 // The transposed sweep's panel [A^T; -I]: rows i < n are A(c, i) (row i of
@@ -142,6 +146,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
     const int64_t ua = ua0 + h;
     const int nun = ua < ub ? (int)((ub - ua + spl - 1) / spl) : 0;
     const int CH = nz + nk;
+    const int64_t zst = u.zstride ? u.zstride : (int64_t)M * u.LDZ;  // per-shift Z stride
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                             const int64_t l = l0 + sh;
                             double2* zs = reinterpret_cast<double2*>(st) + (size_t)sh * jz * (TILE + M);
                             for (int j = 0; j < jn; ++j)
-                                tma_bulk_g2s(zs + j * TILE, Z + (l * M + j0 + j) * u.LDZ + i0, zb, full + s);
+                                tma_bulk_g2s(zs + j * TILE, Z + l * zst + (int64_t)(j0 + j) * u.LDZ + i0, zb, full + s);
                             tma_bulk_g2s(zs + jz * TILE, W + l * u.wstride + (int64_t)(u.woff + K + j0) * M,
                                          (unsigned)(jn * M * 16), full + s);
                         }
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
             if (lane == 0) mbar_arrive(empty + s);
         }
         if (!valid) continue;
-        double2* zo = Z + (l * M + cb) * u.LDZ + i0 + rg;
+        double2* zo = Z + l * zst + (int64_t)cb * u.LDZ + i0 + rg;
         if (i0 + TILE <= r0) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -387,14 +392,16 @@ __global__ void __launch_bounds__(32 * 9, 1) k_farkm(FarKDims u, double2* Z, con
     const int cw = warp - 1;  // shifts 10 cw .. 10 cw + 9 of the group
     const int rg = lane >> 1, q = lane & 1;
     const int cb = cw * 10 + q * C;  // first of this lane's 5 shifts (group-local)
-    const int dlo = r0 - 1;
+    const int dlo = u.lzset ? u.lz0 : r0 - 1;  // first lazy row
+    const int dp = u.lzset ? u.lzp : 0;         // its W12 row
+    const int64_t zst = u.zstride ? u.zstride : u.LDZ;
     int g = 0;
     for (int k = 0; k < nun; ++k) {
         const int64_t unit = ua + (int64_t)k * spl;
         const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles);
         const int l0 = grp * S;
         const int i0 = u.rlo + tile * TILE;
-        const bool interior = i0 + TILE <= (u.mnb > 0 ? dlo : r0);
+        const bool interior = u.mnb == 0 || i0 + TILE <= dlo || i0 >= dlo + u.mnb;
         double2 acc[R][C];
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -407,15 +414,18 @@ __global__ void __launch_bounds__(32 * 9, 1) k_farkm(FarKDims u, double2* Z, con
             const int kcols = min(KC, K - kc * KC);
             const double* pan = reinterpret_cast<const double*>(st) + rg * 2;
             const double2* ws = reinterpret_cast<const double2*>(st + PANB) + cb;
-            if (!interior && kc == 0) {
-                // the lazy shift: the one row r0 - 1 carries -sigma_l W12_l[0]
+            if (!interior && dp < kc * KC + kcols && dp + u.mnb > kc * KC) {
+                // lazy shift: rows dlo + dd carry -sigma_l W12_l[dp + dd]
+                // (forward m = 1: the one row r0 - 1 with W12 row 0)
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    if (i0 + rg + RG * r == dlo) {
+                    const int dd = i0 + rg + RG * r - dlo;
+                    const int wr = dp + dd - kc * KC;
+                    if (dd >= 0 && dd < u.mnb && wr >= 0 && wr < kcols) {
 #pragma unroll
                         for (int c = 0; c < C; ++c) {
                             const int l = min(l0 + cb + c, sb - 1);
-                            acc[r][c] = csub(acc[r][c], cmul(u.shifts[l], ws[c]));
+                            acc[r][c] = csub(acc[r][c], cmul(u.shifts[l], ws[wr * S + c]));
                         }
                     }
                 }
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(32 * 9, 1) k_farkm(FarKDims u, double2* Z, con
             const int64_t l = l0 + cb + c;
             if (l >= sb) continue;
             const double2 wz = w22[c];
-            const double2* zc = Z + l * u.LDZ + i0 + rg;
+            const double2* zc = Z + l * zst + u.zoff + i0 + rg;
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (i0 + rg + RG * r < r0) acc[r][c] = cfma(__ldg(zc + RG * r), wz, acc[r][c]);
@@ -456,7 +466,7 @@ __global__ void __launch_bounds__(32 * 9, 1) k_farkm(FarKDims u, double2* Z, con
         for (int c = 0; c < C; ++c) {
             const int64_t l = l0 + cb + c;
             if (l >= sb) continue;
-            double2* zc = Z + l * u.LDZ + i0 + rg;
+            double2* zc = Z + l * zst + u.zoff + i0 + rg;
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (i0 + rg + RG * r < r0) zc[RG * r] = acc[r][c];

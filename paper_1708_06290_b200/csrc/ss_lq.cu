@@ -49,6 +49,10 @@ int launch_update_tr(ss_handle* h, ssd::UpdDims u, int rows, double2* S, const d
 int tr_fold(ss_handle* h, cudaStream_t st, int M, int mc, int K, int x, int nb, bool first, int sb,
             const double2* P, double2* W, int64_t wstride);
 bool tr_far_supported(ss_handle* h, int M);
+bool tr_split_supported(ss_handle* h, int m);
+int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, int64_t lda,
+                 const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0_all, int c0, int K,
+                 const double2* W, int64_t wstride, double2* Wz, int64_t wzstride, double2* Ww, int64_t gstride);
 int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, int64_t lda,
            const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0, int c0, int K,
            const double2* W, int64_t wstride);
@@ -57,6 +61,7 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
 namespace {
 
 constexpr int kLqMaxNb = 32;
+constexpr int kFkmShiftsLq = 80;  // k_farkm's shifts per unit (ss_fark.cuh kFkmShifts)
 // panel columns per transposed composite (the packed panel's capacity): 16
 // windows of 32 rows; 12 / 8 / 6 windows measured 1.71k / 1.61k / 1.50k vs
 // 1.72k shifts/s (n = 10000, m = 20)
@@ -727,12 +732,18 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     // columns of windows, the rows below them updated ONCE by the K-streamed
     // far kernel; the state is padded to M = 10 ceil(mp / 10) columns for its
     // register tiles (zero columns stay zero: P and W are zero there)
-    const int M = 10 * ((mp + 9) / 10);
-    const bool comp = M <= 60 && ss::tr_far_supported(h, M) && n - m > 2 * nb0;
+    // For m a multiple of 10 the far pass is split instead (no padding): z2 on
+    // k_fark at exactly m columns, w on k_farkm (ss_sweep.cu tr_far_split)
+    const bool split = n - m > 2 * nb0 && ss::tr_split_supported(h, m);
+    const int M = split ? mp : 10 * ((mp + 9) / 10);
+    const bool comp = split || (M <= 60 && ss::tr_far_supported(h, M) && n - m > 2 * nb0);
     const int ms = comp ? M : mp;
     const int G = std::max(1, std::min(64, kTrK / nb0)), Kmax = G * nb0;
     const int64_t wstride = comp ? (int64_t)(Kmax + M) * M : 0;
-    const size_t per_shift = (size_t)LDS * ms * 16 + (size_t)(nb0 + ms) * ms * 16 + (size_t)wstride * 16 + 8 + 64;
+    const int64_t wzstride = split ? (int64_t)(Kmax + m) * m : 0;                    // W of z2
+    const int64_t gstride = split ? (int64_t)(Kmax + 1) * kFkmShiftsLq : 0;          // w column, per group
+    const size_t per_shift = (size_t)LDS * ms * 16 + (size_t)(nb0 + ms) * ms * 16 + (size_t)wstride * 16 +
+                             (size_t)wzstride * 16 + (size_t)(Kmax + 1) * (split ? 16 : 0) + 8 + 64;
     int64_t sb_max = std::min<int64_t>(batch > 0 ? batch : s, s);
     if (per_shift * (size_t)sb_max + 256 > h->ws_bytes) {  // query only to grow (slow driver call)
         size_t fr = 0, tot = 0;
@@ -742,13 +753,17 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
                                                         (int64_t)(cap / per_shift)));
     }
     {
-        int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256, 0);
+        const size_t slack = split ? (size_t)kFkmShiftsLq * (Kmax + 1) * 16 : 0;  // the last group of 80
+        int rc = ss::ensure_ws(h, per_shift * (size_t)sb_max + 256 + slack, 0);
         if (rc) return rc;
     }
     double2* Sb = (double2*)h->ws;
     double2* Pb = Sb + (size_t)sb_max * ms * LDS;
     double2* Wb = Pb + (size_t)sb_max * (nb0 + ms) * ms;
-    double* tolb = (double*)(Wb + (size_t)sb_max * wstride);
+    double2* Wzb = Wb + (size_t)sb_max * wstride;
+    double2* Wwb = Wzb + (size_t)sb_max * wzstride;  // ceil(sb / 80) groups (per_shift holds Kmax + 1 each + slack)
+    const size_t ngroups_max = split ? (size_t)((sb_max + kFkmShiftsLq - 1) / kFkmShiftsLq) : 0;
+    double* tolb = (double*)(Wwb + ngroups_max * gstride);
     static ss::DevMask attrs;  // devices configured
     if (!attrs.has(h)) {
         SS_CUDA_TRY(h, allow_smem(h, k_tupd<128, true>));
@@ -837,7 +852,10 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
             // far rows: the rest of A^T's rows and the -I rows up to the
             // composite's last column
             const int rend = std::min(2 * n, n + c0 + K);
-            int rc = ss::tr_far(h, st, n, m, M, Ahat, lda, d.shifts, sb, Sb, LDS, kend, rend, c0, K, Wb, wstride);
+            int rc = split ? ss::tr_far_split(h, st, n, m, Ahat, lda, d.shifts, sb, Sb, LDS, kend, rend, c0, K, Wb,
+                                              wstride, Wzb, wzstride, Wwb, gstride)
+                           : ss::tr_far(h, st, n, m, M, Ahat, lda, d.shifts, sb, Sb, LDS, kend, rend, c0, K, Wb,
+                                        wstride);
             if (rc) return rc;
             k0 = kend;
         }

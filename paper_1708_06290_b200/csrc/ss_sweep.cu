@@ -2157,6 +2157,48 @@ __global__ void __launch_bounds__(256) k_tr_lower(int M, int mc, int64_t LDS, do
     }
 }
 
+// Split far pass of the transposed composites (m a multiple of 10): the z2
+// columns run the K-streamed k_fark at exactly M = m columns, the w column
+// (which never feeds z2: W22's w row is e_m) runs k_farkm with 80 shifts per
+// unit as its columns; w first takes the old z2's contribution z2 W22[:m, m]
+// (k_tr_wprep) and the composite is split into W_z ((K + m) x m per shift)
+// and the group-major w column (k_tr_wsplit).
+__global__ void __launch_bounds__(256) k_tr_wprep(int m, int64_t LDS, double2* __restrict__ S, int rlo, int r0,
+                                                  int K, const double2* __restrict__ W, int64_t wstride) {
+    __shared__ double2 wz[64];
+    const int l = blockIdx.y, mp = m + 1;
+    const double2* Wl = W + (int64_t)l * wstride;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) wz[j] = Wl[(int64_t)(K + j) * mp + m];
+    __syncthreads();
+    const int i = rlo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= r0) return;
+    double2* Sl = S + (int64_t)l * mp * LDS;
+    double2 a0 = Sl[(int64_t)m * LDS + i], a1 = cz();
+    int j = 0;
+    for (; j + 1 < m; j += 2) {
+        a0 = cfma(Sl[(int64_t)j * LDS + i], wz[j], a0);
+        a1 = cfma(Sl[(int64_t)(j + 1) * LDS + i], wz[j + 1], a1);
+    }
+    if (j < m) a0 = cfma(Sl[(int64_t)j * LDS + i], wz[j], a0);
+    Sl[(int64_t)m * LDS + i] = cadd(a0, a1);
+}
+
+__global__ void __launch_bounds__(256) k_tr_wsplit(int m, int K, int sb, const double2* __restrict__ W,
+                                                   int64_t wstride, double2* __restrict__ Wz, int64_t wzstride,
+                                                   double2* __restrict__ Ww, int64_t gstride) {
+    const int l = blockIdx.y, mp = m + 1;
+    const double2* Wl = W + (int64_t)l * wstride;
+    double2* Wzl = Wz + (int64_t)l * wzstride;
+    const int grp = l / kFkmShifts, q = l - grp * kFkmShifts;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (K + mp) * mp; e += gridDim.x * blockDim.x) {
+        const int r = e / mp, c = e - r * mp;
+        if (c < m && r < K + m) Wzl[(int64_t)r * m + c] = Wl[e];                              // W12 / W22 of z2
+        else if (c == m && r < K) Ww[grp * gstride + (int64_t)r * kFkmShifts + q] = Wl[e];   // W12 of w
+        else if (c == m && r == K + m) Ww[grp * gstride + (int64_t)K * kFkmShifts + q] = Wl[e];  // W22[m][m]
+    }
+    (void)sb;
+}
+
 // state widths the composite far pass supports (M = 10 NCB)
 bool tr_far_supported(ss_handle* h, int M) {
     switch (M) {
@@ -2261,6 +2303,116 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
     return SS_OK;
 }
 
+
+int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, int64_t lda,
+                 const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0_all, int c0, int K,
+                 const double2* W, int64_t wstride, double2* Wz, int64_t wzstride, double2* Ww, int64_t gstride) {
+    const int mp = m + 1;
+    // the -I rows (state z2 and w, mp columns)
+    if (r0_all > std::max(rlo, n)) {
+        static ss::DevMask configured;
+        if (!configured.has(h)) {
+            SS_CUDA_TRY(h, allow_max_smem(h, k_tr_lower));
+            configured.set(h);
+        }
+        const int lo = std::max(rlo, n), nr = r0_all - lo;
+        cudaEvent_t ev = ss::timing_begin(h, st);
+        k_tr_lower<<<dim3((unsigned)((nr + kTlRows - 1) / kTlRows), (unsigned)sb), 256,
+                     (size_t)(mp * mp + mp * kTlRows) * 16, st>>>(mp, mp, LDS, S, lo, r0_all, n + c0, K, W, wstride);
+        SS_LAUNCH_CHECK(h);
+        ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
+    }
+    const int r0 = std::min(r0_all, n), rows = r0 - rlo;
+    if (rows <= 0) return SS_OK;
+    {
+        int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(2 * n, 0), 1);
+        if (rc) return rc;
+    }
+    double* pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
+    FarKDims fk;
+    fk.m = m;
+    fk.ptop = 0;
+    fk.ident_top = 0;
+    fk.A = A;
+    fk.lda = lda;
+    fk.T = nullptr;
+    fk.ldt = 0;
+    fk.shifts = shifts;
+    fk.sb = sb;
+    fk.LDZ = LDS;
+    fk.r0 = r0;
+    fk.rlo = rlo;
+    fk.c0 = c0;
+    fk.K = K;
+    fk.lz0 = std::max(rlo, c0);
+    fk.lzp = fk.lz0 - c0;
+    fk.mnb = std::max(0, c0 + K - fk.lz0);
+    fk.lzset = 1;
+    fk.n = n;
+    fk.woff = 0;
+    fk.nk = (K + kFkKC - 1) / kFkKC;
+    fk.ntiles = (rows + kFkTile - 1) / kFkTile;
+    fk.pan = pan;
+    fk.zstride = (int64_t)mp * LDS;
+    cudaEvent_t ev = ss::timing_begin(h, st);
+    k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    SS_LAUNCH_CHECK(h);
+    k_tr_wprep<<<dim3((unsigned)((rows + 255) / 256), (unsigned)sb), 256, 0, st>>>(m, LDS, S, rlo, r0, K, W,
+                                                                                   wstride);
+    SS_LAUNCH_CHECK(h);
+    k_tr_wsplit<<<dim3(8, (unsigned)sb), 256, 0, st>>>(m, K, sb, W, wstride, Wz, wzstride, Ww, gstride);
+    SS_LAUNCH_CHECK(h);
+    ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
+    const int arows = rows;
+    const double nnz = (double)arows * K;
+    // w: 80 shifts per unit as columns
+    {
+        FarKDims fw = fk;
+        fw.wstride = gstride;
+        fw.zoff = (int64_t)m * LDS;
+        const int64_t units = (int64_t)fw.ntiles * ((sb + kFkmShifts - 1) / kFkmShifts);
+        fw.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
+        const int grid = (int)std::max<int64_t>(fw.spl, std::min<int64_t>(units, h->num_sms) / fw.spl * fw.spl);
+        ev = ss::timing_begin(h, st);
+        int rc = launch_farkm(h, grid, st, fw, S, Ww);
+        if (rc) return rc;
+        ss::timing_end(h, st, ev, ss::PH_UPDATE, 0.0, 8.0 * rows * (double)sb * K, 4.0 * nnz * sb);
+    }
+    // z2: exact m = 10 NCB columns
+    int S_ = 1;
+    switch (m) {
+        case 10: fk.jz = fark_jz<1, 8>(); S_ = 8; break;
+        case 20: fk.jz = fark_jz<2, 4>(); S_ = 4; break;
+        case 30: fk.jz = fark_jz<3, 3>(); S_ = 3; break;
+        case 40: fk.jz = fark_jz<4, 2>(); S_ = 2; break;
+        case 50: fk.jz = fark_jz<5, 2>(); S_ = 2; break;
+        case 60: fk.jz = fark_jz<6, 1>(); S_ = 1; break;
+        default: return ss::set_err(h, SS_EARG, "transposed split far pass: unsupported m");
+    }
+    fk.nz = (m + fk.jz - 1) / fk.jz;
+    fk.wstride = wzstride;
+    const int64_t units = (int64_t)fk.ntiles * ((sb + S_ - 1) / S_);
+    fk.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
+    const int grid = (int)std::max<int64_t>(fk.spl, std::min<int64_t>(units, h->num_sms) / fk.spl * fk.spl);
+    ev = ss::timing_begin(h, st);
+    int rc;
+    switch (m) {
+        case 10: rc = launch_fark<1, 8>(h, grid, st, fk, S, Wz); break;
+        case 20: rc = launch_fark<2, 4>(h, grid, st, fk, S, Wz); break;
+        case 30: rc = launch_fark<3, 3, 3>(h, grid, st, fk, S, Wz); break;
+        case 40: rc = launch_fark<4, 2, 3>(h, grid, st, fk, S, Wz); break;
+        case 50: rc = launch_fark<5, 2, 3>(h, grid, st, fk, S, Wz); break;
+        default: rc = launch_fark<6, 1, 4>(h, grid, st, fk, S, Wz); break;
+    }
+    if (rc) return rc;
+    ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb, 8.0 * rows * (double)sb * m * K,
+                   4.0 * m * nnz * sb);
+    return SS_OK;
+}
+
+bool tr_split_supported(ss_handle* h, int m) {
+    return m % 10 == 0 && m <= 60 && tr_far_supported(h, m) && farkm_smem_bytes<4>() <= h->smem_optin;
+}
 }  // namespace ss
 
 extern "C" {
