@@ -793,26 +793,30 @@ constexpr int kWcNb = 64;
 struct WcShape {
     int S, NST;
 };
+// Consumer warps per CTA = NCB S: a multiple of 4 keeps the four SM
+// sub-partitions' FP64 pipes evenly loaded (m = 50: 10 warps, <5,2,3>, 344
+// shifts/s at config 5; 15 warps, <5,3,2>, 364; 5 warps, <5,1,4>, 273)
 static bool wc_shape(int m, WcShape& w) {
     if (m == 1) { w = {kFkmShifts, 4}; return true; }
-    if (m == 40 || m == 50) { w = {2, 3}; return true; }
-    if (m == 60) { w = {1, 4}; return true; }
+    if (m == 40) { w = {2, 3}; return true; }
+    if (m == 50) { w = {3, 2}; return true; }
+    if (m == 60) { w = {2, 2}; return true; }
     return false;
 }
 static size_t wc_far_smem(int m) {
     switch (m) {
         case 1: return farkm_smem_bytes<4>();
         case 40: return fark_smem_bytes<4, 2, 3>();
-        case 50: return fark_smem_bytes<5, 2, 3>();
-        case 60: return fark_smem_bytes<6, 1, 4>();
+        case 50: return fark_smem_bytes<5, 3, 2>();
+        case 60: return fark_smem_bytes<6, 2, 2>();
         default: return ~(size_t)0;
     }
 }
 static int wc_jz(int m) {
     switch (m) {
         case 40: return fark_jz<4, 2>();
-        case 50: return fark_jz<5, 2>();
-        default: return fark_jz<6, 1>();
+        case 50: return fark_jz<5, 3>();
+        default: return fark_jz<6, 2>();
     }
 }
 static int launch_farkm(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z,
@@ -831,8 +835,8 @@ static int launch_wc_far(ss_handle* h, int m, int grid, cudaStream_t st, const F
                          const double2* W) {
     switch (m) {
         case 40: return launch_fark<4, 2, 3>(h, grid, st, fk, Z, W);
-        case 50: return launch_fark<5, 2, 3>(h, grid, st, fk, Z, W);
-        case 60: return launch_fark<6, 1, 4>(h, grid, st, fk, Z, W);
+        case 50: return launch_fark<5, 3, 2>(h, grid, st, fk, Z, W);
+        case 60: return launch_fark<6, 2, 2>(h, grid, st, fk, Z, W);
         default: return ss::set_err(h, SS_EARG, "window composite: unsupported m");
     }
 }
@@ -2204,7 +2208,7 @@ bool tr_far_supported(ss_handle* h, int M) {
     switch (M) {
         case 10: return fark_smem_bytes<1, 8, kFarkStages>() <= h->smem_optin;
         case 20: return fark_smem_bytes<2, 4, kFarkStages>() <= h->smem_optin;
-        case 30: return fark_smem_bytes<3, 3, 3>() <= h->smem_optin;
+        case 30: return fark_smem_bytes<3, 4, 2>() <= h->smem_optin;
         case 40: case 50: case 60: return wc_far_smem(M) <= h->smem_optin;
         default: return false;
     }
@@ -2269,10 +2273,10 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
     switch (M) {
         case 10: fk.jz = fark_jz<1, 8>(); S_ = 8; break;
         case 20: fk.jz = fark_jz<2, 4>(); S_ = 4; break;
-        case 30: fk.jz = fark_jz<3, 3>(); S_ = 3; break;
+        case 30: fk.jz = fark_jz<3, 4>(); S_ = 4; break;
         case 40: fk.jz = fark_jz<4, 2>(); S_ = 2; break;
-        case 50: fk.jz = fark_jz<5, 2>(); S_ = 2; break;
-        case 60: fk.jz = fark_jz<6, 1>(); S_ = 1; break;
+        case 50: fk.jz = fark_jz<5, 3>(); S_ = 3; break;
+        case 60: fk.jz = fark_jz<6, 2>(); S_ = 2; break;
         default: return ss::set_err(h, SS_EARG, "transposed composite: unsupported width");
     }
     fk.nz = (M + fk.jz - 1) / fk.jz;
@@ -2292,10 +2296,10 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
     switch (M) {
         case 10: rc = launch_fark<1, 8>(h, grid, st, fk, S, W); break;
         case 20: rc = launch_fark<2, 4>(h, grid, st, fk, S, W); break;
-        case 30: rc = launch_fark<3, 3, 3>(h, grid, st, fk, S, W); break;
+        case 30: rc = launch_fark<3, 4, 2>(h, grid, st, fk, S, W); break;
         case 40: rc = launch_fark<4, 2, 3>(h, grid, st, fk, S, W); break;
-        case 50: rc = launch_fark<5, 2, 3>(h, grid, st, fk, S, W); break;
-        default: rc = launch_fark<6, 1, 4>(h, grid, st, fk, S, W); break;
+        case 50: rc = launch_fark<5, 3, 2>(h, grid, st, fk, S, W); break;
+        default: rc = launch_fark<6, 2, 2>(h, grid, st, fk, S, W); break;
     }
     if (rc) return rc;
     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * M * M * (double)sb, 8.0 * rows * (double)sb * M * K,
@@ -2383,10 +2387,10 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     switch (m) {
         case 10: fk.jz = fark_jz<1, 8>(); S_ = 8; break;
         case 20: fk.jz = fark_jz<2, 4>(); S_ = 4; break;
-        case 30: fk.jz = fark_jz<3, 3>(); S_ = 3; break;
+        case 30: fk.jz = fark_jz<3, 4>(); S_ = 4; break;
         case 40: fk.jz = fark_jz<4, 2>(); S_ = 2; break;
-        case 50: fk.jz = fark_jz<5, 2>(); S_ = 2; break;
-        case 60: fk.jz = fark_jz<6, 1>(); S_ = 1; break;
+        case 50: fk.jz = fark_jz<5, 3>(); S_ = 3; break;
+        case 60: fk.jz = fark_jz<6, 2>(); S_ = 2; break;
         default: return ss::set_err(h, SS_EARG, "transposed split far pass: unsupported m");
     }
     fk.nz = (m + fk.jz - 1) / fk.jz;
@@ -2399,10 +2403,10 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     switch (m) {
         case 10: rc = launch_fark<1, 8>(h, grid, st, fk, S, Wz); break;
         case 20: rc = launch_fark<2, 4>(h, grid, st, fk, S, Wz); break;
-        case 30: rc = launch_fark<3, 3, 3>(h, grid, st, fk, S, Wz); break;
+        case 30: rc = launch_fark<3, 4, 2>(h, grid, st, fk, S, Wz); break;
         case 40: rc = launch_fark<4, 2, 3>(h, grid, st, fk, S, Wz); break;
-        case 50: rc = launch_fark<5, 2, 3>(h, grid, st, fk, S, Wz); break;
-        default: rc = launch_fark<6, 1, 4>(h, grid, st, fk, S, Wz); break;
+        case 50: rc = launch_fark<5, 3, 2>(h, grid, st, fk, S, Wz); break;
+        default: rc = launch_fark<6, 2, 2>(h, grid, st, fk, S, Wz); break;
     }
     if (rc) return rc;
     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb, 8.0 * rows * (double)sb * m * K,
