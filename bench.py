@@ -617,6 +617,23 @@ def main(argv=None):
                       "failures": int((fail_t >= 0).sum().item())}
         del Xt, rhs
 
+    # ---- IRKA on the config-4 system (reduced order 20) ----
+    irka = None
+    if not args.no_reduced and cfg == 4 and rank == 0:
+        r_ord, iters = 20, 3
+        ss.irka_iterate(chf, r_ord, maxiter=1, fixed_iters=True, nb=32)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, ist = ss.irka_iterate(chf, r_ord, maxiter=iters, fixed_iters=True, nb=32)
+        torch.cuda.synchronize()
+        ms_i = (time.perf_counter() - t0) * 1e3 / iters
+        irka = {"op": f"irka_iterate (reduced order {r_ord}, {iters} fixed iterations; per iteration "
+                      f"{r_ord} reduced + {r_ord} transposed shifted solves, device bases and "
+                      "projections, host r x r pencil)",
+                "ms_per_iteration": ms_i, "shifted_solves_per_s": 2 * r_ord / (ms_i * 1e-3),
+                "timing": "host wall clock around the host-synchronous call (rank 0)",
+                "perturbations": len(ist.perturbations)}
+
     # ---- e2e through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -696,6 +713,7 @@ def main(argv=None):
                                "f_alg_per_shift": fa},
             "reduced": reduced,
             "transposed": transposed,
+            "irka": irka,
             "phase_seconds": {k: sec5[i] for i, k in enumerate(ss.counters.ALL_PHASES)},
             "reduction_ms": red_ms,
             "cpu_baseline": cpu,
