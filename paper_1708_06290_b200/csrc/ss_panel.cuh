@@ -63,9 +63,10 @@ constexpr int kPYin = 4;
 __host__ __device__ inline size_t pan_ws_doubles(int G) {
     return (size_t)G * kPBmax * 2 + (size_t)G + 8 + (size_t)G * kPBmax * kPYin;  // + V^T V partials
 }
-__host__ __device__ inline size_t pan_smem_bytes(int bw, int G, int nown_staged) {
-    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (size_t)kPTC * G + (size_t)kPBmax * kPYin +
-            (size_t)(kPT / 32) * 32 * kPYin + (size_t)2 * nown_staged * bw) * 8;
+__host__ __device__ inline size_t pan_smem_bytes(int bw, int G, int nown_staged, bool cl = false) {
+    return ((size_t)bw * bw + 3 * kPBmax + kPT / 32 + 8 + (cl ? 0 : (size_t)kPTC * G) + (size_t)kPBmax * kPYin +
+            (size_t)(kPT / 32) * 32 * kPYin + (cl ? (size_t)kPBmax * (2 + kPYin) + 8 : 0) +
+            (size_t)2 * nown_staged * bw) * 8;
 }
 
 // The CTA's own rows of V and Y, staged in shared memory when they fit
@@ -123,7 +124,7 @@ __device__ __forceinline__ void cta_sums(const double* part, int G, int nt, doub
 // S1(j): right update of column j from the completed mini-blocks (Y columns
 // t < jr), own rows; then the partials of V^T a_j (t < j)
 __device__ __forceinline__ void s1_right(const Pan& p, const Own& o, double* vrs, int j, int js, int rlo, int rhi,
-                                         double* ppart_c, int G) {
+                                         double* ppart_c, int pstride) {
     double* a = p.a0 + (int64_t)j * p.lda;
     const int jr = p.yext ? min(js, max(j - p.m + 1, 0)) : 0;
     if (jr > 0) {
@@ -144,19 +145,58 @@ __device__ __forceinline__ void s1_right(const Pan& p, const Own& o, double* vrs
         }
         __syncthreads();
     }
-    own_vdots(o, rlo, rhi, a, j, ppart_c, G);
+    own_vdots(o, rlo, rhi, a, j, ppart_c, pstride);
 }
+
+// Cross-CTA communication of the panel kernel.  GRID: every SM (cooperative
+// launch), partials in global scratch ([t][G]) gathered with cp.async, grid
+// barriers (1.2 us each on B200).  CLUSTER: one cluster of kPCl CTAs for
+// small panels (nk <= kPCl kPClRows): partials in each CTA's shared memory,
+// summed over the cluster through distributed shared memory in rank order,
+// hardware cluster barriers (0.24 us).  Both sum in a fixed order: every CTA
+// gets identical values and runs are reproducible.
+constexpr int kPCl = 16;        // CTAs in the cluster variant
+constexpr int kPClRows = 128;   // rows per CTA it covers (own V / Y rows staged in shared memory)
+
+template <bool CL>
+struct PanComm {
+    int G, cta;
+    double* gpart;  // GRID: global partials base of this array ([t][G]); CLUSTER: this CTA's smem array
+    double* pbuf;   // GRID: gather buffer (smem)
+    __device__ __forceinline__ void sync() const {
+        if constexpr (CL) cg::this_cluster().sync();
+        else cg::this_grid().sync();
+    }
+    // where this CTA writes partial t: out[t * stride()]
+    __device__ __forceinline__ double* out() const { return CL ? gpart : gpart + cta; }
+    __device__ __forceinline__ int stride() const { return CL ? 1 : G; }
+    // d[t] = sum over CTAs of partial t (after sync())
+    __device__ __forceinline__ void sums(int nt, double* d) const {
+        if constexpr (CL) {
+            cg::cluster_group cl = cg::this_cluster();
+            for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+                double s = 0.0;
+                for (int r = 0; r < G; ++r) s += cl.map_shared_rank(gpart, r)[t];
+                d[t] = s;
+            }
+        } else {
+            cta_sums(gpart, G, nt, d, pbuf);
+        }
+    }
+};
 
 // Y[:, ms:me] = (A0 V[:, ms:me] - Y[:, :ms] (V[:, :ms]^T V[:, ms:me])) T[ms:me, ms:me]
 // for the own rows (hessenberg.py:83-96 mini_boundaries; me - ms <= kPYin):
 // V^T V across CTAs (partials, one grid barrier, gathered sums), A0 V with
 // the warps splitting the trailing columns and lanes on rows (a fixed-order
 // combine in shared memory), the rest row-local.
-__device__ void yext_inline(const Pan& p, const Own& o, int ms, int me, int rlo, int rhi, int G, const double* Ts,
-                            int bw, double* vpart, double* vtv, double* avs, double* pbuf) {
-    cg::grid_group grid = cg::this_grid();
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cta = blockIdx.x;
+template <bool CL>
+__device__ void yext_inline(const Pan& p, const Own& o, int ms, int me, int rlo, int rhi, const PanComm<CL>& vc,
+                            const double* Ts, int bw, double* vtv, double* avs) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cw = me - ms, ne = ms * cw;
+    double* vpo = vc.out();
+    const int vst = vc.stride();
     // (1) V^T V partials: entry e = t + u ms (t < ms, u < cw), stored [e][G]
     for (int e = warp; e < ne; e += kPT / 32) {
         const int t = e % ms, u = e / ms;
@@ -166,7 +206,7 @@ __device__ void yext_inline(const Pan& p, const Own& o, int ms, int me, int rlo,
         for (int i = rlo + lane; i < rhi; i += 32) s = fma(vt[i], vu[i], s);
 #pragma unroll
         for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
-        if (lane == 0) vpart[(size_t)e * G + cta] = s;
+        if (lane == 0) vpo[(size_t)e * vst] = s;
     }
     // (2) A0 V for the own rows, 8 rows at a time: every thread takes trailing
     // columns c = tid, tid + 256, ... (the 8 rows of a column are contiguous:
@@ -213,9 +253,9 @@ __device__ void yext_inline(const Pan& p, const Own& o, int ms, int me, int rlo,
         }
         __syncthreads();
     }
-    grid.sync();
+    vc.sync();
     if (ne > 0) {
-        cta_sums(vpart, G, ne, vtv, pbuf);
+        vc.sums(ne, vtv);
         __syncthreads();
     }
     // (3) own rows: (A0 V - Y VtV) T, written to Y (and the staged copy)
@@ -245,8 +285,8 @@ __device__ void yext_inline(const Pan& p, const Own& o, int ms, int me, int rlo,
     __syncthreads();
 }
 
+template <bool CL>
 __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int stage) {
-    cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
     const int bw = p.bw, nk = p.nk;
     double* Ts = sm;               // bw x bw, col-major (ld bw)
@@ -256,9 +296,10 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     double* sc = red + kPT / 32;   // [8] tau, beta, scale
     double* vrs = sc + 8;          // [kPBmax] V row of the right update
     double* pbuf = vrs + kPBmax;   // [kPTC * G] cross-CTA partials (cta_sums)
-    double* vtv = pbuf + (size_t)kPTC * gridDim.x;  // [kPBmax * kPYin] V^T V of the Y extension
+    double* vtv = pbuf + (CL ? 0 : (size_t)kPTC * gridDim.x);  // [kPBmax * kPYin] V^T V of the Y extension
     double* avs = vtv + kPBmax * kPYin;             // [8 warps][32 rows][kPYin] A0 V partials
-    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int cta = CL ? (int)cg::this_cluster().block_rank() : blockIdx.x;
     const int rlo = (int)((int64_t)nk * cta / G), rhi = (int)((int64_t)nk * (cta + 1) / G);
     const int nown = rhi - rlo;
     Own o{p.V, p.Y, 0, p.ldv};
@@ -266,7 +307,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     if (stage) {
         // own rows of V (columns < jb; column j written here as it is formed)
         // and Y (columns < js, read-only in this kernel)
-        Vs = avs + (kPT / 32) * 32 * kPYin;
+        Vs = avs + (kPT / 32) * 32 * kPYin + (CL ? kPBmax * (2 + kPYin) + 8 : 0);
         double* Ys = Vs + (size_t)nown * bw;
         for (int e = tid; e < nown * jb; e += kPT) {
             const int r = e % nown, t = e / nown;
@@ -279,11 +320,14 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
             }
         o = Own{Vs, Ys, rlo, nown};
     }
-    double* ppart = p.ws;                        // [kPBmax][G]
-    double* qpart = ppart + (size_t)G * kPBmax;  // [kPBmax][G]
-    double* spart = qpart + (size_t)G * kPBmax;  // [G]
-    double* scal = spart + G;                    // [8]: alpha
-    double* vpart = scal + 8;                    // [kPBmax * kPYin][G] V^T V partials
+    // partial sums: GRID in global scratch ([t][G]), CLUSTER in shared memory
+    double* gp = p.ws;
+    double* scal = gp + (size_t)G * kPBmax * 2 + G;  // [8]: alpha (global in both variants)
+    double* cp = avs + (kPT / 32) * 32 * kPYin;      // CLUSTER: [kPBmax] p, [kPBmax] q, [8] s, [kPBmax kPYin] v
+    const PanComm<CL> pc{G, cta, CL ? cp : gp, pbuf};
+    const PanComm<CL> qc{G, cta, CL ? cp + kPBmax : gp + (size_t)G * kPBmax, pbuf};
+    const PanComm<CL> sc_{G, cta, CL ? cp + 2 * kPBmax : gp + (size_t)G * kPBmax * 2, pbuf};
+    const PanComm<CL> vc{G, cta, CL ? cp + 2 * kPBmax + 8 : scal + 8, pbuf};
     // T columns of the earlier mini-blocks (upper triangle)
     for (int e = tid; e < bw * bw; e += kPT) {
         const int r = e % bw, c = e / bw;
@@ -291,12 +335,12 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
     }
     __syncthreads();
     int ms = js;  // first column of the current mini-block
-    s1_right(p, o, vrs, js, ms, rlo, rhi, ppart + cta, G);
-    grid.sync();
+    s1_right(p, o, vrs, js, ms, rlo, rhi, pc.out(), pc.stride());
+    pc.sync();
     for (int j = js; j < jb; ++j) {
         double* a = p.a0 + (int64_t)j * p.lda;
         // ---- S2: w = T^T (sum of partials); a -= V w; squares below row j ----
-        cta_sums(ppart, G, j, d, pbuf);
+        pc.sums(j, d);
         __syncthreads();
         for (int t = tid; t < j; t += kPT) {
             double s = 0.0;
@@ -326,11 +370,11 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
         if (tid == 0) {
             double t = 0.0;
             for (int q = 0; q < kPT / 32; ++q) t += red[q];
-            spart[cta] = t;
+            sc_.out()[0] = t;
         }
-        grid.sync();
+        sc_.sync();
         // ---- S3: Householder scalars (householder_vector, kernels.py:74-99) ----
-        cta_sums(spart, G, 1, red, pbuf);
+        sc_.sums(1, red);
         __syncthreads();
         if (tid == 0) {
             const double sigma = red[0];
@@ -364,13 +408,13 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
             else if (i > j) a[i] = 0.0;
         }
         __syncthreads();
-        own_vdots(o, rlo, rhi, vj, j, qpart + cta, G);
+        own_vdots(o, rlo, rhi, vj, j, qc.out(), qc.stride());
         // in-kernel Y extension: a mini-block ends at this column
         const bool ybnd = p.yin && ((j + 1 - ms) == p.m || j + 1 == jb);
-        if (j + 1 < jb && !ybnd) s1_right(p, o, vrs, j + 1, ms, rlo, rhi, ppart + cta, G);
-        grid.sync();
+        if (j + 1 < jb && !ybnd) s1_right(p, o, vrs, j + 1, ms, rlo, rhi, pc.out(), pc.stride());
+        qc.sync();
         // ---- T column (kernels.py:156-160; every CTA, same order) ----
-        cta_sums(qpart, G, j, d, pbuf);
+        qc.sums(j, d);
         __syncthreads();
         for (int r = tid; r < j; r += kPT) {
             double s = 0.0;
@@ -380,12 +424,12 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
         if (tid == 0) Ts[j + j * bw] = tau;
         __syncthreads();
         if (ybnd) {
-            yext_inline(p, o, ms, j + 1, rlo, rhi, G, Ts, bw, vpart, vtv, avs, pbuf);
+            yext_inline<CL>(p, o, ms, j + 1, rlo, rhi, vc, Ts, bw, vtv, avs);
             ms = j + 1;
             if (j + 1 < jb) {
                 __syncthreads();
-                s1_right(p, o, vrs, j + 1, ms, rlo, rhi, ppart + cta, G);
-                grid.sync();
+                s1_right(p, o, vrs, j + 1, ms, rlo, rhi, pc.out(), pc.stride());
+                pc.sync();
             }
         }
     }
@@ -394,6 +438,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(Pan p, int js, int jb, int sta
             const int r = e % bw, c = js + e / bw;
             p.T[r + (int64_t)c * p.ldt] = r <= c ? Ts[r + c * bw] : 0.0;
         }
+    if constexpr (CL) cg::this_cluster().sync();  // no CTA leaves while its shared memory may be read
 }
 
 }  // namespace ssr

@@ -176,19 +176,42 @@ int apply_left(Ctx& x, double* M, int64_t ldm, int mcols, const double* V, int64
 int panel_cols(Ctx& x, ssr::Pan& p, int js, int jb) {
     static ss::DevMask configured;  // devices configured
     if (!configured.has(x.h)) {
-        SS_CUDA_TRY(x.h, cudaFuncSetAttribute(ssr::k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SS_CUDA_TRY(x.h, cudaFuncSetAttribute(ssr::k_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)x.h->smem_optin));
+        SS_CUDA_TRY(x.h, cudaFuncSetAttribute(ssr::k_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)x.h->smem_optin));
+        SS_CUDA_TRY(x.h, cudaFuncSetAttribute(ssr::k_panel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         configured.set(x.h);
     }
+    // small panels: one cluster of kPCl CTAs (hardware cluster barriers and
+    // distributed-shared-memory sums); large: every SM, grid barriers
+    // (not with the in-kernel Y extension: its A0 V stream wants every SM)
+    const bool cl = !p.yin && p.nk <= ssr::kPCl * ssr::kPClRows;
+    const int G = cl ? ssr::kPCl : x.h->num_sms;
     // the CTAs' own rows of V and Y in shared memory when they fit
-    const int nown = (p.nk + x.h->num_sms - 1) / x.h->num_sms;
-    const int G = x.h->num_sms;
-    int stage = ssr::pan_smem_bytes(p.bw, G, nown) <= x.h->smem_optin ? 1 : 0;
-    const size_t smem = ssr::pan_smem_bytes(p.bw, G, stage ? nown : 0);
+    const int nown = (p.nk + G - 1) / G;
+    int stage = ssr::pan_smem_bytes(p.bw, G, nown, cl) <= x.h->smem_optin ? 1 : 0;
+    const size_t smem = ssr::pan_smem_bytes(p.bw, G, stage ? nown : 0, cl);
     if (smem > x.h->smem_optin) return ss::set_err(x.h, SS_EARG, "reduction: panel too wide for shared memory");
-    void* args[] = {(void*)&p, (void*)&js, (void*)&jb, (void*)&stage};
-    SS_CUDA_TRY(x.h, cudaLaunchCooperativeKernel((const void*)ssr::k_panel, dim3(G), dim3(ssr::kPT),
-                                                 args, smem, x.st));
+    if (cl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ssr::kPCl);
+        cfg.blockDim = dim3(ssr::kPT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = x.st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = ssr::kPCl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SS_CUDA_TRY(x.h, cudaLaunchKernelEx(&cfg, ssr::k_panel<true>, p, js, jb, stage));
+    } else {
+        void* args[] = {(void*)&p, (void*)&js, (void*)&jb, (void*)&stage};
+        SS_CUDA_TRY(x.h, cudaLaunchCooperativeKernel((const void*)ssr::k_panel<false>, dim3(G), dim3(ssr::kPT),
+                                                     args, smem, x.st));
+    }
     x.h->launches++;
     return SS_OK;
 }
