@@ -49,6 +49,8 @@ int launch_update_tr(ss_handle* h, ssd::UpdDims u, int rows, double2* S, const d
 int tr_fold(ss_handle* h, cudaStream_t st, int M, int mc, int K, int x, int nb, bool first, int sb,
             const double2* P, double2* W, int64_t wstride);
 bool tr_far_supported(ss_handle* h, int M);
+int wsuffix(ss_handle* h, cudaStream_t st, int sb, int g, const int* x, const int* nb, int M, int mc, int K,
+            const double2* P, int64_t slab, double2* W, int64_t wstride);
 bool tr_split_supported(ss_handle* h, int m);
 int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, int64_t lda,
                  const double2* shifts, int sb, double2* S, int64_t LDS, int rlo, int r0_all, int c0, int K,
@@ -742,7 +744,10 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     const int64_t wstride = comp ? (int64_t)(Kmax + M) * M : 0;
     const int64_t wzstride = split ? (int64_t)(Kmax + m) * m : 0;                    // W of z2
     const int64_t gstride = split ? (int64_t)(Kmax + 1) * kFkmShiftsLq : 0;          // w column, per group
-    const size_t per_shift = (size_t)LDS * ms * 16 + (size_t)(nb0 + ms) * ms * 16 + (size_t)wstride * 16 +
+    // composites keep every window's P (the composite is built from all of
+    // them at its end, k_wsuffix): G slabs
+    const int nslab = comp ? G : 1;
+    const size_t per_shift = (size_t)LDS * ms * 16 + (size_t)nslab * (nb0 + ms) * ms * 16 + (size_t)wstride * 16 +
                              (size_t)wzstride * 16 + (size_t)(Kmax + 1) * (split ? 16 : 0) + 8 + 64;
     int64_t sb_max = std::min<int64_t>(batch > 0 ? batch : s, s);
     if (per_shift * (size_t)sb_max + 256 > h->ws_bytes) {  // query only to grow (slow driver call)
@@ -759,7 +764,8 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
     }
     double2* Sb = (double2*)h->ws;
     double2* Pb = Sb + (size_t)sb_max * ms * LDS;
-    double2* Wb = Pb + (size_t)sb_max * (nb0 + ms) * ms;
+    const int64_t pslab = (int64_t)sb_max * (nb0 + ms) * ms;  // one window's P of the batch
+    double2* Wb = Pb + (size_t)nslab * pslab;
     double2* Wzb = Wb + (size_t)sb_max * wstride;
     double2* Wwb = Wzb + (size_t)sb_max * wzstride;  // ceil(sb / 80) groups (per_shift holds Kmax + 1 each + slack)
     const size_t ngroups_max = split ? (size_t)((sb_max + kFkmShiftsLq - 1) / kFkmShiftsLq) : 0;
@@ -807,13 +813,16 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
             const int c0 = k0 + m;                       // first panel column
             const int kend = k0w[g - 1] + nbw[g - 1];    // first far row
             const int K = kend - k0;                     // panel columns of the composite
+            int xw[64];
             for (int b = 0; b < g; ++b) {
                 LqStep ls;
                 ls.k0 = k0w[b];
                 ls.nb = nbw[b];
                 ls.c0 = k0w[b] + m;
+                xw[b] = k0w[b] - k0;
+                double2* Pw = Pb + (size_t)b * pslab;  // this window's P slab
                 cudaEvent_t ev = ss::timing_begin(h, st);
-                int rc = launch_lq(h, m, sb, st, d, ls, Sb, Pb);
+                int rc = launch_lq(h, m, sb, st, d, ls, Sb, Pw);
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_RQ);
                 const int rows = kend - (ls.k0 + ls.nb);  // near: the composite's rows below this window
@@ -839,13 +848,15 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
                     u.lz0 = ls.k0 + ls.nb + (m - u.mnb);
                     u.lzp = ls.nb - u.mnb;
                     ev = ss::timing_begin(h, st);
-                    rc = ss::launch_update_tr(h, u, rows, Sb, Pb, st);
+                    rc = ss::launch_update_tr(h, u, rows, Sb, Pw, st);
                     if (rc) return rc;
                     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * M * M * (double)sb,
                                    8.0 * rows * (double)sb * M * ls.nb, 4.0 * mp * (double)rows * ls.nb * sb);
                 }
-                ev = ss::timing_begin(h, st);
-                rc = ss::tr_fold(h, st, M, mp, K, ls.k0 - k0, ls.nb, b == 0, sb, Pb, Wb, wstride);
+            }
+            {
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                int rc = ss::wsuffix(h, st, sb, g, xw, nbw, M, mp, K, Pb, pslab, Wb, wstride);
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
             }

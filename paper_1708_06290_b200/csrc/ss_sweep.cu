@@ -905,6 +905,75 @@ __global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool
     }
 }
 
+// The composite from ALL its windows' P at once (instead of folding window by
+// window, which multiplies the earlier windows' W12 rows again for every
+// later window: O(g^2) row products).  In processing order b = 0 .. g-1:
+//     W12[x_b, x_b + nb_b) = P12_b S_b,  S_b = P22_{b+1} ... P22_{g-1},
+//     W22 = P22_0 ... P22_{g-1}  (= S_{-1})
+// built backward with S in shared memory; one CTA per shift.  Only the first
+// mc <= M columns are carried (the padding of P / W is zero).
+constexpr int kWsufMax = 64;  // windows per composite (the transposed G <= 64)
+struct WsufArgs {
+    int g, M, mc, K;
+    int x[kWsufMax], nb[kWsufMax];
+    const double2* P;   // window b, shift l: P + b * slab + l * (nb_b + M) M
+    int64_t slab;
+    double2* W;         // shift l: W + l * wstride, rows of M
+    int64_t wstride;
+};
+__host__ __device__ inline size_t wsuf_smem(int M) { return (size_t)3 * M * M * 16; }
+
+__global__ void __launch_bounds__(256) k_wsuffix(WsufArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int M = a.M, mc = a.mc, l = blockIdx.x, tid = threadIdx.x;
+    double2* Sm = reinterpret_cast<double2*>(smem);  // S (M x M, only mc x mc used)
+    double2* Sn = Sm + M * M;                        // next S
+    double2* P22 = Sn + M * M;
+    double2* Wl = a.W + (int64_t)l * a.wstride;
+    for (int e = tid; e < mc * mc; e += blockDim.x) Sm[(e / mc) * M + e % mc] = make_double2(e / mc == e % mc ? 1.0 : 0.0, 0.0);
+    for (int b = a.g - 1; b >= 0; --b) {
+        const int nb = a.nb[b];
+        const double2* Pl = a.P + b * a.slab + (int64_t)l * (nb + M) * M;
+        for (int e = tid; e < mc * mc; e += blockDim.x) P22[(e / mc) * M + e % mc] = Pl[(int64_t)(nb + e / mc) * M + e % mc];
+        __syncthreads();
+        // W12 rows of window b: P12_b S
+        for (int e = tid; e < nb * mc; e += blockDim.x) {
+            const int r = e / mc, c = e - r * mc;
+            const double2* pr = Pl + (int64_t)r * M;
+            double2 a0 = cz(), a1 = cz();
+            int j = 0;
+            for (; j + 1 < mc; j += 2) {
+                a0 = cfma(pr[j], Sm[j * M + c], a0);
+                a1 = cfma(pr[j + 1], Sm[(j + 1) * M + c], a1);
+            }
+            if (j < mc) a0 = cfma(pr[j], Sm[j * M + c], a0);
+            Wl[(int64_t)(a.x[b] + r) * M + c] = cadd(a0, a1);
+        }
+        for (int e = tid; e < nb * (M - mc); e += blockDim.x)  // zero padding (no NaN can arise there)
+            Wl[(int64_t)(a.x[b] + e / (M - mc)) * M + mc + e % (M - mc)] = cz();
+        // S <- P22_b S
+        for (int e = tid; e < mc * mc; e += blockDim.x) {
+            const int r = e / mc, c = e - r * mc;
+            double2 a0 = cz(), a1 = cz();
+            int j = 0;
+            for (; j + 1 < mc; j += 2) {
+                a0 = cfma(P22[r * M + j], Sm[j * M + c], a0);
+                a1 = cfma(P22[r * M + j + 1], Sm[(j + 1) * M + c], a1);
+            }
+            if (j < mc) a0 = cfma(P22[r * M + j], Sm[j * M + c], a0);
+            Sn[r * M + c] = cadd(a0, a1);
+        }
+        __syncthreads();
+        for (int e = tid; e < mc * mc; e += blockDim.x) Sm[(e / mc) * M + e % mc] = Sn[(e / mc) * M + e % mc];
+        __syncthreads();
+    }
+    // W22 = S (mc x mc block; the rest of the M x M block is zero padding)
+    for (int e = tid; e < M * M; e += blockDim.x) {
+        const int r = e / M, c = e % M;
+        Wl[(int64_t)(a.K + r) * M + c] = (r < mc && c < mc) ? Sm[r * M + c] : cz();
+    }
+}
+
 // m = 1: the same fold elementwise in the group layout (row-major across the
 // 80 shifts of a group: coalesced), one thread per (row, shift).
 __global__ void __launch_bounds__(256) k_wcomp1(int K, int x, int nb, bool first, int sb, int64_t pstride,
@@ -2201,6 +2270,33 @@ __global__ void __launch_bounds__(256) k_tr_wsplit(int m, int K, int sb, const d
         else if (c == m && r == K + m) Ww[grp * gstride + (int64_t)K * kFkmShifts + q] = Wl[e];  // W22[m][m]
     }
     (void)sb;
+}
+
+// the composite W of g windows from their P slabs (k_wsuffix)
+int wsuffix(ss_handle* h, cudaStream_t st, int sb, int g, const int* x, const int* nb, int M, int mc, int K,
+            const double2* P, int64_t slab, double2* W, int64_t wstride) {
+    static ss::DevMask configured;
+    if (!configured.has(h)) {
+        SS_CUDA_TRY(h, allow_max_smem(h, k_wsuffix));
+        configured.set(h);
+    }
+    if (g > kWsufMax) return ss::set_err(h, SS_EARG, "composite: too many windows");
+    WsufArgs a;
+    a.g = g;
+    a.M = M;
+    a.mc = mc;
+    a.K = K;
+    for (int b = 0; b < g; ++b) {
+        a.x[b] = x[b];
+        a.nb[b] = nb[b];
+    }
+    a.P = P;
+    a.slab = slab;
+    a.W = W;
+    a.wstride = wstride;
+    k_wsuffix<<<sb, 256, wsuf_smem(M), st>>>(a);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
 }
 
 // state widths the composite far pass supports (M = 10 NCB)
