@@ -46,8 +46,7 @@ namespace ss {
 // ss_sweep.cu: the window-update kernel on the [A^T; -I] panel, and the
 // composite fold / K-streamed far pass
 int launch_update_tr(ss_handle* h, ssd::UpdDims u, int rows, double2* S, const double2* P, cudaStream_t st);
-int tr_fold(ss_handle* h, cudaStream_t st, int M, int mc, int K, int x, int nb, bool first, int sb,
-            const double2* P, double2* W, int64_t wstride);
+
 bool tr_far_supported(ss_handle* h, int M);
 int wsuffix(ss_handle* h, cudaStream_t st, int sb, int g, const int* x, const int* nb, int M, int mc, int K,
             const double2* P, int64_t slab, double2* W, int64_t wstride);

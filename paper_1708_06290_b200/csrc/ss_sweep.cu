@@ -841,9 +841,6 @@ static int launch_wc_far(ss_handle* h, int m, int grid, cudaStream_t st, const F
     }
 }
 
-constexpr int kWcRows = 32;  // W rows per k_wcomp CTA
-__host__ __device__ inline size_t wcomp_smem(int m) { return (size_t)(m * m + kWcRows * m) * 16; }
-
 // Composite W layout: element (row, c) of shift l at
 //   W + (l / G) gs + (l % G) ls + row rs + c
 // (m > 1: G = 1, gs = per-shift stride, rs = m, j-major rows of one shift;
@@ -854,56 +851,6 @@ struct WcLayout {
     int64_t gs, ls, rs;
     __host__ __device__ int64_t off(int l) const { return (int64_t)(l / G) * gs + (int64_t)(l % G) * ls; }
 };
-
-// Fold window P (rows [0, nb) P12, [nb, nb + m) P22; P_l at P + l pstride)
-// into the composite W of shift l: rows [x, x + nb) <- P12; rows
-// [x + nb, K + m) <- rows P22 (first window of the composite, x + nb == K:
-// W22 <- P22).  grid (sb, row chunks).
-// mc <= m: columns actually carried (the transposed sweep pads its m + 1 state
-// columns to m = 10 ceil((m + 1) / 10); the padding of P and W is zero and
-// stays zero, so only mc columns are multiplied)
-__global__ void __launch_bounds__(256) k_wcomp(int m, int K, int x, int nb, bool first, int64_t pstride,
-                                               const double2* __restrict__ P, WcLayout lw,
-                                               double2* __restrict__ W, int ra, int rb, int mc) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double2* P22 = reinterpret_cast<double2*>(smem);  // m x m
-    double2* Wr = P22 + m * m;                        // [kWcRows][m]
-    const int l = blockIdx.x, tid = threadIdx.x;
-    const double2* Pl = P + (int64_t)l * pstride;
-    double2* Wl = W + lw.off(l);
-    const int64_t rs = lw.rs;
-    // rows multiplied by P22: the earlier windows' W12 rows [ra, rb) (below
-    // the window in the forward sweep, above it in the transposed one), then
-    // W22 (rows [K, K + m))
-    const int n1 = rb - ra, nrows = n1 + m;
-    auto wrow = [&](int q) { return q < n1 ? ra + q : K + (q - n1); };
-    const int c0 = blockIdx.y * kWcRows;
-    if (blockIdx.y == 0)
-        for (int e = tid; e < nb * m; e += blockDim.x) Wl[(int64_t)(x + e / m) * rs + e % m] = Pl[e];
-    if (first) {
-        if (blockIdx.y == 0)
-            for (int e = tid; e < m * m; e += blockDim.x)
-                Wl[(int64_t)(K + e / m) * rs + e % m] = Pl[(int64_t)nb * m + e];
-        return;
-    }
-    if (c0 >= nrows) return;
-    const int rc = min(kWcRows, nrows - c0);
-    for (int e = tid; e < m * m; e += blockDim.x) P22[e] = Pl[(int64_t)nb * m + e];
-    for (int e = tid; e < rc * m; e += blockDim.x) Wr[e] = Wl[(int64_t)wrow(c0 + e / m) * rs + e % m];
-    __syncthreads();
-    for (int e = tid; e < rc * mc; e += blockDim.x) {
-        const int r = e / mc, c = e - r * mc;
-        const double2* wr = Wr + r * m;
-        double2 a0 = cz(), a1 = cz();
-        int j = 0;
-        for (; j + 1 < mc; j += 2) {
-            a0 = cfma(wr[j], P22[j * m + c], a0);
-            a1 = cfma(wr[j + 1], P22[(j + 1) * m + c], a1);
-        }
-        if (j < mc) a0 = cfma(wr[j], P22[j * m + c], a0);
-        Wl[(int64_t)wrow(c0 + r) * rs + c] = cadd(a0, a1);
-    }
-}
 
 // The composite from ALL its windows' P at once (instead of folding window by
 // window, which multiplies the earlier windows' W12 rows again for every
@@ -921,56 +868,103 @@ struct WsufArgs {
     double2* W;         // shift l: W + l * wstride, rows of M
     int64_t wstride;
 };
-__host__ __device__ inline size_t wsuf_smem(int M) { return (size_t)3 * M * M * 16; }
+// Both products of window b are ONE (nb + M) x M times M x M product:
+// [W12_b; S_new] = P_b S.  Register-tiled: each thread owns 4 x 4 outputs
+// (rows rt + nr i, columns ct + nc k: interleaved, so a warp's shared loads
+// of one k are contiguous) with P_b and S staged in shared memory (row
+// length LS = 4 ceil(M / 4) + 1: odd in 16-byte units, adjacent rows in
+// different banks; zero padded).  Tiles are numbered S rows first, so a
+// thread holds at most one S tile in registers across the barrier that
+// precedes the in-place S update (M <= 64: ceil(M / 4)^2 <= kWsT).
+constexpr int kWsT = 384;
+__host__ __device__ inline int wsuf_nc(int M) { return (M + 3) >> 2; }
+__host__ __device__ inline size_t wsuf_smem(int M, int nbmax) {
+    const int Q = 4 * wsuf_nc(M), LS = Q + 1;
+    return ((size_t)(nbmax + 3 + Q) * LS + (size_t)Q * LS) * 16;
+}
 
-__global__ void __launch_bounds__(256) k_wsuffix(WsufArgs a) {
+__global__ void __launch_bounds__(kWsT) k_wsuffix(WsufArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int M = a.M, mc = a.mc, l = blockIdx.x, tid = threadIdx.x;
-    double2* Sm = reinterpret_cast<double2*>(smem);  // S (M x M, only mc x mc used)
-    double2* Sn = Sm + M * M;                        // next S
-    double2* P22 = Sn + M * M;
+    const int nc = wsuf_nc(M), Q = 4 * nc, LS = Q + 1, nS = nc * nc;
+    double2* S = reinterpret_cast<double2*>(smem);  // Q x LS (only mc x mc nonzero)
+    double2* Ps = S + Q * LS;                       // (nb + Q) x LS
     double2* Wl = a.W + (int64_t)l * a.wstride;
-    for (int e = tid; e < mc * mc; e += blockDim.x) Sm[(e / mc) * M + e % mc] = make_double2(e / mc == e % mc ? 1.0 : 0.0, 0.0);
-    for (int b = a.g - 1; b >= 0; --b) {
-        const int nb = a.nb[b];
-        const double2* Pl = a.P + b * a.slab + (int64_t)l * (nb + M) * M;
-        for (int e = tid; e < mc * mc; e += blockDim.x) P22[(e / mc) * M + e % mc] = Pl[(int64_t)(nb + e / mc) * M + e % mc];
-        __syncthreads();
-        // W12 rows of window b: P12_b S
-        for (int e = tid; e < nb * mc; e += blockDim.x) {
-            const int r = e / mc, c = e - r * mc;
-            const double2* pr = Pl + (int64_t)r * M;
-            double2 a0 = cz(), a1 = cz();
-            int j = 0;
-            for (; j + 1 < mc; j += 2) {
-                a0 = cfma(pr[j], Sm[j * M + c], a0);
-                a1 = cfma(pr[j + 1], Sm[(j + 1) * M + c], a1);
-            }
-            if (j < mc) a0 = cfma(pr[j], Sm[j * M + c], a0);
-            Wl[(int64_t)(a.x[b] + r) * M + c] = cadd(a0, a1);
-        }
-        for (int e = tid; e < nb * (M - mc); e += blockDim.x)  // zero padding (no NaN can arise there)
-            Wl[(int64_t)(a.x[b] + e / (M - mc)) * M + mc + e % (M - mc)] = cz();
-        // S <- P22_b S
-        for (int e = tid; e < mc * mc; e += blockDim.x) {
-            const int r = e / mc, c = e - r * mc;
-            double2 a0 = cz(), a1 = cz();
-            int j = 0;
-            for (; j + 1 < mc; j += 2) {
-                a0 = cfma(P22[r * M + j], Sm[j * M + c], a0);
-                a1 = cfma(P22[r * M + j + 1], Sm[(j + 1) * M + c], a1);
-            }
-            if (j < mc) a0 = cfma(P22[r * M + j], Sm[j * M + c], a0);
-            Sn[r * M + c] = cadd(a0, a1);
-        }
-        __syncthreads();
-        for (int e = tid; e < mc * mc; e += blockDim.x) Sm[(e / mc) * M + e % mc] = Sn[(e / mc) * M + e % mc];
-        __syncthreads();
+    for (int e = tid; e < Q * LS; e += kWsT) {
+        const int r = e / LS, c = e - r * LS;
+        S[e] = make_double2(r == c && r < mc ? 1.0 : 0.0, 0.0);
     }
-    // W22 = S (mc x mc block; the rest of the M x M block is zero padding)
-    for (int e = tid; e < M * M; e += blockDim.x) {
-        const int r = e / M, c = e % M;
-        Wl[(int64_t)(a.K + r) * M + c] = (r < mc && c < mc) ? Sm[r * M + c] : cz();
+    for (int b = a.g - 1; b >= 0; --b) {
+        const int nb = a.nb[b], R = nb + M, nrw = (nb + 3) >> 2;
+        const double2* Pl = a.P + b * a.slab + (int64_t)l * R * M;
+        // rows [0, 4 nrw) hold W12 (zero beyond nb), rows [4 nrw, 4 nrw + Q)
+        // P22 (zero beyond M)
+        const int W0 = 4 * nrw;
+        for (int e = tid; e < (W0 + Q) * LS; e += kWsT) {
+            const int r = e / LS, c = e - r * LS;
+            const int pr = r < W0 ? (r < nb ? r : -1) : (r - W0 < M ? nb + r - W0 : -1);
+            Ps[e] = (pr >= 0 && c < M) ? Pl[(int64_t)pr * M + c] : cz();
+        }
+        __syncthreads();
+        const int ntiles = nS + nrw * nc;
+        double2 keep[4][4];
+        bool has_s = false;
+        int ks_r = 0, ks_c = 0;
+        for (int t = tid; t < ntiles; t += kWsT) {
+            const bool st = t < nS;
+            const int u = st ? t : t - nS;
+            const int rt = u / nc, ct = u - rt * nc, nr = st ? nc : nrw;
+            const double2* pr = Ps + (st ? W0 : 0) * LS + rt * LS;
+            double2 acc[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[i][k] = cz();
+            for (int j = 0; j < mc; ++j) {
+                double2 pa[4], sv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pa[i] = pr[i * nr * LS + j];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sv[k] = S[j * LS + ct + nc * k];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[i][k] = cfma(pa[i], sv[k], acc[i][k]);
+            }
+            if (st) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) keep[i][k] = acc[i][k];
+                has_s = true;
+                ks_r = rt;
+                ks_c = ct;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = rt + nrw * i;
+                    if (r >= nb) continue;
+                    double2* w = Wl + (int64_t)(a.x[b] + r) * M;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (ct + nc * k < M) w[ct + nc * k] = acc[i][k];
+                }
+            }
+        }
+        __syncthreads();  // every read of S and Ps done
+        if (has_s) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) S[(ks_r + nc * i) * LS + ks_c + nc * k] = keep[i][k];
+        }
+        // (the next window's staging barrier orders these writes)
+    }
+    __syncthreads();
+    // W22 = S (the padding rows / columns of S are zero)
+    for (int e = tid; e < M * M; e += kWsT) {
+        const int r = e / M, c = e - r * M;
+        Wl[(int64_t)(a.K + r) * M + c] = S[r * LS + c];
     }
 }
 
@@ -1063,6 +1057,13 @@ void account_ref_flops(ss_handle* h, int sb, int n, int m, int ptop, int nb0) {
         k -= nb;
     }
 }
+
+}  // namespace
+namespace ss {
+int wsuffix(ss_handle* h, cudaStream_t st, int sb, int g, const int* x, const int* nb, int M, int mc, int K,
+            const double2* P, int64_t slab, double2* W, int64_t wstride);
+}
+namespace {
 
 int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs B, int nb0,
                  int64_t LDZ, double rtol, bool use_house, const UpdTile& tile, bool two_level,
@@ -1311,18 +1312,17 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     }
     if (wc) {
         // ---- window composites (wide windows: k_rq_big + near k_update +
-        // k_wcomp per window, one k_fark per composite) ----
+        // k_wsuffix per composite (m = 1: k_wcomp1 per window), one k_fark per
+        // composite) ----
         account_ref_flops(h, sb, n, m, ptop, nb0);  // the reference's stack
         WcShape wsh;
         wc_shape(m, wsh);
         // composite W layout (k_fark: per shift j-major; m = 1, k_farkm:
         // groups of 80 shifts side by side)
         const int64_t wstride = m == 1 ? (int64_t)(kWcWin * nb0 + 1) * kFkmShifts : (int64_t)(kWcWin * nb0 + m) * m;
-        const WcLayout lw = m == 1 ? WcLayout{kFkmShifts, wstride, 1, kFkmShifts} : WcLayout{1, wstride, 0, m};
         static ss::DevMask configured;  // devices configured
         if (!configured.has(h)) {
             SS_CUDA_TRY(h, allow_max_smem(h, k_rq_big));
-            SS_CUDA_TRY(h, allow_max_smem(h, k_wcomp));
             configured.set(h);
         }
         while (k >= m + 1) {
@@ -1340,8 +1340,14 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             const int c0 = ktop - m - nbtop;          // first panel column of the composite
             const int K = (k - m) - c0;               // its columns
             const int r0G = ptop + ktop - nbtop;      // first row of its top window
+            // m > 1: every window keeps its P (slab b), the composite is built
+            // once at the end (k_wsuffix); m = 1 folds window by window
+            const int64_t pslab = (int64_t)sb * (nb0 + m) * m;
+            int xw[kWcWin];
             for (int b = 0; b < g; ++b) {
                 const int nb = nbw[b], r0 = ptop + kw[b] - nb, cw = kw[b] - m - nb, nc = nb + m;
+                double2* const Pw = m == 1 ? B.P : B.P + b * pslab;
+                xw[b] = cw - c0;
                 int rc = feed_wait(h, feed, st);  // this window's panel columns
                 if (rc) return rc;
                 cudaEvent_t ev = ss::timing_begin(h, st);
@@ -1361,7 +1367,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (m == 1)
                     k_rq_m1<<<(sb + 4 * kM1Warps - 1) / (4 * kM1Warps), 32 * kM1Warps, 0, st>>>(rd, B.Z, B.P);
                 else
-                    k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(nb, m), st>>>(rd, B.Z, B.P);
+                    k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(nb, m), st>>>(rd, B.Z, Pw);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_RQ);
                 if (r0 > r0G && m == 1) {
@@ -1441,23 +1447,24 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                     dim3 gu((unsigned)((rows + kUpdRows - 1) / kUpdRows), (unsigned)((sb + u.SG - 1) / u.SG));
                     ev = ss::timing_begin(h, st);
                     rc = launch_update(h, tile, gu, 32 * u.S * nws * u.ksplit, upd_smem_bytes(nb, m, u.S), st, u,
-                                       B.Z, B.Z, B.P);
+                                       B.Z, B.Z, Pw);
                     if (rc) return rc;
                     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
                                    8.0 * rows * (double)sb * m * nb, 4.0 * m * (double)rows * nb * sb);
                 }
-                ev = ss::timing_begin(h, st);
-                const int nrows = K + m - (cw - c0 + nb);
                 if (m == 1) {
+                    ev = ss::timing_begin(h, st);
                     const int64_t tot = (int64_t)(K + 1 - (cw - c0)) * kFkmShifts * ((sb + kFkmShifts - 1) / kFkmShifts);
                     const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 8 * (int64_t)h->num_sms);
                     k_wcomp1<<<blocks, 256, 0, st>>>(K, cw - c0, nb, b == 0, sb, (int64_t)nc, B.P, wstride, B.W);
-                } else {
-                    dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
-                    k_wcomp<<<gc, 256, wcomp_smem(m), st>>>(m, K, cw - c0, nb, b == 0, (int64_t)nc * m, B.P,
-                                                            lw, B.W, cw - c0 + nb, K, m);
+                    SS_LAUNCH_CHECK(h);
+                    ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
                 }
-                SS_LAUNCH_CHECK(h);
+            }
+            if (m > 1) {
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                int rc = ss::wsuffix(h, st, sb, g, xw, nbw, m, m, K, B.P, pslab, B.W, wstride);
+                if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
             }
             // far rows [0, r0G): one K-streamed pass over the composite
@@ -2013,7 +2020,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     WcShape wsh;
     const bool wc = !two_level && a.mode == 0 && (rq_big(m) || (m == 1 && use_house)) && wc_shape(m, wsh) &&
                     !getenv("SS_ONE_LEVEL") && !(m == 1 && getenv("SS_RQ_M1_OFF")) &&
-                    wc_far_smem(m) <= h->smem_optin && wcomp_smem(m) <= h->smem_optin &&
+                    wc_far_smem(m) <= h->smem_optin && wsuf_smem(m, kWcNb) <= h->smem_optin &&
                     kWcWin * kWcNb <= 4 * kBlkNB;
     if (wc) nb0 = std::min(nb0, kWcNb);
     a.defer = a.mode == 1 && two_level && !getenv("SS_NO_DEFER");
@@ -2066,7 +2073,8 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     const int ncmax = nb0 + m;
     const int64_t wc_stride = wc ? (int64_t)(kWcWin * nb0 + m) * m : 0;  // composite W per shift
     const size_t wc_slack = m == 1 ? (size_t)kFkmShifts * wc_stride * 16 : 0;  // last group of 80 shifts
-    const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)ncmax * m + wc_stride;
+    const int wc_slabs = wc && m > 1 ? kWcWin : 1;  // window P kept per composite (k_wsuffix)
+    const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)wc_slabs * ncmax * m + wc_stride;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64 +
                              (size_t)(xh_stride + w22h_stride + y_stride) * 16;
     int64_t sb_max = std::min<int64_t>(a.batch > 0 ? a.batch : a.s, a.s);
@@ -2124,7 +2132,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
             B.Z = Z0 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * pst;
             B.pan = pan;
-            if (wc) B.W = B.P + (size_t)cnt * ncmax * m;  // after the parts' window P
+            if (wc) B.W = B.P + (size_t)wc_slabs * cnt * ncmax * m;  // after the parts' window P
             if (a.defer) {
                 B.Xh = Xh0 + (size_t)off * xh_stride;
                 B.W22h = W22h0 + (size_t)off * w22h_stride;
@@ -2155,25 +2163,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
 }  // namespace
 
 namespace ss {
-// ---- transposed-sweep composites (ss_lq.cu): fold and far pass ----------
-// Fold window P ((nb + M) x M per shift, M = padded state width) into the
-// composite W ((K + M) x M per shift): W12[x, x + nb) <- P12, W12[0, x) and
-// W22 <- . P22 (the earlier windows sit ABOVE in the top-down sweep).
-int tr_fold(ss_handle* h, cudaStream_t st, int M, int mc, int K, int x, int nb, bool first, int sb,
-            const double2* P, double2* W, int64_t wstride) {
-    static ss::DevMask configured;
-    if (!configured.has(h)) {
-        SS_CUDA_TRY(h, allow_max_smem(h, k_wcomp));
-        configured.set(h);
-    }
-    const WcLayout lw{1, wstride, 0, M};
-    const int nrows = x + M;
-    dim3 gc((unsigned)sb, (unsigned)std::max(1, (nrows + kWcRows - 1) / kWcRows));
-    k_wcomp<<<gc, 256, wcomp_smem(M), st>>>(M, K, x, nb, first, (int64_t)(nb + M) * M, P, lw, W, 0, x, mc);
-    SS_LAUNCH_CHECK(h);
-    return SS_OK;
-}
-
+// ---- transposed-sweep composites (ss_lq.cu): far pass ----------
 // The far pass's -I rows [rlo, r0) (rlo >= n): their panel row has at most
 // one entry (-1 in column i - n), so instead of the dense K-streamed pass:
 //   z_i <- z_i W22 - [0 <= i - dlo < K] W12[i - dlo]        (dlo = n + c0)
@@ -2294,7 +2284,11 @@ int wsuffix(ss_handle* h, cudaStream_t st, int sb, int g, const int* x, const in
     a.slab = slab;
     a.W = W;
     a.wstride = wstride;
-    k_wsuffix<<<sb, 256, wsuf_smem(M), st>>>(a);
+    int nbmax = 0;
+    for (int b = 0; b < g; ++b) nbmax = std::max(nbmax, nb[b]);
+    const size_t smem = wsuf_smem(M, nbmax);
+    if (M > 64 || smem > h->smem_optin) return ss::set_err(h, SS_EARG, "composite: state too wide");
+    k_wsuffix<<<sb, kWsT, smem, st>>>(a);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
