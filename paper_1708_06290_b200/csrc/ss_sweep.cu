@@ -46,6 +46,7 @@
 #include "ss_far4.cuh"
 #include "ss_far.cuh"
 #include "ss_fark.cuh"
+#include "ss_farkd.cuh"
 
 using namespace ssd;
 
@@ -758,6 +759,25 @@ static size_t fark_pan_bytes(int n, int ptop) {
     const size_t ntiles = (size_t)(ptop + n) / kFkTile + 2;
     return ntiles * ((4 * kBlkNB + kFkKC - 1) / kFkKC) * kFkKC * kFkTile * 8;  // K <= 4 outer blocks
 }
+// m = 20 two-level far pass on the FP64 tensor cores (ss_farkd.cuh);
+// -DSS_FARK_DFMA builds the DFMA consumer instead (comparison builds)
+#ifdef SS_FARK_DFMA
+constexpr bool kFarkDmma = false;
+#else
+constexpr bool kFarkDmma = true;
+#endif
+template <int NCB, int S, int NST = kFarkStages>
+int launch_farkd(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
+    static ss::DevMask configured;
+    if (!configured.has(h)) {
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkd<NCB, S, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)fark_smem_bytes<NCB, S, NST>()));
+        configured.set(h);
+    }
+    k_farkd<NCB, S, NST><<<grid, 32 * (1 + NCB * S), fark_smem_bytes<NCB, S, NST>(), st>>>(fk, Z, W);
+    SS_LAUNCH_CHECK(h);
+    return SS_OK;
+}
 template <int NCB, int S, int NST = kFarkStages>
 int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
     static ss::DevMask configured;  // devices configured
@@ -1137,12 +1157,16 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 // at config 4 against 3 x 4 / 5 x 3 / 6 x 2: 4.01k / 4.31k / 4.70k
                 // vs 4.82k shifts/s)
                 constexpr int S20 = 4, N20 = kFarkStages;
-                fk.jz = m == 10 ? fark_jz<1, 8>() : fark_jz<2, S20>();
+                const bool dmma = m == 20 && kFarkDmma;
+                fk.jz = m == 10 ? fark_jz<1, 8>() : dmma ? farkd_jz<2, S20>() : fark_jz<2, S20>();
                 fk.nz = (m + fk.jz - 1) / fk.jz;
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
                 cudaEvent_t ev = ss::timing_begin(h, st);
-                k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                if (dmma)
+                    k_pack_panel_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                else
+                    k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
                 const int S = m == 10 ? 8 : S20;
@@ -1158,7 +1182,8 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (r0 > std::max(rlo, ptop)) nnz += (double)(r0 - std::max(rlo, ptop)) * ncols;
                 ev = ss::timing_begin(h, st);
                 int rc = m == 10 ? launch_fark<1, 8>(h, grid, st, fk, B.Z, B.P)
-                                 : launch_fark<2, S20, N20>(h, grid, st, fk, B.Z, B.P);
+                         : dmma    ? launch_farkd<2, S20, N20>(h, grid, st, fk, B.Z, B.P)
+                                   : launch_fark<2, S20, N20>(h, grid, st, fk, B.Z, B.P);
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
                                8.0 * rows * (double)sb * m * ncols, 4.0 * m * nnz * sb);
