@@ -12,10 +12,14 @@
 // the consumer no longer spends its issue bandwidth on operand loads and
 // fixed-latency waits (k_fark: 64% of the FP64 pipe with issue 44% active).
 //
-// Warp layout: NCB warps per shift, warp (shift sw, row block wr) owns rows
-// [wr 64 / NCB, +64 / NCB) (MT = 4 / NCB m16 tiles) and all 2m real columns
-// (NT = m / 4 n8 tiles).  Accumulator fragment (i, nt): c0 + i c1 is the
-// complex entry (row gq, column 4 nt + tq), c2 + i c3 the one 8 rows below.
+// Warp layout: WR x WC warps per shift, warp (shift sw, wr, wc) owns the
+// m16 row tiles wr, wr + WR, .. (MT = 4 / WR) and a range of NTW of the
+// NT = ceil(m / 4) n8 column tiles (the last one partial when m % 4 != 0,
+// its missing columns predicated to zero).  The accumulators must fit the
+// register budget of 9 warps per CTA (168 per thread: one SM sub-partition
+// holds 3 of them), hence column-split warps for wide m.  Accumulator fragment (i, nt): c0 + i c1 is
+// the complex entry (row gq, column 4 nt + tq), c2 + i c3 the one 8 rows
+// below.
 //
 // The panel chunk is packed by k_pack_panel_d in DMMA fragment order: for
 // k-step ks (8 panel columns) and m16 tile mt, the 32 lanes' (a0, a1) pairs
@@ -69,12 +73,15 @@ __host__ __device__ constexpr int farkd_jz() {
     return fark_jz<NCB, S>() & ~3;
 }
 
-template <int NCB, int S, int NST>
-__global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
+template <int NCB, int S, int NST, int WR, int WC>
+__global__ void __launch_bounds__(32 * (1 + WR * WC * S), 1)
     k_farkd(FarKDims u, double2* Z, const double2* __restrict__ W) {
-    constexpr int NW = NCB * S, M = 10 * NCB, TILE = kFkTile, KC = kFkKC;
-    constexpr int MT = 4 / NCB, NT = M / 4, M2 = 2 * M;
-    static_assert(NCB == 2 || NCB == 4, "k_farkd: 64 / NCB rows per warp, m a multiple of 4");
+    // WR x WC warps per shift; warp (wr, wc) owns the m16 row tiles wr,
+    // wr + WR, .. and the n8 column tiles [wc NTW, wc NTW + NTW) (the last
+    // one partial when 2m % 8 != 0)
+    constexpr int WPS = WR * WC, NW = WPS * S, M = 10 * NCB, TILE = kFkTile, KC = kFkKC;
+    constexpr int MT = 4 / WR, M2 = 2 * M, NT = (M2 + 7) / 8, NTW = (NT + WC - 1) / WC;
+    static_assert(WR == 1 || WR == 2 || WR == 4, "k_farkd: 4 row tiles per unit");
     constexpr size_t SB = fark_stage_bytes<NCB, S>();
     constexpr size_t PANB = (size_t)KC * TILE * 8;
     static_assert(farkd_jz<NCB, S>() >= 4, "k_farkd: a Z chunk must hold one k8 step");
@@ -147,11 +154,20 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
     }
 
     // ---------------- consumers ----------------
-    const int cw = warp - 1, sw = cw / NCB, wr = cw - sw * NCB;
+    const int cw = warp - 1, sw = cw / WPS, wr = (cw - sw * WPS) % WR, wc = (cw - sw * WPS) / WR;
     const int gq = lane >> 2, tq = lane & 3;
-    const int rb = wr * (TILE / NCB);  // first tile row of this warp
+    const int t0 = WC == 1 ? 0 : wc * NTW;  // first n8 tile of this warp
+    // every tile full and every warp's tile range in bounds: no predicates
+    constexpr bool EXACT = (M2 % 8 == 0) && (NT % WC == 0);
+    // m % 4 == 0: every k8 step of the state part is full (jz % 4 == 0)
+    constexpr bool ZEX = M % 4 == 0;
     const int dlo = u.lzset ? u.lz0 : r0 - M;
     const int dp = u.lzset ? u.lzp : 0;
+    // the lane's B column (real) of its n8 tile t: 8 (t0 + t) + gq; complex
+    // output column of its accumulators: 4 (t0 + t) + tq
+    auto bcol_ok = [&](int t) { return EXACT || 8 * (t0 + t) + gq < M2; };
+    auto ccol_ok = [&](int t) { return EXACT || 4 * (t0 + t) + tq < M; };
+    auto tile_ok = [&](int t) { return EXACT || t0 + t < NT; };
     int g = 0;
     for (int k = 0; k < nun; ++k) {
         const int64_t unit = ua + (int64_t)k * spl;
@@ -161,11 +177,11 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
         const int i0 = u.rlo + tile * TILE;
         const bool interior = u.mnb == 0 || i0 + TILE <= dlo || i0 >= dlo + u.mnb;
         const double2 sig = interior ? cz() : u.shifts[l];
-        double acc[MT][NT][4];
+        double acc[MT][NTW][4];
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
-            for (int t = 0; t < NT; ++t)
+            for (int t = 0; t < NTW; ++t)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) acc[i][t][v] = 0.0;
         for (int ch = 0; ch < CH; ++ch, ++g) {
@@ -174,32 +190,39 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
             const unsigned char* st = stages + (size_t)s * SB;
             if (valid) {
                 if (ch < nz) {
-                    // state part: A = Z_old (real view), B = W22e
+                    // state part: A = Z_old (real view), B = W22e; k8 step = 4
+                    // complex state columns (the chunk's last step may be partial)
                     const int j0 = ch * jz, jn = min(jz, M - j0);
                     const double* zsd = reinterpret_cast<const double*>(st) + (size_t)sw * jz * (TILE + M) * 2;
                     const double2* w22 = reinterpret_cast<const double2*>(zsd) + jz * TILE;
                     for (int kb = 0; kb < jn; kb += 4) {
-                        double a[MT][4], b[NT][2];
+                        const int kn = jn - kb;  // complex columns left in this step
+                        double a[MT][4], b[NTW][2];
 #pragma unroll
                         for (int i = 0; i < MT; ++i)
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
-                                const int row = rb + 16 * i + gq + 8 * (v & 1), kk = tq + 4 * (v >> 1);
-                                a[i][v] = zsd[((kb + (kk >> 1)) * TILE + row) * 2 + (kk & 1)];
+                                const int row = 16 * (wr + WR * i) + gq + 8 * (v & 1), kk = tq + 4 * (v >> 1);
+                                a[i][v] = ZEX || (kk >> 1) < kn ? zsd[((kb + (kk >> 1)) * TILE + row) * 2 + (kk & 1)] : 0.0;
                             }
 #pragma unroll
-                        for (int t = 0; t < NT; ++t)
+                        for (int t = 0; t < NTW; ++t)
 #pragma unroll
                             for (int v = 0; v < 2; ++v) {
                                 const int kk = tq + 4 * v;
-                                const double2 w = w22[(kb + (kk >> 1)) * M + 4 * t + (gq >> 1)];
-                                // W22e[2j + pj][2c + pc]
-                                b[t][v] = (kk & 1) ? ((gq & 1) ? w.x : -w.y) : ((gq & 1) ? w.y : w.x);
+                                double bv = 0.0;
+                                if ((ZEX || (kk >> 1) < kn) && bcol_ok(t)) {
+                                    const double2 w = w22[(kb + (kk >> 1)) * M + 4 * (t0 + t) + (gq >> 1)];
+                                    // W22e[2j + pj][2c + pc]
+                                    bv = (kk & 1) ? ((gq & 1) ? w.x : -w.y) : ((gq & 1) ? w.y : w.x);
+                                }
+                                b[t][v] = bv;
                             }
 #pragma unroll
                         for (int i = 0; i < MT; ++i)
 #pragma unroll
-                            for (int t = 0; t < NT; ++t) dmma8(acc[i][t], a[i], b[t]);
+                            for (int t = 0; t < NTW; ++t)
+                                if (tile_ok(t)) dmma8(acc[i][t], a[i], b[t]);
                     }
                 } else {
                     const int kc = ch - nz, kcols = min(KC, K - kc * KC);
@@ -212,13 +235,13 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                         for (int i = 0; i < MT; ++i)
 #pragma unroll
                             for (int hh = 0; hh < 2; ++hh) {
-                                const int dd = i0 + rb + 16 * i + gq + 8 * hh - dlo;
+                                const int dd = i0 + 16 * (wr + WR * i) + gq + 8 * hh - dlo;
                                 const int wrow = dp + dd - kc * KC;
                                 if (dd >= 0 && dd < u.mnb && wrow >= 0 && wrow < kcols) {
 #pragma unroll
-                                    for (int t = 0; t < NT; ++t) {
-                                        const double2 w = ws[wrow * M + 4 * t + tq];
-                                        const double2 d = cmul(sig, w);
+                                    for (int t = 0; t < NTW; ++t) {
+                                        if (!ccol_ok(t)) continue;
+                                        const double2 d = cmul(sig, ws[wrow * M + 4 * (t0 + t) + tq]);
                                         acc[i][t][2 * hh] -= d.x;
                                         acc[i][t][2 * hh + 1] -= d.y;
                                     }
@@ -227,11 +250,10 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                     }
                     const int nks = (kcols + 7) >> 3;
                     for (int ks = 0; ks < nks; ++ks) {
-                        double a[MT][4], b[NT][2];
+                        double a[MT][4], b[NTW][2];
 #pragma unroll
                         for (int i = 0; i < MT; ++i) {
-                            const int mt = rb / 16 + i;
-                            const double* pa = pan + ((ks * 4 + mt) * 2) * 64 + lane * 2;
+                            const double* pa = pan + ((ks * 4 + wr + WR * i) * 2) * 64 + lane * 2;
                             const double2 lo = *reinterpret_cast<const double2*>(pa);
                             const double2 hi = *reinterpret_cast<const double2*>(pa + 64);
                             a[i][0] = lo.x;
@@ -240,24 +262,20 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
                             a[i][3] = hi.y;
                         }
                         const int k0 = ks * 8 + tq, k1 = k0 + 4;
-                        if (ks * 8 + 8 <= kcols) {
+                        // W12 rows past the composite are not copied (stale): zero them
+                        const bool full8 = ks * 8 + 8 <= kcols;
 #pragma unroll
-                            for (int t = 0; t < NT; ++t) {
-                                b[t][0] = wsd[k0 * M2 + 8 * t + gq];
-                                b[t][1] = wsd[k1 * M2 + 8 * t + gq];
-                            }
-                        } else {
-                            // W12 rows past the composite are not copied (stale)
-#pragma unroll
-                            for (int t = 0; t < NT; ++t) {
-                                b[t][0] = k0 < kcols ? wsd[k0 * M2 + 8 * t + gq] : 0.0;
-                                b[t][1] = k1 < kcols ? wsd[k1 * M2 + 8 * t + gq] : 0.0;
-                            }
+                        for (int t = 0; t < NTW; ++t) {
+                            const bool cok = bcol_ok(t);
+                            const int c = 8 * (t0 + t) + gq;
+                            b[t][0] = cok && (full8 || k0 < kcols) ? wsd[k0 * M2 + c] : 0.0;
+                            b[t][1] = cok && (full8 || k1 < kcols) ? wsd[k1 * M2 + c] : 0.0;
                         }
 #pragma unroll
                         for (int i = 0; i < MT; ++i)
 #pragma unroll
-                            for (int t = 0; t < NT; ++t) dmma8(acc[i][t], a[i], b[t]);
+                            for (int t = 0; t < NTW; ++t)
+                                if (tile_ok(t)) dmma8(acc[i][t], a[i], b[t]);
                     }
                 }
             }
@@ -270,11 +288,13 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
         for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                const int row = i0 + rb + 16 * i + gq + 8 * hh;
+                const int row = i0 + 16 * (wr + WR * i) + gq + 8 * hh;
                 if (row >= r0) continue;
 #pragma unroll
-                for (int t = 0; t < NT; ++t)
-                    zo[(int64_t)(4 * t + tq) * u.LDZ + row] = make_double2(acc[i][t][2 * hh], acc[i][t][2 * hh + 1]);
+                for (int t = 0; t < NTW; ++t)
+                    if (ccol_ok(t))
+                        zo[(int64_t)(4 * (t0 + t) + tq) * u.LDZ + row] =
+                            make_double2(acc[i][t][2 * hh], acc[i][t][2 * hh + 1]);
             }
     }
 }

@@ -766,15 +766,15 @@ constexpr bool kFarkDmma = false;
 #else
 constexpr bool kFarkDmma = true;
 #endif
-template <int NCB, int S, int NST = kFarkStages>
+template <int NCB, int S, int NST, int WR, int WC>
 int launch_farkd(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
     static ss::DevMask configured;
     if (!configured.has(h)) {
-        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkd<NCB, S, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkd<NCB, S, NST, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)fark_smem_bytes<NCB, S, NST>()));
         configured.set(h);
     }
-    k_farkd<NCB, S, NST><<<grid, 32 * (1 + NCB * S), fark_smem_bytes<NCB, S, NST>(), st>>>(fk, Z, W);
+    k_farkd<NCB, S, NST, WR, WC><<<grid, 32 * (1 + WR * WC * S), fark_smem_bytes<NCB, S, NST>(), st>>>(fk, Z, W);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -819,24 +819,24 @@ struct WcShape {
 static bool wc_shape(int m, WcShape& w) {
     if (m == 1) { w = {kFkmShifts, 4}; return true; }
     if (m == 40) { w = {2, 3}; return true; }
-    if (m == 50) { w = {3, 2}; return true; }
-    if (m == 60) { w = {2, 2}; return true; }
+    if (m == 50) { w = kFarkDmma ? WcShape{1, 4} : WcShape{3, 2}; return true; }
+    if (m == 60) { w = kFarkDmma ? WcShape{1, 4} : WcShape{2, 2}; return true; }
     return false;
 }
 static size_t wc_far_smem(int m) {
     switch (m) {
         case 1: return farkm_smem_bytes<4>();
         case 40: return fark_smem_bytes<4, 2, 3>();
-        case 50: return fark_smem_bytes<5, 3, 2>();
-        case 60: return fark_smem_bytes<6, 2, 2>();
+        case 50: return kFarkDmma ? fark_smem_bytes<5, 1, 4>() : fark_smem_bytes<5, 3, 2>();
+        case 60: return kFarkDmma ? fark_smem_bytes<6, 1, 4>() : fark_smem_bytes<6, 2, 2>();
         default: return ~(size_t)0;
     }
 }
 static int wc_jz(int m) {
     switch (m) {
-        case 40: return fark_jz<4, 2>();
-        case 50: return fark_jz<5, 3>();
-        default: return fark_jz<6, 2>();
+        case 40: return kFarkDmma ? farkd_jz<4, 2>() : fark_jz<4, 2>();
+        case 50: return kFarkDmma ? farkd_jz<5, 1>() : fark_jz<5, 3>();
+        default: return kFarkDmma ? farkd_jz<6, 1>() : fark_jz<6, 2>();
     }
 }
 static int launch_farkm(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z,
@@ -853,10 +853,11 @@ static int launch_farkm(ss_handle* h, int grid, cudaStream_t st, const FarKDims&
 }
 static int launch_wc_far(ss_handle* h, int m, int grid, cudaStream_t st, const FarKDims& fk, double2* Z,
                          const double2* W) {
+    // DMMA: four warps per shift (one m16 row tile each, every column tile)
     switch (m) {
-        case 40: return launch_fark<4, 2, 3>(h, grid, st, fk, Z, W);
-        case 50: return launch_fark<5, 3, 2>(h, grid, st, fk, Z, W);
-        case 60: return launch_fark<6, 2, 2>(h, grid, st, fk, Z, W);
+        case 40: return kFarkDmma ? launch_farkd<4, 2, 3, 2, 2>(h, grid, st, fk, Z, W) : launch_fark<4, 2, 3>(h, grid, st, fk, Z, W);
+        case 50: return kFarkDmma ? launch_farkd<5, 1, 4, 4, 2>(h, grid, st, fk, Z, W) : launch_fark<5, 3, 2>(h, grid, st, fk, Z, W);
+        case 60: return kFarkDmma ? launch_farkd<6, 1, 4, 4, 2>(h, grid, st, fk, Z, W) : launch_fark<6, 2, 2>(h, grid, st, fk, Z, W);
         default: return ss::set_err(h, SS_EARG, "window composite: unsupported m");
     }
 }
@@ -1157,8 +1158,9 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 // at config 4 against 3 x 4 / 5 x 3 / 6 x 2: 4.01k / 4.31k / 4.70k
                 // vs 4.82k shifts/s)
                 constexpr int S20 = 4, N20 = kFarkStages;
-                const bool dmma = m == 20 && kFarkDmma;
-                fk.jz = m == 10 ? fark_jz<1, 8>() : dmma ? farkd_jz<2, S20>() : fark_jz<2, S20>();
+                const bool dmma = kFarkDmma;
+                fk.jz = m == 10 ? (dmma ? farkd_jz<1, 4>() : fark_jz<1, 8>())
+                                : (dmma ? farkd_jz<2, S20>() : fark_jz<2, S20>());
                 fk.nz = (m + fk.jz - 1) / fk.jz;
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
@@ -1169,7 +1171,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                     k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
-                const int S = m == 10 ? 8 : S20;
+                const int S = m == 10 ? (dmma ? 4 : 8) : S20;
                 const int64_t units = (int64_t)fk.ntiles * ((sb + S - 1) / S);
                 // teams of 4 CTAs per shift group: the live W set drops from ~100 MB
                 // (over L2) to ~25 MB, DRAM bytes per launch 8.5 -> 2.6 GB at config 4
@@ -1181,9 +1183,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 if (top_hi > rlo) nnz += (double)(top_hi - rlo) * ncols;
                 if (r0 > std::max(rlo, ptop)) nnz += (double)(r0 - std::max(rlo, ptop)) * ncols;
                 ev = ss::timing_begin(h, st);
-                int rc = m == 10 ? launch_fark<1, 8>(h, grid, st, fk, B.Z, B.P)
-                         : dmma    ? launch_farkd<2, S20, N20>(h, grid, st, fk, B.Z, B.P)
-                                   : launch_fark<2, S20, N20>(h, grid, st, fk, B.Z, B.P);
+                int rc = m == 10 ? (dmma ? launch_farkd<1, 4, kFarkStages, 2, 1>(h, grid, st, fk, B.Z, B.P)
+                                         : launch_fark<1, 8>(h, grid, st, fk, B.Z, B.P))
+                                 : (dmma ? launch_farkd<2, S20, N20, 2, 1>(h, grid, st, fk, B.Z, B.P)
+                                         : launch_fark<2, S20, N20>(h, grid, st, fk, B.Z, B.P));
                 if (rc) return rc;
                 ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
                                8.0 * rows * (double)sb * m * ncols, 4.0 * m * nnz * sb);
@@ -1519,7 +1522,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
                 cudaEvent_t ev = ss::timing_begin(h, st);
-                k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                if (m > 1 && kFarkDmma)
+                    k_pack_panel_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                else
+                    k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
                 const int64_t units = (int64_t)fk.ntiles * ((sb + wsh.S - 1) / wsh.S);
