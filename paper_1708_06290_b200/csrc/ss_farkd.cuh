@@ -66,6 +66,23 @@ __global__ void __launch_bounds__(256) k_pack_panel_d(FarKDims u, double* __rest
     }
 }
 
+// k_pack_panel_tr in fragment order: rows i < n are A(c, i), rows n + r are
+// -[r == c]; zero outside [rlo, r0) x [c0, c0 + K)
+__global__ void __launch_bounds__(256) k_pack_panel_tr_d(FarKDims u, double* __restrict__ pan) {
+    const int tile = blockIdx.x / u.nk, kc = blockIdx.x - tile * u.nk;
+    double* dst = pan + (size_t)blockIdx.x * kFkKC * kFkTile;
+    for (int e = threadIdx.x; e < kFkKC * kFkTile; e += blockDim.x) {
+        const int j = e % kFkKC, rr = e / kFkKC;
+        const int i = u.rlo + tile * kFkTile + rr, jc = kc * kFkKC + j, col = u.c0 + jc;
+        double v = 0.0;
+        if (i < u.r0 && jc < u.K) {
+            if (i < u.n) v = u.A[col + (int64_t)i * u.lda];
+            else v = (i - u.n == col) ? -1.0 : 0.0;
+        }
+        dst[farkd_pan_index(j, rr)] = v;
+    }
+}
+
 // state columns per Z chunk: k_fark's, rounded down to a multiple of 4 (one
 // k8 step = 4 complex columns)
 template <int NCB, int S>

@@ -2325,11 +2325,58 @@ int wsuffix(ss_handle* h, cudaStream_t st, int sb, int g, const int* x, const in
 }
 
 // state widths the composite far pass supports (M = 10 NCB)
+// The transposed sweep's K-streamed passes over M state columns (M = 10 ..
+// 60): (shifts per unit, Z-chunk width) and the launch, on k_farkd (DMMA;
+// -DSS_FARK_DFMA: k_fark)
+static int tr_shape(int M, int& jz) {
+    if (kFarkDmma) {
+        switch (M) {
+            case 10: jz = farkd_jz<1, 4>(); return 4;
+            case 20: jz = farkd_jz<2, 4>(); return 4;
+            case 30: jz = farkd_jz<3, 2>(); return 2;
+            case 40: jz = farkd_jz<4, 2>(); return 2;
+            case 50: jz = farkd_jz<5, 1>(); return 1;
+            case 60: jz = farkd_jz<6, 1>(); return 1;
+            default: return 0;
+        }
+    }
+    switch (M) {
+        case 10: jz = fark_jz<1, 8>(); return 8;
+        case 20: jz = fark_jz<2, 4>(); return 4;
+        case 30: jz = fark_jz<3, 4>(); return 4;
+        case 40: jz = fark_jz<4, 2>(); return 2;
+        case 50: jz = fark_jz<5, 3>(); return 3;
+        case 60: jz = fark_jz<6, 2>(); return 2;
+        default: return 0;
+    }
+}
+static int tr_launch(ss_handle* h, int M, int grid, cudaStream_t st, const FarKDims& fk, double2* S,
+                     const double2* W) {
+    if (kFarkDmma) {
+        switch (M) {
+            case 10: return launch_farkd<1, 4, kFarkStages, 2, 1>(h, grid, st, fk, S, W);
+            case 20: return launch_farkd<2, 4, kFarkStages, 2, 1>(h, grid, st, fk, S, W);
+            case 30: return launch_farkd<3, 2, kFarkStages, 4, 1>(h, grid, st, fk, S, W);
+            case 40: return launch_farkd<4, 2, 3, 2, 2>(h, grid, st, fk, S, W);
+            case 50: return launch_farkd<5, 1, 4, 4, 2>(h, grid, st, fk, S, W);
+            default: return launch_farkd<6, 1, 4, 4, 2>(h, grid, st, fk, S, W);
+        }
+    }
+    switch (M) {
+        case 10: return launch_fark<1, 8>(h, grid, st, fk, S, W);
+        case 20: return launch_fark<2, 4>(h, grid, st, fk, S, W);
+        case 30: return launch_fark<3, 4, 2>(h, grid, st, fk, S, W);
+        case 40: return launch_fark<4, 2, 3>(h, grid, st, fk, S, W);
+        case 50: return launch_fark<5, 3, 2>(h, grid, st, fk, S, W);
+        default: return launch_fark<6, 2, 2>(h, grid, st, fk, S, W);
+    }
+}
+
 bool tr_far_supported(ss_handle* h, int M) {
     switch (M) {
         case 10: return fark_smem_bytes<1, 8, kFarkStages>() <= h->smem_optin;
         case 20: return fark_smem_bytes<2, 4, kFarkStages>() <= h->smem_optin;
-        case 30: return fark_smem_bytes<3, 4, 2>() <= h->smem_optin;
+        case 30: return (kFarkDmma ? fark_smem_bytes<3, 2, kFarkStages>() : fark_smem_bytes<3, 4, 2>()) <= h->smem_optin;
         case 40: case 50: case 60: return wc_far_smem(M) <= h->smem_optin;
         default: return false;
     }
@@ -2390,19 +2437,14 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
     fk.nk = (K + kFkKC - 1) / kFkKC;
     fk.ntiles = (rows + kFkTile - 1) / kFkTile;
     fk.pan = pan;
-    int S_ = 1;
-    switch (M) {
-        case 10: fk.jz = fark_jz<1, 8>(); S_ = 8; break;
-        case 20: fk.jz = fark_jz<2, 4>(); S_ = 4; break;
-        case 30: fk.jz = fark_jz<3, 4>(); S_ = 4; break;
-        case 40: fk.jz = fark_jz<4, 2>(); S_ = 2; break;
-        case 50: fk.jz = fark_jz<5, 3>(); S_ = 3; break;
-        case 60: fk.jz = fark_jz<6, 2>(); S_ = 2; break;
-        default: return ss::set_err(h, SS_EARG, "transposed composite: unsupported width");
-    }
+    const int S_ = tr_shape(M, fk.jz);
+    if (!S_) return ss::set_err(h, SS_EARG, "transposed composite: unsupported width");
     fk.nz = (M + fk.jz - 1) / fk.jz;
     cudaEvent_t ev = ss::timing_begin(h, st);
-    k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    if (kFarkDmma)
+        k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    else
+        k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
     SS_LAUNCH_CHECK(h);
     ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
     const int64_t units = (int64_t)fk.ntiles * ((sb + S_ - 1) / S_);
@@ -2413,15 +2455,7 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
     const int arows = std::max(0, std::min(r0, n) - rlo);
     const double nnz = (double)arows * K + (double)std::min(K, std::max(0, r0 - std::max(rlo, n)));
     ev = ss::timing_begin(h, st);
-    int rc;
-    switch (M) {
-        case 10: rc = launch_fark<1, 8>(h, grid, st, fk, S, W); break;
-        case 20: rc = launch_fark<2, 4>(h, grid, st, fk, S, W); break;
-        case 30: rc = launch_fark<3, 4, 2>(h, grid, st, fk, S, W); break;
-        case 40: rc = launch_fark<4, 2, 3>(h, grid, st, fk, S, W); break;
-        case 50: rc = launch_fark<5, 3, 2>(h, grid, st, fk, S, W); break;
-        default: rc = launch_fark<6, 2, 2>(h, grid, st, fk, S, W); break;
-    }
+    int rc = tr_launch(h, M, grid, st, fk, S, W);
     if (rc) return rc;
     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * M * M * (double)sb, 8.0 * rows * (double)sb * M * K,
                    4.0 * (m + 1) * nnz * sb);
@@ -2449,11 +2483,15 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     }
     const int r0 = std::min(r0_all, n), rows = r0 - rlo;
     if (rows <= 0) return SS_OK;
+    // k_farkm (w) reads the lane-interleaved panel, k_farkd (z2) the
+    // fragment-ordered one: both are packed
+    const size_t pb = fark_pan_bytes(2 * n, 0);
     {
-        int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(2 * n, 0), 1);
+        int rc = ss::ensure_ws(h, (1u << 20) + (kFarkDmma ? 2 : 1) * pb, 1);
         if (rc) return rc;
     }
     double* pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
+    double* pan_d = kFarkDmma ? reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20) + pb) : pan;
     FarKDims fk;
     fk.m = m;
     fk.ptop = 0;
@@ -2482,6 +2520,10 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     cudaEvent_t ev = ss::timing_begin(h, st);
     k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
     SS_LAUNCH_CHECK(h);
+    if (kFarkDmma) {
+        k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan_d);
+        SS_LAUNCH_CHECK(h);
+    }
     k_tr_wprep<<<dim3((unsigned)((rows + 255) / 256), (unsigned)sb), 256, 0, st>>>(m, LDS, S, rlo, r0, K, W,
                                                                                    wstride);
     SS_LAUNCH_CHECK(h);
@@ -2504,31 +2546,16 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
         ss::timing_end(h, st, ev, ss::PH_UPDATE, 0.0, 8.0 * rows * (double)sb * K, 4.0 * nnz * sb);
     }
     // z2: exact m = 10 NCB columns
-    int S_ = 1;
-    switch (m) {
-        case 10: fk.jz = fark_jz<1, 8>(); S_ = 8; break;
-        case 20: fk.jz = fark_jz<2, 4>(); S_ = 4; break;
-        case 30: fk.jz = fark_jz<3, 4>(); S_ = 4; break;
-        case 40: fk.jz = fark_jz<4, 2>(); S_ = 2; break;
-        case 50: fk.jz = fark_jz<5, 3>(); S_ = 3; break;
-        case 60: fk.jz = fark_jz<6, 2>(); S_ = 2; break;
-        default: return ss::set_err(h, SS_EARG, "transposed split far pass: unsupported m");
-    }
+    const int S_ = tr_shape(m, fk.jz);
+    if (!S_) return ss::set_err(h, SS_EARG, "transposed split far pass: unsupported m");
     fk.nz = (m + fk.jz - 1) / fk.jz;
     fk.wstride = wzstride;
+    fk.pan = pan_d;
     const int64_t units = (int64_t)fk.ntiles * ((sb + S_ - 1) / S_);
     fk.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
     const int grid = (int)std::max<int64_t>(fk.spl, std::min<int64_t>(units, h->num_sms) / fk.spl * fk.spl);
     ev = ss::timing_begin(h, st);
-    int rc;
-    switch (m) {
-        case 10: rc = launch_fark<1, 8>(h, grid, st, fk, S, Wz); break;
-        case 20: rc = launch_fark<2, 4>(h, grid, st, fk, S, Wz); break;
-        case 30: rc = launch_fark<3, 4, 2>(h, grid, st, fk, S, Wz); break;
-        case 40: rc = launch_fark<4, 2, 3>(h, grid, st, fk, S, Wz); break;
-        case 50: rc = launch_fark<5, 3, 2>(h, grid, st, fk, S, Wz); break;
-        default: rc = launch_fark<6, 2, 2>(h, grid, st, fk, S, Wz); break;
-    }
+    int rc = tr_launch(h, m, grid, st, fk, S, Wz);
     if (rc) return rc;
     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb, 8.0 * rows * (double)sb * m * K,
                    4.0 * m * nnz * sb);
