@@ -316,4 +316,178 @@ __global__ void __launch_bounds__(32 * (1 + WR * WC * S), 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_farkm on the tensor cores (m = 1: config 3's far pass; the transposed
+// sweep's w column): the group's 80 shifts are the 160 interleaved real
+// columns of one real GEMM  Z(64 x 160) += Pan(64 x K) W12(K x 160)  (the
+// group-major W rows are exactly that matrix), W22 diagonal across the
+// columns in the epilogue.  8 consumer warps: 2 row groups (2 m16 tiles
+// each) x 4 column groups (5 n8 tiles = 20 shifts each).
+template <int NST>
+__global__ void __launch_bounds__(32 * 9, 1) k_farkmd(FarKDims u, double2* Z, const double2* __restrict__ W) {
+    constexpr int S = kFkmShifts, TILE = kFkTile, KC = kFkKC, WR = 2, MT = 2, NTW = 5, S2 = 2 * S;
+    constexpr size_t SB = farkm_stage_bytes();
+    constexpr size_t PANB = (size_t)KC * TILE * 8;
+    static_assert(4 * NTW * 8 == S2, "k_farkmd: 4 column groups of 5 n8 tiles");
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NST]
+    uint64_t* empty = full + NST;                         // [NST] (count 8)
+    unsigned char* stages = smem + 256;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = u.r0, sb = u.sb, K = u.K, nk = u.nk;
+    const int nsu = (sb + S - 1) / S;
+    const int64_t units = (int64_t)u.ntiles * nsu;
+    const int64_t gstride = (int64_t)u.wstride;  // complex per group: (Kmax + 1) x 80
+    const int spl = u.spl, team = blockIdx.x / spl, h = blockIdx.x - team * spl, nteams = gridDim.x / spl;
+    const int64_t ua0 = units * team / nteams, ub = units * (team + 1) / nteams;
+    const int64_t ua = ua0 + h;
+    const int nun = ua < ub ? (int)((ub - ua + spl - 1) / spl) : 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (nun <= 0) return;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int g = 0;
+            for (int k = 0; k < nun; ++k) {
+                const int64_t unit = ua + (int64_t)k * spl;
+                const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = g % NST, use = g / NST;
+                    if (use > 0) mbar_wait_sleep(empty + s, (use - 1) & 1);
+                    unsigned char* st = stages + (size_t)s * SB;
+                    const int kcols = min(KC, K - kc * KC);
+                    mbar_expect_tx(full + s, (unsigned)PANB + (unsigned)(kcols * S * 16));
+                    tma_bulk_g2s(st, u.pan + ((size_t)tile * nk + kc) * KC * TILE, (unsigned)PANB, full + s);
+                    tma_bulk_g2s(st + PANB, W + grp * gstride + (int64_t)kc * KC * S, (unsigned)(kcols * S * 16),
+                                 full + s);
+                }
+            }
+        }
+        return;
+    }
+
+    const int cw = warp - 1, wr = cw % WR, wc = cw / WR;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int t0 = wc * NTW;
+    const int dlo = u.lzset ? u.lz0 : r0 - 1;
+    const int dp = u.lzset ? u.lzp : 0;
+    const int64_t zst = u.zstride ? u.zstride : u.LDZ;
+    int g = 0;
+    for (int k = 0; k < nun; ++k) {
+        const int64_t unit = ua + (int64_t)k * spl;
+        const int grp = (int)(unit / u.ntiles), tile = (int)(unit - (int64_t)grp * u.ntiles);
+        const int l0 = grp * S;
+        const int i0 = u.rlo + tile * TILE;
+        const bool interior = u.mnb == 0 || i0 + TILE <= dlo || i0 >= dlo + u.mnb;
+        double acc[MT][NTW][4];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int t = 0; t < NTW; ++t)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[i][t][v] = 0.0;
+        for (int kc = 0; kc < nk; ++kc, ++g) {
+            const int s = g % NST, use = g / NST;
+            mbar_wait(full + s, use & 1);
+            const unsigned char* st = stages + (size_t)s * SB;
+            const int kcols = min(KC, K - kc * KC);
+            const double* pan = reinterpret_cast<const double*>(st);
+            const double* wsd = reinterpret_cast<const double*>(st + PANB);
+            if (!interior && dp < kc * KC + kcols && dp + u.mnb > kc * KC) {
+                // lazy shift: rows dlo + dd carry -sigma_l W12_l[dp + dd]
+                const double2* ws = reinterpret_cast<const double2*>(wsd);
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int dd = i0 + 16 * (wr + WR * i) + gq + 8 * hh - dlo;
+                        const int wrow = dp + dd - kc * KC;
+                        if (dd >= 0 && dd < u.mnb && wrow >= 0 && wrow < kcols) {
+#pragma unroll
+                            for (int t = 0; t < NTW; ++t) {
+                                const int c = 4 * (t0 + t) + tq;
+                                const int l = min(l0 + c, sb - 1);
+                                const double2 d = cmul(u.shifts[l], ws[wrow * S + c]);
+                                acc[i][t][2 * hh] -= d.x;
+                                acc[i][t][2 * hh + 1] -= d.y;
+                            }
+                        }
+                    }
+            }
+            const int nks = (kcols + 7) >> 3;
+            for (int ks = 0; ks < nks; ++ks) {
+                double a[MT][4], b[NTW][2];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const double* pa = pan + ((ks * 4 + wr + WR * i) * 2) * 64 + lane * 2;
+                    const double2 lo = *reinterpret_cast<const double2*>(pa);
+                    const double2 hi = *reinterpret_cast<const double2*>(pa + 64);
+                    a[i][0] = lo.x;
+                    a[i][1] = lo.y;
+                    a[i][2] = hi.x;
+                    a[i][3] = hi.y;
+                }
+                const int k0 = ks * 8 + tq, k1 = k0 + 4;
+                const bool full8 = ks * 8 + 8 <= kcols;
+#pragma unroll
+                for (int t = 0; t < NTW; ++t) {
+                    const int c = 8 * (t0 + t) + gq;
+                    b[t][0] = full8 || k0 < kcols ? wsd[k0 * S2 + c] : 0.0;
+                    b[t][1] = full8 || k1 < kcols ? wsd[k1 * S2 + c] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int t = 0; t < NTW; ++t) dmma8(acc[i][t], a[i], b[t]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        // epilogue: z <- z W22 + acc (every load before any store: Z is not restrict)
+        const double2* w22 = W + grp * gstride + (int64_t)K * S;
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {
+            const int c = 4 * (t0 + t) + tq;
+            const int64_t l = l0 + c;
+            if (l >= sb) continue;
+            const double2 wz = w22[c];
+            const double2* zc = Z + l * zst + u.zoff;
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int row = i0 + 16 * (wr + WR * i) + gq + 8 * hh;
+                    if (row < r0) {
+                        const double2 z = __ldg(zc + row);
+                        const double2 r = cfma(z, wz, make_double2(acc[i][t][2 * hh], acc[i][t][2 * hh + 1]));
+                        acc[i][t][2 * hh] = r.x;
+                        acc[i][t][2 * hh + 1] = r.y;
+                    }
+                }
+        }
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {
+            const int c = 4 * (t0 + t) + tq;
+            const int64_t l = l0 + c;
+            if (l >= sb) continue;
+            double2* zc = Z + l * zst + u.zoff;
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int row = i0 + 16 * (wr + WR * i) + gq + 8 * hh;
+                    if (row < r0) zc[row] = make_double2(acc[i][t][2 * hh], acc[i][t][2 * hh + 1]);
+                }
+        }
+    }
+}
+
 }  // namespace ssd

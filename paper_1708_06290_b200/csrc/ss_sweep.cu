@@ -845,9 +845,14 @@ static int launch_farkm(ss_handle* h, int grid, cudaStream_t st, const FarKDims&
     if (!configured.has(h)) {
         SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)farkm_smem_bytes<4>()));
+        SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkmd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)farkm_smem_bytes<4>()));
         configured.set(h);
     }
-    k_farkm<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
+    if (kFarkDmma)
+        k_farkmd<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
+    else
+        k_farkm<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -1522,7 +1527,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
                 cudaEvent_t ev = ss::timing_begin(h, st);
-                if (m > 1 && kFarkDmma)
+                if (kFarkDmma)
                     k_pack_panel_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
                 else
                     k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
@@ -2483,15 +2488,11 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     }
     const int r0 = std::min(r0_all, n), rows = r0 - rlo;
     if (rows <= 0) return SS_OK;
-    // k_farkm (w) reads the lane-interleaved panel, k_farkd (z2) the
-    // fragment-ordered one: both are packed
-    const size_t pb = fark_pan_bytes(2 * n, 0);
     {
-        int rc = ss::ensure_ws(h, (1u << 20) + (kFarkDmma ? 2 : 1) * pb, 1);
+        int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(2 * n, 0), 1);
         if (rc) return rc;
     }
     double* pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
-    double* pan_d = kFarkDmma ? reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20) + pb) : pan;
     FarKDims fk;
     fk.m = m;
     fk.ptop = 0;
@@ -2518,12 +2519,13 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     fk.pan = pan;
     fk.zstride = (int64_t)mp * LDS;
     cudaEvent_t ev = ss::timing_begin(h, st);
-    k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    // one packed panel for both passes (k_farkmd and k_farkd read the
+    // fragment order; -DSS_FARK_DFMA: k_farkm / k_fark the lane-interleaved one)
+    if (kFarkDmma)
+        k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    else
+        k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
     SS_LAUNCH_CHECK(h);
-    if (kFarkDmma) {
-        k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan_d);
-        SS_LAUNCH_CHECK(h);
-    }
     k_tr_wprep<<<dim3((unsigned)((rows + 255) / 256), (unsigned)sb), 256, 0, st>>>(m, LDS, S, rlo, r0, K, W,
                                                                                    wstride);
     SS_LAUNCH_CHECK(h);
@@ -2550,7 +2552,6 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     if (!S_) return ss::set_err(h, SS_EARG, "transposed split far pass: unsupported m");
     fk.nz = (m + fk.jz - 1) / fk.jz;
     fk.wstride = wzstride;
-    fk.pan = pan_d;
     const int64_t units = (int64_t)fk.ntiles * ((sb + S_ - 1) / S_);
     fk.spl = units >= 8 * (int64_t)h->num_sms ? 4 : 1;
     const int grid = (int)std::max<int64_t>(fk.spl, std::min<int64_t>(units, h->num_sms) / fk.spl * fk.spl);
