@@ -797,10 +797,12 @@ int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, dou
 // RQ, k_rq_big): the windows of a composite (up to kWcWin windows of kWcNb
 // columns, bottom-up) are factored one by one; each window's P updates only
 // the composite's own rows above it ("near", the generic k_update) and is
-// folded into the composite W = [W12 (K x m); W22 (m x m)]:
-//     W12[window rows] <- P12,  W12[rows below] <- W12 P22,  W22 <- W22 P22
-// (k_wcomp); the rows above the composite then get ONE K-streamed update
-// (k_fark, one pass over the K columns).  The far rows' state x W22 share of
+// kept; the composite W = [W12 (K x m); W22 (m x m)] is then built from all
+// of them at once (k_wsuffix, the suffix product of the windows' P22; the
+// same algebra as folding window by window:
+//     W12[window rows] <- P12,  W12[rows below] <- W12 P22,  W22 <- W22 P22)
+// and the rows above the composite get ONE K-streamed update (k_farkd, one
+// pass over the K columns).  The far rows' state x W22 share of
 // the work drops from 2m / nb0 (104% at m = 50, nb0 = 96) to 2m / K.
 // Same algebra as the two-level sweep's composites (ss_block.cuh).
 // ---------------------------------------------------------------------------
