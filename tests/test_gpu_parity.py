@@ -587,14 +587,15 @@ def test_m1_throughput_rq_vs_warp_rq(n, nb, monkeypatch):
 
 
 @pytest.mark.parametrize("n,m,p", [(400, 50, 50), (330, 33, 7), (500, 20, 20), (260, 16, 4), (300, 63, 5),
-                                   (420, 100, 90), (380, 70, 3)])
+                                   (420, 100, 90), (380, 70, 3), (1500, 40, 6), (1300, 50, 9), (1400, 60, 4)])
 def test_wide_m_paths_vs_oracle(n, m, p):
     """Block widths outside the two-level set: m + 1 > 32 takes the scheduled
     Givens block RQ (config 5: m = 50; m = 100: head matrices in global
     scratch), m = 16 / 20 the one-level update with
     several column blocks per shift (config 4: m = 20).  Transfer function and
     reduced solve vs the C oracle, conjugate pairs of complex shifts as in
-    config 4 / 5."""
+    config 4 / 5.  n >= 1300 at m = 40 / 50 / 60: several window composites,
+    so the K-streamed far pass (k_farkd) runs over real far rows."""
     sysb = ss.random_stable_system(n, m, p, seed=n + 7 * m, circular=True)
     chf = ss.reduce_controller_hessenberg(sysb.A, sysb.B, sysb.C, block_size=64)
     rng = np.random.default_rng(m)
