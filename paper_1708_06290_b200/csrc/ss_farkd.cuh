@@ -185,6 +185,10 @@ __global__ void __launch_bounds__(32 * (1 + WR * WC * S), 1)
     auto bcol_ok = [&](int t) { return EXACT || 8 * (t0 + t) + gq < M2; };
     auto ccol_ok = [&](int t) { return EXACT || 4 * (t0 + t) + tq < M; };
     auto tile_ok = [&](int t) { return EXACT || t0 + t < NT; };
+    // the lane's element of the 2 x 2 expansion of a W22 entry (state part):
+    // row parity pj = tq & 1, column parity pc = gq & 1
+    const int wsel = ((tq ^ gq) & 1);                                    // 0: re, 1: im
+    const long long wneg = ((tq & 1) && !(gq & 1)) ? (long long)0x8000000000000000ULL : 0;  // -im
     int g = 0;
     for (int k = 0; k < nun; ++k) {
         const int64_t unit = ua + (int64_t)k * spl;
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(32 * (1 + WR * WC * S), 1)
                     // complex state columns (the chunk's last step may be partial)
                     const int j0 = ch * jz, jn = min(jz, M - j0);
                     const double* zsd = reinterpret_cast<const double*>(st) + (size_t)sw * jz * (TILE + M) * 2;
-                    const double2* w22 = reinterpret_cast<const double2*>(zsd) + jz * TILE;
+                    const double* w22d = zsd + (size_t)jz * TILE * 2;
                     for (int kb = 0; kb < jn; kb += 4) {
                         const int kn = jn - kb;  // complex columns left in this step
                         double a[MT][4], b[NTW][2];
@@ -229,9 +233,11 @@ __global__ void __launch_bounds__(32 * (1 + WR * WC * S), 1)
                                 const int kk = tq + 4 * v;
                                 double bv = 0.0;
                                 if ((ZEX || (kk >> 1) < kn) && bcol_ok(t)) {
-                                    const double2 w = w22[(kb + (kk >> 1)) * M + 4 * (t0 + t) + (gq >> 1)];
-                                    // W22e[2j + pj][2c + pc]
-                                    bv = (kk & 1) ? ((gq & 1) ? w.x : -w.y) : ((gq & 1) ? w.y : w.x);
+                                    // W22e[2j + pj][2c + pc] = pj == pc ? re : (pj ? -im : im):
+                                    // one 8-byte load at a lane-constant offset, sign by XOR
+                                    const double w =
+                                        w22d[((kb + (kk >> 1)) * M + 4 * (t0 + t) + (gq >> 1)) * 2 + wsel];
+                                    bv = __longlong_as_double(__double_as_longlong(w) ^ wneg);
                                 }
                                 b[t][v] = bv;
                             }
