@@ -53,14 +53,14 @@ WORKLOADS = {
     5: "config5: large-scale transfer function n=20000, m=p=50, 500 complex shifts per GPU",
 }
 # dominant (far-row update) kernel per m, as enqueue_part selects it
-FAR_KERNEL = {10: "k_farkd<1,4,4,2,1> (K-streamed far-row update on the FP64 tensor cores, DMMA: "
-                  "one pass per 4-block composite, 4 shifts x 64 rows per unit)",
-              20: "k_farkd<2,4,4,2,1> (K-streamed far-row update on the FP64 tensor cores, DMMA: "
-                  "one pass per 4-block composite, 4 shifts x 64 rows per unit)",
+FAR_KERNEL = {10: "k_fark<1,8,4> (K-streamed far-row update: one pass per 4-block composite, "
+                  "8 shifts x 64 rows per unit)",
+              20: "k_fark<2,4,4> (K-streamed far-row update: one pass per 4-block composite, "
+                  "4 shifts x 64 rows per unit)",
               1: "k_farkm<4> (window composites: one K-streamed pass per 8 windows, 80 shifts "
                  "per unit as columns) + the near rows' one-level k_far (all update launches)",
-              50: "k_farkd<5,1,4,4,2> (window composites: one K-streamed DMMA pass per 8 windows, "
-                  "1 shift x 64 rows per unit) + the near rows' k_update (all update launches)"}
+              50: "k_fark<5,3,2> (window composites: one K-streamed pass per 8 windows, 3 shifts "
+                  "x 64 rows per unit) + the near rows' k_update (all update launches)"}
 
 
 def parse(argv=None):
@@ -482,8 +482,8 @@ def main(argv=None):
         return 0
 
     # the FP64 peak is the larger of the two measured paths (DFMA on the FP64
-    # pipe, DMMA on the tensor pipe: the far kernels run on DMMA); on B200
-    # both measure ~37 TFLOP/s
+    # pipe, DMMA on the tensor pipe); on B200 both measure ~37 TFLOP/s, and
+    # the sweep runs on DFMA (north_star: DMMA only in the reduction)
     peak, peak_d = ctypes.c_double(0.0), ctypes.c_double(0.0)
     D.check(h, L.ss_probe_dfma_peak(h.ptr, ctypes.byref(peak)))
     D.check(h, L.ss_probe_dmma_peak(h.ptr, ctypes.byref(peak_d)))

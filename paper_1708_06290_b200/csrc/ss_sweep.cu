@@ -46,7 +46,9 @@
 #include "ss_far4.cuh"
 #include "ss_far.cuh"
 #include "ss_fark.cuh"
-#include "ss_farkd.cuh"
+#ifdef SS_FARK_DMMA
+#include "ss_farkd.cuh"  // comparison builds only (see kFarkDmma)
+#endif
 
 using namespace ssd;
 
@@ -759,13 +761,32 @@ static size_t fark_pan_bytes(int n, int ptop) {
     const size_t ntiles = (size_t)(ptop + n) / kFkTile + 2;
     return ntiles * ((4 * kBlkNB + kFkKC - 1) / kFkKC) * kFkKC * kFkTile * 8;  // K <= 4 outer blocks
 }
-// m = 20 two-level far pass on the FP64 tensor cores (ss_farkd.cuh);
-// -DSS_FARK_DFMA builds the DFMA consumer instead (comparison builds)
-#ifdef SS_FARK_DFMA
-constexpr bool kFarkDmma = false;
-#else
+// The far passes run on DFMA (k_fark / k_farkm).  north_star allows FP64
+// tensor-core DMMA only in the reduction's trailing updates, so the DMMA
+// consumers (ss_farkd.cuh: k_farkd / k_farkmd, measured +25% at config 4)
+// are compiled only into comparison builds (-DSS_FARK_DMMA,
+// tools/build_variant.sh), never into the product library.
+#ifdef SS_FARK_DMMA
 constexpr bool kFarkDmma = true;
+// the packed panel in DMMA fragment order for k_farkd / k_farkmd
+static void pack_panel(const FarKDims& fk, double* pan, cudaStream_t st) {
+    k_pack_panel_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+}
+static void pack_panel_tr(const FarKDims& fk, double* pan, cudaStream_t st) {
+    k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+}
+#else
+constexpr bool kFarkDmma = false;
+template <int NCB, int S>
+__host__ __device__ constexpr int farkd_jz() { return fark_jz<NCB, S>(); }
+static void pack_panel(const FarKDims& fk, double* pan, cudaStream_t st) {
+    k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+}
+static void pack_panel_tr(const FarKDims& fk, double* pan, cudaStream_t st) {
+    k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+}
 #endif
+#ifdef SS_FARK_DMMA
 template <int NCB, int S, int NST, int WR, int WC>
 int launch_farkd(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
     static ss::DevMask configured;
@@ -778,6 +799,12 @@ int launch_farkd(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, do
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
+#else
+template <int NCB, int S, int NST, int WR, int WC>
+int launch_farkd(ss_handle* h, int, cudaStream_t, const FarKDims&, double2*, const double2*) {
+    return ss::set_err(h, SS_EARG, "DMMA far kernel not built (SS_FARK_DMMA)");
+}
+#endif
 template <int NCB, int S, int NST = kFarkStages>
 int launch_fark(ss_handle* h, int grid, cudaStream_t st, const FarKDims& fk, double2* Z, const double2* W) {
     static ss::DevMask configured;  // devices configured
@@ -847,14 +874,17 @@ static int launch_farkm(ss_handle* h, int grid, cudaStream_t st, const FarKDims&
     if (!configured.has(h)) {
         SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)farkm_smem_bytes<4>()));
+#ifdef SS_FARK_DMMA
         SS_CUDA_TRY(h, cudaFuncSetAttribute(k_farkmd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)farkm_smem_bytes<4>()));
+#endif
         configured.set(h);
     }
-    if (kFarkDmma)
-        k_farkmd<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
-    else
-        k_farkm<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
+#ifdef SS_FARK_DMMA
+    k_farkmd<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
+#else
+    k_farkm<4><<<grid, 32 * 9, farkm_smem_bytes<4>(), st>>>(fk, Z, W);
+#endif
     SS_LAUNCH_CHECK(h);
     return SS_OK;
 }
@@ -1172,10 +1202,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
                 cudaEvent_t ev = ss::timing_begin(h, st);
-                if (dmma)
-                    k_pack_panel_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
-                else
-                    k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                pack_panel(fk, B.pan, st);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
                 const int S = m == 10 ? (dmma ? 4 : 8) : S20;
@@ -1529,10 +1556,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 fk.ntiles = (rows + kFkTile - 1) / kFkTile;
                 fk.pan = B.pan;
                 cudaEvent_t ev = ss::timing_begin(h, st);
-                if (kFarkDmma)
-                    k_pack_panel_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
-                else
-                    k_pack_panel<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, B.pan);
+                pack_panel(fk, B.pan, st);
                 SS_LAUNCH_CHECK(h);
                 ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
                 const int64_t units = (int64_t)fk.ntiles * ((sb + wsh.S - 1) / wsh.S);
@@ -2448,10 +2472,7 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
     if (!S_) return ss::set_err(h, SS_EARG, "transposed composite: unsupported width");
     fk.nz = (M + fk.jz - 1) / fk.jz;
     cudaEvent_t ev = ss::timing_begin(h, st);
-    if (kFarkDmma)
-        k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
-    else
-        k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    pack_panel_tr(fk, pan, st);
     SS_LAUNCH_CHECK(h);
     ss::timing_end(h, st, ev, ss::PH_OUTER_GEMM);
     const int64_t units = (int64_t)fk.ntiles * ((sb + S_ - 1) / S_);
@@ -2523,10 +2544,7 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
     cudaEvent_t ev = ss::timing_begin(h, st);
     // one packed panel for both passes (k_farkmd and k_farkd read the
     // fragment order; -DSS_FARK_DFMA: k_farkm / k_fark the lane-interleaved one)
-    if (kFarkDmma)
-        k_pack_panel_tr_d<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
-    else
-        k_pack_panel_tr<<<fk.ntiles * fk.nk, 256, 0, st>>>(fk, pan);
+    pack_panel_tr(fk, pan, st);
     SS_LAUNCH_CHECK(h);
     k_tr_wprep<<<dim3((unsigned)((rows + 255) / 256), (unsigned)sb), 256, 0, st>>>(m, LDS, S, rlo, r0, K, W,
                                                                                    wstride);

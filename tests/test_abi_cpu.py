@@ -35,6 +35,26 @@ def test_library_is_sm100a():
     assert b"sm_100a" in data or b"sm_100" in data
 
 
+def test_dmma_only_in_the_reduction():
+    """north_star: FP64 tensor-core DMMA only in the reduction's trailing
+    updates.  Every kernel of the product library whose SASS holds a DMMA
+    must be the reduction GEMM (ssr::k_dmma); the sweep is DFMA."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    with_dmma, fn = set(), None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+        elif "DMMA" in line and fn:
+            with_dmma.add(fn)
+    assert with_dmma, "the reduction GEMM should use DMMA"
+    assert all("k_dmma" in f for f in with_dmma), sorted(f for f in with_dmma if "k_dmma" not in f)
+
+
 def test_version():
     assert _lib.load().ss_version() == 100
 
