@@ -40,7 +40,10 @@ namespace ssd {
 
 constexpr int kFkTile = 64;  // rows per unit
 constexpr int kFarkUnroll = 4;  // panel columns unrolled in the main loop (2 / 8: same / -0.6%)
-constexpr int kFkKC = 32;    // panel columns per chunk
+#ifndef SS_FKKC
+#define SS_FKKC 32  // comparison builds vary it (tools/build_variant.sh)
+#endif
+constexpr int kFkKC = SS_FKKC;    // panel columns per chunk
 
 struct FarKDims {
     int m, ptop, ident_top;
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(32 * (1 + NCB * S), 1)
 // shifts); consumer warp w owns shifts 10 w .. 10 w + 9 of the group (lane
 // q = lane & 1 five of them) with the same 4 x 5 register tile and the same
 // packed panel as k_fark.  Per shift the composite is W12 (K entries) and the
-// scalar W22, stored group-major [group][row][80] (k_wcomp1) so a KC-row chunk
+// scalar W22, stored group-major [group][row][80] (k_wsuffix1) so a KC-row chunk
 // of the group's W is ONE contiguous bulk copy.  W22 is diagonal across the
 // unit's columns: z <- z W22 + Pan W12 is applied in the epilogue from the Z
 // values read there (no Z chunks through the ring).

@@ -751,10 +751,17 @@ struct PartBufs {
 // (transfer function); SS_FAR_PASSES=1 keeps the 64 / 128-column pass
 // kernels (k_far / k_far4) for comparison.
 constexpr int kFarkStages = 4;
+// m = 20 unit shape: shifts per unit x ring stages (comparison builds vary them)
+#ifndef SS_S20
+#define SS_S20 4
+#endif
+#ifndef SS_N20
+#define SS_N20 kFarkStages
+#endif
 static bool fark_supported(ss_handle* h, int m, int mode) {
     if (mode != 0 || getenv("SS_FAR_PASSES")) return false;
     if (m == 10) return fark_smem_bytes<1, 8, kFarkStages>() <= h->smem_optin;
-    if (m == 20) return fark_smem_bytes<2, 4, kFarkStages>() <= h->smem_optin;
+    if (m == 20) return fark_smem_bytes<2, SS_S20, SS_N20>() <= h->smem_optin;
     return false;
 }
 static size_t fark_pan_bytes(int n, int ptop) {
@@ -1026,26 +1033,39 @@ __global__ void __launch_bounds__(kWsT) k_wsuffix(WsufArgs a) {
     }
 }
 
-// m = 1: the same fold elementwise in the group layout (row-major across the
-// 80 shifts of a group: coalesced), one thread per (row, shift).
-__global__ void __launch_bounds__(256) k_wcomp1(int K, int x, int nb, bool first, int sb, int64_t pstride,
-                                                const double2* __restrict__ P, int64_t gstride,
-                                                double2* __restrict__ W) {
+// m = 1: the composite from all its windows' P at once (scalars: W12 rows of
+// window b = P12_b times the suffix product of the later windows' P22, W22 =
+// the product of all of them), in the group layout [group][row][80]
+// (row-major across a group's shifts: coalesced), one thread per (row,
+// shift).  Windows: rows [x_b, x_b + nb_b) of the composite, P of window b,
+// shift l at P + b slab + l (nb_b + 1).
+struct Wsuf1Args {
+    int g, K, sb;
+    int x[kWcWin], nb[kWcWin];
+    const double2* P;
+    int64_t slab, gstride;
+    double2* W;
+};
+__global__ void __launch_bounds__(256) k_wsuffix1(Wsuf1Args a) {
     constexpr int S = kFkmShifts;
-    const int ngroups = (sb + S - 1) / S;
-    const int r_lo = first ? x : x;  // rows [x, K + 1)
-    const int64_t per = (int64_t)(K + 1 - r_lo) * S;
+    const int ngroups = (a.sb + S - 1) / S;
+    const int64_t per = (int64_t)(a.K + 1) * S;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per * ngroups;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int grp = (int)(e / per);
         const int64_t rem = e - grp * per;
-        const int row = r_lo + (int)(rem / S), c = (int)(rem % S);
-        const int l = min(grp * S + c, sb - 1);
-        const double2* Pl = P + (int64_t)l * pstride;
-        double2* w = W + grp * gstride + (int64_t)row * S + c;
-        if (row < x + nb) *w = Pl[row - x];
-        else if (first) *w = Pl[nb];  // row K: W22 <- P22
-        else *w = cmul(*w, Pl[nb]);
+        const int row = (int)(rem / S), c = (int)(rem % S);
+        const int l = min(grp * S + c, a.sb - 1);
+        double2 v = make_double2(1.0, 0.0);
+        int bw = -1;  // the window holding this row (W12), -1: the W22 row
+        if (row < a.K)
+            for (int b = 0; b < a.g; ++b)
+                if (row >= a.x[b] && row < a.x[b] + a.nb[b]) bw = b;
+        // suffix product of the P22 of the windows after bw (all of them for W22)
+        for (int b = bw + 1; b < a.g; ++b)
+            v = cmul(v, a.P[b * a.slab + (int64_t)l * (a.nb[b] + 1) + a.nb[b]]);
+        if (bw >= 0) v = cmul(a.P[bw * a.slab + (int64_t)l * (a.nb[bw] + 1) + (row - a.x[bw])], v);
+        a.W[grp * a.gstride + (int64_t)row * S + c] = v;
     }
 }
 
@@ -1194,7 +1214,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 // m = 20: 4 shifts x 2 column blocks per unit, 4 stages (measured
                 // at config 4 against 3 x 4 / 5 x 3 / 6 x 2: 4.01k / 4.31k / 4.70k
                 // vs 4.82k shifts/s)
-                constexpr int S20 = 4, N20 = kFarkStages;
+                constexpr int S20 = SS_S20, N20 = SS_N20;
                 const bool dmma = kFarkDmma;
                 fk.jz = m == 10 ? (dmma ? farkd_jz<1, 4>() : fark_jz<1, 8>())
                                 : (dmma ? farkd_jz<2, S20>() : fark_jz<2, S20>());
@@ -1374,7 +1394,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
     }
     if (wc) {
         // ---- window composites (wide windows: k_rq_big + near k_update +
-        // k_wsuffix per composite (m = 1: k_wcomp1 per window), one k_fark per
+        // k_wsuffix per composite (m = 1: k_wsuffix1), one k_fark per
         // composite) ----
         account_ref_flops(h, sb, n, m, ptop, nb0);  // the reference's stack
         WcShape wsh;
@@ -1392,7 +1412,10 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             // m = 1: 6 windows per composite (config 3: 8 / 6 / 4 / 2 windows
             // measured 1.36M / 1.42M / 1.40M / 1.29M shifts/s -- the near rows
             // grow with the square of the window count)
-            const int gmax = m == 1 ? 6 : kWcWin;
+#ifndef SS_WC_M1
+#define SS_WC_M1 6  // comparison builds vary it
+#endif
+            const int gmax = m == 1 ? SS_WC_M1 : kWcWin;
             for (int kk = k; kk >= m + 1 && g < gmax; ++g) {
                 kw[g] = kk;
                 nbw[g] = std::min(nb0, kk - m);
@@ -1408,7 +1431,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
             int xw[kWcWin];
             for (int b = 0; b < g; ++b) {
                 const int nb = nbw[b], r0 = ptop + kw[b] - nb, cw = kw[b] - m - nb, nc = nb + m;
-                double2* const Pw = m == 1 ? B.P : B.P + b * pslab;
+                double2* const Pw = B.P + b * pslab;
                 xw[b] = cw - c0;
                 int rc = feed_wait(h, feed, st);  // this window's panel columns
                 if (rc) return rc;
@@ -1427,7 +1450,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                 rd.shifts = d.shifts;
                 rd.LDZ = LDZ;
                 if (m == 1)
-                    k_rq_m1<<<(sb + 4 * kM1Warps - 1) / (4 * kM1Warps), 32 * kM1Warps, 0, st>>>(rd, B.Z, B.P);
+                    k_rq_m1<<<(sb + 4 * kM1Warps - 1) / (4 * kM1Warps), 32 * kM1Warps, 0, st>>>(rd, B.Z, Pw);
                 else
                     k_rq_big<<<sb, kRqBigThreads, rq_big_smem_bytes(nb, m), st>>>(rd, B.Z, Pw);
                 SS_LAUNCH_CHECK(h);
@@ -1469,7 +1492,7 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                     const int64_t units = (int64_t)((rows + f.tile() - 1) / f.tile()) * ((sb + 9) / 10);
                     const int grid = (int)std::min<int64_t>(units, h->num_sms);
                     ev = ss::timing_begin(h, st);
-                    rc = launch_far(h, f, grid, far_smem_bytes(nb, 10, f.tile(), f.NST), st, u, B.Z, B.P);
+                    rc = launch_far(h, f, grid, far_smem_bytes(nb, 10, f.tile(), f.NST), st, u, B.Z, Pw);
                     if (rc) return rc;
                     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * (double)sb,
                                    8.0 * rows * (double)sb * nb, 4.0 * (double)rows * nb * sb);
@@ -1514,16 +1537,27 @@ int enqueue_part(ss_handle* h, const SweepArgs& a, int64_t lo, int sb, PartBufs 
                     ss::timing_end(h, st, ev, ss::PH_UPDATE, 8.0 * rows * m * m * (double)sb,
                                    8.0 * rows * (double)sb * m * nb, 4.0 * m * (double)rows * nb * sb);
                 }
-                if (m == 1) {
-                    ev = ss::timing_begin(h, st);
-                    const int64_t tot = (int64_t)(K + 1 - (cw - c0)) * kFkmShifts * ((sb + kFkmShifts - 1) / kFkmShifts);
-                    const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 8 * (int64_t)h->num_sms);
-                    k_wcomp1<<<blocks, 256, 0, st>>>(K, cw - c0, nb, b == 0, sb, (int64_t)nc, B.P, wstride, B.W);
-                    SS_LAUNCH_CHECK(h);
-                    ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
-                }
             }
-            if (m > 1) {
+            if (m == 1) {
+                cudaEvent_t ev = ss::timing_begin(h, st);
+                Wsuf1Args wa;
+                wa.g = g;
+                wa.K = K;
+                wa.sb = sb;
+                for (int b = 0; b < g; ++b) {
+                    wa.x[b] = xw[b];
+                    wa.nb[b] = nbw[b];
+                }
+                wa.P = B.P;
+                wa.slab = pslab;
+                wa.gstride = wstride;
+                wa.W = B.W;
+                const int64_t tot = (int64_t)(K + 1) * kFkmShifts * ((sb + kFkmShifts - 1) / kFkmShifts);
+                const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 8 * (int64_t)h->num_sms);
+                k_wsuffix1<<<blocks, 256, 0, st>>>(wa);
+                SS_LAUNCH_CHECK(h);
+                ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
+            } else {
                 cudaEvent_t ev = ss::timing_begin(h, st);
                 int rc = ss::wsuffix(h, st, sb, g, xw, nbw, m, m, K, B.P, pslab, B.W, wstride);
                 if (rc) return rc;
@@ -2135,7 +2169,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     const int ncmax = nb0 + m;
     const int64_t wc_stride = wc ? (int64_t)(kWcWin * nb0 + m) * m : 0;  // composite W per shift
     const size_t wc_slack = m == 1 ? (size_t)kFkmShifts * wc_stride * 16 : 0;  // last group of 80 shifts
-    const int wc_slabs = wc && m > 1 ? kWcWin : 1;  // window P kept per composite (k_wsuffix)
+    const int wc_slabs = wc ? kWcWin : 1;  // window P kept per composite (k_wsuffix / k_wsuffix1)
     const int64_t pst = two_level ? (int64_t)(a.group * kBlkNB + m) * m : (int64_t)wc_slabs * ncmax * m + wc_stride;
     const size_t per_shift = (size_t)LDZ * m * 16 + (size_t)pst * 16 + 64 +
                              (size_t)(xh_stride + w22h_stride + y_stride) * 16;
