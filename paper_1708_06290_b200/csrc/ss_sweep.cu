@@ -2195,8 +2195,11 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     double2* W22h0 = Xh0 + (size_t)sb_max * xh_stride;
     double2* Y0 = W22h0 + (size_t)sb_max * w22h_stride;
     double* pan = nullptr;  // k_fark's packed panel, after the 1 MB scratch of fro2_trace
+    // (wide-window composites run two halves of a batch on two streams: one
+    // packed panel per half)
+    const size_t pan_elems = fark_pan_bytes(n, ptop) / 8;
     if ((two_level && fark_supported(h, m, mode_far)) || wc) {
-        int rc = ss::ensure_ws(h, (1u << 20) + fark_pan_bytes(n, ptop), 1);
+        int rc = ss::ensure_ws(h, (1u << 20) + (wc ? 2 : 1) * pan_elems * 8, 1);
         if (rc) return rc;
         pan = reinterpret_cast<double*>(static_cast<char*>(h->ws2) + (1u << 20));
     }
@@ -2209,7 +2212,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
     const bool far_m20 = !two_level && tile.exact && tile.G == 2 && tile.C == 5 &&
                          (m + tile.G * tile.C - 1) / (tile.G * tile.C) == 2;
     const bool far_m1 = !two_level && m == 1;
-    int NS = (two_level || wc || far_m20 || far_m1) ? 1 : 2;
+    int NS = (two_level || far_m20 || far_m1) ? 1 : 2;
     if (sb_max < 64 || feed.on) NS = 1;
     cudaStream_t streams[2] = {st, st};
     if (NS == 2) {
@@ -2227,7 +2230,7 @@ int run_sweep(ss_handle* h, const SweepArgs& a_in, cudaStream_t st) {
             PartBufs B;
             B.Z = Z0 + (size_t)off * m * LDZ;
             B.P = P0 + (size_t)off * pst;
-            B.pan = pan;
+            B.pan = pan && wc ? pan + (size_t)p * pan_elems : pan;
             if (wc) B.W = B.P + (size_t)wc_slabs * cnt * ncmax * m;  // after the parts' window P
             if (a.defer) {
                 B.Xh = Xh0 + (size_t)off * xh_stride;
