@@ -2266,27 +2266,33 @@ namespace ss {
 // The far pass's -I rows [rlo, r0) (rlo >= n): their panel row has at most
 // one entry (-1 in column i - n), so instead of the dense K-streamed pass:
 //   z_i <- z_i W22 - [0 <= i - dlo < K] W12[i - dlo]        (dlo = n + c0)
-// One CTA per (64-row tile, shift): the rows' M state columns and W22 in
-// shared memory; a thread owns 4 rows x 4 columns (rows rg + 16 r, columns
-// cg + 16 c) in registers: 8 shared loads per 16 complex FMAs.
-constexpr int kTlRows = 64;
+// One CTA per (row tile, shift): the rows' mc state columns and W22 in
+// shared memory; a thread owns 4 rows x 4 columns in registers (rows rg +
+// RG r, columns cg + CG c, CG = ceil(mc / 4) column groups, RG = 256 / CG
+// row groups: the tile is 4 RG rows, so no thread slot is spent on columns
+// past mc): 8 shared loads per 16 complex FMAs.
+__host__ __device__ inline int tl_cg(int mc) { return (mc + 3) / 4; }
+__host__ __device__ inline int tl_rows(int mc) { return 4 * (256 / tl_cg(mc)); }
+__host__ __device__ inline size_t tl_smem(int M, int mc) { return (size_t)(M * M + mc * tl_rows(mc)) * 16; }
 __global__ void __launch_bounds__(256) k_tr_lower(int M, int mc, int64_t LDS, double2* __restrict__ S, int rlo,
                                                   int r0, int dlo, int K, const double2* __restrict__ W,
                                                   int64_t wstride) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const int CG = tl_cg(mc), RG = 256 / CG, TR = 4 * RG;
     double2* W22 = reinterpret_cast<double2*>(smem);  // M x M
-    double2* Zs = W22 + M * M;                         // [M][kTlRows]
+    double2* Zs = W22 + M * M;                         // [mc][TR]
     const int l = blockIdx.y, t = threadIdx.x;
-    const int i0 = rlo + blockIdx.x * kTlRows;
+    const int i0 = rlo + blockIdx.x * TR;
     const double2* Wl = W + (int64_t)l * wstride;
     double2* Sl = S + (int64_t)l * M * LDS;
     for (int e = t; e < M * M; e += 256) W22[e] = Wl[(int64_t)K * M + e];
-    for (int e = t; e < mc * kTlRows; e += 256) {
-        const int j = e / kTlRows, r = e - j * kTlRows;
+    for (int e = t; e < mc * TR; e += 256) {
+        const int j = e / TR, r = e - j * TR;
         Zs[e] = i0 + r < r0 ? Sl[(int64_t)j * LDS + i0 + r] : cz();
     }
     __syncthreads();
-    const int rg = t & 15, cg = t >> 4;
+    if (t >= RG * CG) return;
+    const int rg = t % RG, cg = t / RG;
     double2 acc[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -2295,9 +2301,9 @@ __global__ void __launch_bounds__(256) k_tr_lower(int M, int mc, int64_t LDS, do
     for (int j = 0; j < mc; ++j) {  // padding columns (>= mc) are zero
         double2 z[4], w[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) z[r] = Zs[j * kTlRows + rg + 16 * r];
+        for (int r = 0; r < 4; ++r) z[r] = Zs[j * TR + rg + RG * r];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) w[c] = cg + 16 * c < mc ? W22[j * M + cg + 16 * c] : cz();
+        for (int c = 0; c < 4; ++c) w[c] = cg + CG * c < mc ? W22[j * M + cg + CG * c] : cz();
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -2305,12 +2311,12 @@ __global__ void __launch_bounds__(256) k_tr_lower(int M, int mc, int64_t LDS, do
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int i = i0 + rg + 16 * r;
+        const int i = i0 + rg + RG * r;
         if (i >= r0) continue;
         const int dd = i - dlo;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const int col = cg + 16 * c;
+            const int col = cg + CG * c;
             if (col >= mc) continue;
             double2 v = acc[r][c];
             if (dd >= 0 && dd < K) v = csub(v, Wl[(int64_t)dd * M + col]);
@@ -2466,8 +2472,8 @@ int tr_far(ss_handle* h, cudaStream_t st, int n, int m, int M, const double* A, 
         }
         const int lo = std::max(rlo, n), nr = r0_all - lo;
         cudaEvent_t ev = ss::timing_begin(h, st);
-        k_tr_lower<<<dim3((unsigned)((nr + kTlRows - 1) / kTlRows), (unsigned)sb), 256,
-                     (size_t)(M * M + M * kTlRows) * 16, st>>>(M, m + 1, LDS, S, lo, r0_all, n + c0, K, W, wstride);
+        k_tr_lower<<<dim3((unsigned)((nr + tl_rows(m + 1) - 1) / tl_rows(m + 1)), (unsigned)sb), 256,
+                     tl_smem(M, m + 1), st>>>(M, m + 1, LDS, S, lo, r0_all, n + c0, K, W, wstride);
         SS_LAUNCH_CHECK(h);
         ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
     }
@@ -2541,8 +2547,8 @@ int tr_far_split(ss_handle* h, cudaStream_t st, int n, int m, const double* A, i
         }
         const int lo = std::max(rlo, n), nr = r0_all - lo;
         cudaEvent_t ev = ss::timing_begin(h, st);
-        k_tr_lower<<<dim3((unsigned)((nr + kTlRows - 1) / kTlRows), (unsigned)sb), 256,
-                     (size_t)(mp * mp + mp * kTlRows) * 16, st>>>(mp, mp, LDS, S, lo, r0_all, n + c0, K, W, wstride);
+        k_tr_lower<<<dim3((unsigned)((nr + tl_rows(mp) - 1) / tl_rows(mp)), (unsigned)sb), 256,
+                     tl_smem(mp, mp), st>>>(mp, mp, LDS, S, lo, r0_all, n + c0, K, W, wstride);
         SS_LAUNCH_CHECK(h);
         ss::timing_end(h, st, ev, ss::PH_BATCHED_GEMM);
     }
