@@ -640,6 +640,117 @@ __global__ void __launch_bounds__(256) k_ttail(TDims d, double2* __restrict__ S,
     if (tid == 0) d.fail[l] = s_fail;
 }
 
+// The same tail for m <= 32 without m^2 / 2 passes over the 2n-row columns:
+// the rotations and the substitution values depend only on the m x m top
+// block (rows [n - m, n)), so warp 0 runs the whole tail on that block in
+// shared memory (lane = row; same operations, same order as k_ttail) and
+// records every rotation and every w; then each thread replays them on its
+// rows of [n, 2n) with the row's m state values in a shared-memory slice
+// (x = w[n:] is the only output; the state is not written back).
+constexpr int kTtMax = 32;
+__host__ __device__ inline size_t ttail_s_smem(int m) {
+    return (size_t)m * 256 * 16 + (size_t)kTtMax * kTtMax * 16;
+}
+__global__ void __launch_bounds__(256) k_ttail_s(TDims d, const double2* __restrict__ S, double2* __restrict__ X,
+                                                 int64_t ldx) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NR = kTtMax * (kTtMax - 1) / 2;
+    __shared__ double rc[NR];
+    __shared__ double2 rs[NR], wk[kTtMax], wt[kTtMax];
+    __shared__ int s_fail;
+    double2* xs = reinterpret_cast<double2*>(smem);  // [m][256]: thread t's row values at j * 256 + t
+    double2* Ts = xs + (size_t)d.m * 256;           // top block [column][kTtMax]
+    const int l = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const int n = d.n, m = d.m;
+    const double2* Sl = S + (int64_t)l * d.ms * d.LDS;
+    const double2* wv = Sl + (int64_t)m * d.LDS;
+    if (tid < 32) {
+        int fail = d.fail[l];
+        const double tol = d.tol[l];
+        if (lane < m) {
+            for (int j = 0; j < m; ++j) Ts[j * kTtMax + lane] = Sl[(int64_t)j * d.LDS + n - m + lane];
+            wt[lane] = wv[n - m + lane];
+        }
+        __syncwarp();
+        if (fail < 0) {
+            int idx = 0;
+            for (int kk = 1; kk < m && fail < 0; ++kk) {
+                const int rl = kk - 1;
+                double2* hc = Ts + (kk - 1) * kTtMax;
+                for (int c = kk; c < m; ++c, ++idx) {
+                    double2* tc = Ts + c * kTtMax;
+                    double cc;
+                    double2 ss, rv;
+                    givens(hc[rl], tc[rl], cc, ss, rv);
+                    __syncwarp();
+                    if (lane < m) {
+                        double2 hh = hc[lane], tt = tc[lane];
+                        rot_apply(cc, ss, hh, tt);
+                        hc[lane] = hh;
+                        tc[lane] = tt;
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc[rl] = cz();
+                        hc[rl] = rv;
+                        rc[idx] = cc;
+                        rs[idx] = ss;
+                    }
+                    __syncwarp();
+                }
+                const double2 piv = hc[rl];
+                if (hypot(piv.x, piv.y) <= tol) {
+                    fail = n - m + rl;
+                    break;
+                }
+                const double2 w = cdiv(wt[rl], piv);
+                __syncwarp();
+                if (lane == 0) {
+                    wt[rl] = w;
+                    wk[rl] = w;
+                }
+                if (lane > rl && lane < m) wt[lane] = csub(wt[lane], cmul(hc[lane], w));
+                __syncwarp();
+            }
+            if (fail < 0) {
+                const double2 piv = Ts[(m - 1) * kTtMax + m - 1];
+                if (hypot(piv.x, piv.y) <= tol) {
+                    fail = n - 1;
+                } else if (lane == 0) {
+                    wk[m - 1] = cdiv(wt[m - 1], piv);
+                }
+            }
+        }
+        if (lane == 0) s_fail = fail;
+    }
+    __syncthreads();
+    const int fail = s_fail;
+    const double qn = __longlong_as_double(0x7ff8000000000000ULL);
+    double2* Xl = X + (int64_t)l * ldx;
+    if (fail >= 0) {
+        for (int i = tid; i < n; i += blockDim.x) Xl[i] = make_double2(qn, qn);
+        if (tid == 0) d.fail[l] = fail;
+        return;
+    }
+    for (int i = n + tid; i < 2 * n; i += blockDim.x) {
+        for (int j = 0; j < m; ++j) xs[j * 256 + tid] = Sl[(int64_t)j * d.LDS + i];
+        double2 w = wv[i];
+        int idx = 0;
+        for (int kk = 1; kk < m; ++kk) {
+            double2 hh = xs[(kk - 1) * 256 + tid];
+            for (int c = kk; c < m; ++c, ++idx) {
+                double2 tt = xs[c * 256 + tid];
+                rot_apply(rc[idx], rs[idx], hh, tt);
+                xs[c * 256 + tid] = tt;
+            }
+            w = csub(w, cmul(hh, wk[kk - 1]));
+        }
+        w = csub(w, cmul(xs[(m - 1) * 256 + tid], wk[m - 1]));
+        Xl[i - n] = w;
+    }
+    if (tid == 0) d.fail[l] = -1;
+}
+
 __global__ void k_tol(int sb, const double2* __restrict__ shifts, const double* __restrict__ scal,
                       int n, double rtol, double* __restrict__ tol) {
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
@@ -920,7 +1031,16 @@ extern "C" int ss_solve_transposed(ss_handle* h, int n, int m, const double* Aha
             k0 += ls.nb;
         }
         cudaEvent_t ev = ss::timing_begin(h, st);
-        k_ttail<<<sb, 256, 0, st>>>(d, Sb, (double2*)X + lo * ldx, ldx);
+        if (m <= kTtMax && ttail_s_smem(m) + 8192 <= h->smem_optin) {
+            static ss::DevMask configured;
+            if (!configured.has(h)) {
+                SS_CUDA_TRY(h, allow_smem(h, k_ttail_s));
+                configured.set(h);
+            }
+            k_ttail_s<<<sb, 256, ttail_s_smem(m), st>>>(d, Sb, (double2*)X + lo * ldx, ldx);
+        } else {
+            k_ttail<<<sb, 256, 0, st>>>(d, Sb, (double2*)X + lo * ldx, ldx);
+        }
         SS_LAUNCH_CHECK(h);
         ss::timing_end(h, st, ev, ss::PH_TAIL);
     }
